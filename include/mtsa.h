@@ -1,0 +1,85 @@
+/* mtsa.h — C ABI of the B200-native MTraining hot path (arXiv 2510.18830).
+ *
+ * What this library computes (citations are PAPER.md lines, "P:n", of
+ * /root/reference/PAPER.md at the time of writing):
+ *   - the vertical-slash (VS) sparse index of Alg. 1: window
+ *     attention of the last 64 queries, online top-p budgets for
+ *     vertical columns and 64x64-pooled slash offsets (P:228-229,
+ *     P:249), sparseformat;
+ *   - block-sparse attention forward/backward over that index (Eq. 1
+ *     P:111, Eq. 12), with the merge of partial (O, LSE) across ring
+ *     steps (merge_out_and_lse);
+ *   - the balanced (64-token block-striped) sparse ring, flat and
+ *     hierarchical (Alg. 2), over NCCL send/recv.
+ *
+ * Conventions shared by every entry point:
+ *   - All tensor pointers are CUDA DEVICE pointers owned by the caller, unless a
+ *     parameter says "host".  The library never allocates device memory: calls
+ *     that need scratch take a caller workspace sized by the matching
+ *     *_workspace_bytes() function.
+ *   - All compute calls are asynchronous on the caller's stream.  Argument
+ *     validation happens synchronously before any launch; a validation failure
+ *     launches nothing.  Asynchronous CUDA failures surface as MT_ECUDA on the
+ *     next call that checks (or via cudaStreamSynchronize by the caller).
+ *   - Layouts (token-major, bf16 = IEEE bfloat16):
+ *       Q, O, dO, dQ : [S_loc][Hq][d]      K, V, dK, dV : [S_loc][Hkv][d]
+ *       LSE          : float32 [Hq][S_loc], natural log.
+ *     S_loc = S / W is the rank-local (block-striped) length; W = 1 on one GPU.
+ *   - Supported: d = 128, block = last_q = 64, Hq % Hkv == 0, S % (64 W) == 0.
+ *   - No exceptions, abort() or exit() cross this boundary; functions return
+ *     mt_status, and mt_last_error() gives a thread-local message.
+ */
+#ifndef MTSA_H_
+#define MTSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mt_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  MT_OK = 0,
+  MT_ESHAPE = 1,       /* null pointer / bad dimension */
+  MT_EWINDOW = 2,      /* S < 64 or S % 64 != 0 (window = last 64 queries) */
+  MT_ECONFIG = 3,      /* p_v or p_s outside (0, 1] */
+  MT_ELAYOUT = 4,      /* S % (64 * W) != 0 for the block-striped layout */
+  MT_ECAPACITY = 5,    /* an output buffer is too small */
+  MT_EWORKSPACE = 6,   /* workspace too small */
+  MT_EUNSUPPORTED = 7, /* d != 128, block != 64, non-sm_100 device */
+  MT_ECUDA = 8,        /* CUDA runtime / launch error */
+  MT_ENCCL = 9         /* NCCL error */
+} mt_status;
+
+/* Thread-local description of the last non-MT_OK status returned on this thread. */
+const char* mt_last_error(void);
+
+/* Problem shape.  seq_len is the GLOBAL sequence length S. */
+typedef struct {
+  int64_t seq_len;
+  int32_t n_q_heads;  /* Hq */
+  int32_t n_kv_heads; /* Hkv; q head h uses kv head h / (Hq / Hkv) */
+  int32_t head_dim;   /* d, must be 128 */
+  int32_t block;      /* B = stripe = slash block = window rows, must be 64 */
+} mt_shape;
+
+/* Online top-p targets of Alg. 1 ("p_v, p_s", read as reals in (0, 1]). */
+typedef struct {
+  float p_v;
+  float p_s;
+} mt_vs_params;
+
+/* ------------------------------------------------------------------ tests */
+/* Hardware self-test hook (not part of the attention API): one 128-row tcgen05
+ * MMA configuration on one CTA, see csrc/selftest.cu for the variants.
+ * A, B: bf16 device buffers, D: float32 device buffer [128][N]. */
+mt_status mt_selftest_mma(int variant, const void* A, const void* B, float* D,
+                          mt_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MTSA_H_ */

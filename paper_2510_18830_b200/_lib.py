@@ -1,0 +1,72 @@
+"""ctypes loader for libmtsa.so (the C ABI in include/mtsa.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  There is no fallback — a missing or unloadable library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libmtsa.so"
+
+MT_STATUS = {
+    0: "MT_OK", 1: "MT_ESHAPE", 2: "MT_EWINDOW", 3: "MT_ECONFIG", 4: "MT_ELAYOUT",
+    5: "MT_ECAPACITY", 6: "MT_EWORKSPACE", 7: "MT_EUNSUPPORTED", 8: "MT_ECUDA", 9: "MT_ENCCL",
+}
+
+
+class MTError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{MT_STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = MT_STATUS.get(status, str(status))
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("seq_len", ctypes.c_int64), ("n_q_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("block", ctypes.c_int32)]
+
+
+class VSParams(ctypes.Structure):
+    _fields_ = [("p_v", ctypes.c_float), ("p_s", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (the CUDA path has no fallback)")
+        _lib = ctypes.CDLL(str(LIB_PATH))
+        _lib.mt_last_error.restype = ctypes.c_char_p
+        for name, argtypes in _SIGS.items():
+            fn = getattr(_lib, name)
+            fn.restype = ctypes.c_int
+            fn.argtypes = argtypes
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise MTError(status, lib().mt_last_error().decode(errors="replace"))
+
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+I64 = ctypes.c_int64
+SZ = ctypes.c_size_t
+
+_SIGS: dict[str, list] = {
+    "mt_selftest_mma": [I, P, P, P, P],
+}
+
+
+def declared_symbols() -> list[str]:
+    return ["mt_last_error", *_SIGS.keys()]

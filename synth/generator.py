@@ -1,0 +1,188 @@
+"""Synthetic VS-structured Q/K/V (DESIGN.md §3 "input recipe").
+
+Grounded in Theorem 3.1: after RoPE the expected score
+E[z_{n,m}] depends only on n - m, which makes slash lines; outliers in the
+key distribution make vertical lines.  So:
+
+  pre-RoPE  q_{n,h} = a * mu_q(h) + N(0, I) + 0.5 * b * u(g)
+            k_{m,g} = a * mu_k(g) + N(0, I) + [m in sinks] * b * u(g)
+  mu_k(g)  : random unit vector on the 16 highest-frequency RoPE pairs
+  mu_q(h)  : normalize(mu_k(g(h)) + rho * xi_h), xi_h on the same pairs
+  u(g)     : random unit vector on the 4 lowest-frequency pairs
+  sinks    : tokens 0..3 plus 16 random tokens (per kv head)
+  RoPE     : half-split pairs (i, i + d/2), theta_i = base^(-2i/d), base = 1e6
+  V, dO    : N(0, I)
+
+Returned tensors are bf16 bit patterns (numpy uint16), token-major
+[S][H][d].  Values with |x| < 2^-60 are flushed to +0 so every bf16 x bf16
+product is an exact normal fp32 number (reading R11, VS-IDX I1).
+Generation is chunked over tokens and seeded per chunk, so the same
+(seed, shape) gives the same bytes on any host.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+CHUNK = 8192  # tokens per independently seeded chunk
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    seq_len: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int = 128
+    world: tuple = (1,)
+    note: str = ""
+
+
+# BASELINE.json configs (index = position in its "configs" list).
+CONFIGS = {
+    "C1": Workload("C1", 4096, 8, 1, note="1 kv group, seq 4K, 1 GPU"),
+    "C2": Workload("C2", 65536, 16, 2, note="Qwen2.5-3B-shaped, seq 64K, 1 GPU"),
+    "C3": Workload("C3", 131072, 16, 2, world=(2, 4, 8), note="striped ring, seq 128K"),
+    "C4": Workload("C4", 524288, 16, 2, world=(8,), note="striped ring, seq 512K, 8 GPUs"),
+    "C5": Workload("C5", 524288, 16, 2, world=(8,), note="hierarchical 2x4 ring, 512K-1M"),
+}
+
+# Generator strength `a` per sequence length, calibrated so the VS index at
+# p_v = p_s = 0.9 selects about 5% of the causal area ("sparsity 0.95").
+# See DESIGN.md §3 for the calibration run; realised density is always reported.
+DEFAULT_A = {4096: 10.0, 65536: 16.0, 131072: 16.0, 524288: 18.0, 1048576: 18.0}
+DEFAULT_B = 12.0
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16, returned as uint16 bit patterns."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    bits = u.astype(np.uint16)
+    # flush |x| < 2^-60 (bf16 exponent field < 127 - 60) to +0
+    tiny = ((bits >> 7) & 0xFF) < (127 - 60)
+    bits[tiny] = 0
+    return bits
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def _rope_tables(pos: np.ndarray, d: int, base: float):
+    half = d // 2
+    inv = base ** (-2.0 * np.arange(half, dtype=np.float64) / d)
+    ang = pos[:, None].astype(np.float64) * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def _apply_rope(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
+    # x: [T][H][d]; cos/sin: [T][d/2]
+    half = x.shape[-1] // 2
+    x0, x1 = x[..., :half], x[..., half:]
+    c, s = cos[:, None, :], sin[:, None, :]
+    return np.concatenate([x0 * c - x1 * s, x0 * s + x1 * c], axis=-1)
+
+
+def _head_vectors(seed: int, Hq: int, Hkv: int, d: int, rho: float):
+    rng = np.random.default_rng([seed, 0xABC])
+    half = d // 2
+    hi = np.r_[np.arange(16), half + np.arange(16)]            # 16 highest-frequency pairs
+    lo = np.r_[np.arange(half - 4, half), d - 4 + np.arange(4)]  # 4 lowest-frequency pairs
+    mu_k = np.zeros((Hkv, d), np.float64)
+    u = np.zeros((Hkv, d), np.float64)
+    for g in range(Hkv):
+        v = rng.standard_normal(hi.size)
+        mu_k[g, hi] = v / np.linalg.norm(v)
+        w = rng.standard_normal(lo.size)
+        u[g, lo] = w / np.linalg.norm(w)
+    mu_q = np.zeros((Hq, d), np.float64)
+    grp = Hq // Hkv
+    for h in range(Hq):
+        xi = np.zeros(d)
+        xi[hi] = rng.standard_normal(hi.size)
+        xi /= np.linalg.norm(xi)
+        v = mu_k[h // grp] + rho * xi
+        mu_q[h] = v / np.linalg.norm(v)
+    return mu_q.astype(np.float32), mu_k.astype(np.float32), u.astype(np.float32)
+
+
+def _sinks(seed: int, S: int, Hkv: int, n_random: int = 16):
+    rng = np.random.default_rng([seed, 0x51A])
+    out = []
+    for _ in range(Hkv):
+        extra = rng.choice(np.arange(4, S), size=min(n_random, max(S - 4, 0)), replace=False)
+        out.append(np.unique(np.r_[np.arange(min(4, S)), extra]))
+    return out
+
+
+def make_qkv(S: int, Hq: int, Hkv: int, d: int = 128, seed: int = 0, a: float | None = None,
+             b: float = DEFAULT_B, rho: float = 0.35, rope_base: float = 1e6):
+    """Return (q, k, v) bf16 bit arrays [S][Hq|Hkv][d] (uint16)."""
+    if a is None:
+        a = DEFAULT_A.get(S, 16.0)
+    mu_q, mu_k, u = _head_vectors(seed, Hq, Hkv, d, rho)
+    sinks = _sinks(seed, S, Hkv)
+    grp = Hq // Hkv
+    q = np.empty((S, Hq, d), np.uint16)
+    k = np.empty((S, Hkv, d), np.uint16)
+    v = np.empty((S, Hkv, d), np.uint16)
+    for c0 in range(0, S, CHUNK):
+        c1 = min(S, c0 + CHUNK)
+        T = c1 - c0
+        rng = np.random.default_rng([seed, 0x5EED, c0 // CHUNK])
+        qn = rng.standard_normal((T, Hq, d), dtype=np.float32)
+        kn = rng.standard_normal((T, Hkv, d), dtype=np.float32)
+        vn = rng.standard_normal((T, Hkv, d), dtype=np.float32)
+        qx = a * mu_q[None] + qn + 0.5 * b * u[np.arange(Hq) // grp][None]
+        kx = a * mu_k[None] + kn
+        for g in range(Hkv):
+            sk = sinks[g]
+            sk = sk[(sk >= c0) & (sk < c1)] - c0
+            kx[sk, g, :] += b * u[g]
+        cos, sin = _rope_tables(np.arange(c0, c1), d, rope_base)
+        q[c0:c1] = f32_to_bf16_bits(_apply_rope(qx, cos, sin))
+        k[c0:c1] = f32_to_bf16_bits(_apply_rope(kx, cos, sin))
+        v[c0:c1] = f32_to_bf16_bits(vn)
+    return q, k, v
+
+
+def make_grad_out(S: int, Hq: int, d: int = 128, seed: int = 0) -> np.ndarray:
+    """dO ~ N(0, I), bf16 bits [S][Hq][d]."""
+    out = np.empty((S, Hq, d), np.uint16)
+    for c0 in range(0, S, CHUNK):
+        c1 = min(S, c0 + CHUNK)
+        rng = np.random.default_rng([seed, 0xD0, c0 // CHUNK])
+        out[c0:c1] = f32_to_bf16_bits(rng.standard_normal((c1 - c0, Hq, d), dtype=np.float32))
+    return out
+
+
+def make_index_lists(S: int, Hq: int, density: float, seed: int = 0, band: int = 4,
+                     block: int = 64):
+    """Controlled-density mode: explicit vertical columns and slash offsets.
+
+    Slash offsets: a local band 0..band-1 plus random offsets; verticals:
+    sinks 0..3 plus random columns.  Counts are chosen so the slash part
+    alone covers about `density` of the causal block area.  Returns lists
+    of sorted int32 arrays (i_v[h], i_s[h]).  No index arithmetic of the
+    method happens here: these lists are INPUTS that replace Alg. 1's output.
+    """
+    nb = S // block
+    rng = np.random.default_rng([seed, 0x1D5])
+    iv, isl = [], []
+    for _ in range(Hq):
+        n_off = max(band, int(round(density * nb)))
+        offs = set(range(min(band, nb)))
+        pool = np.arange(band, nb)
+        if n_off > band and pool.size:
+            # favour small offsets (RoPE locality): draw from a decaying law
+            pr = 1.0 / (1.0 + pool / 64.0)
+            pr /= pr.sum()
+            offs |= set(rng.choice(pool, size=min(n_off - band, pool.size), replace=False, p=pr).tolist())
+        n_col = max(4, int(round(0.02 * S ** 0.5 * 8)))
+        cols = set(range(4)) | set(rng.choice(S, size=min(n_col, S), replace=False).tolist())
+        iv.append(np.array(sorted(cols), np.int32))
+        isl.append(np.array(sorted(offs), np.int32))
+    return iv, isl
