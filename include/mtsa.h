@@ -72,6 +72,57 @@ typedef struct {
   float p_s;
 } mt_vs_params;
 
+/* Vertical-slash index (Alg. 1 output, P:225 i_v and P:229 i_s), caller-owned
+ * DEVICE arrays.  For q head h:
+ *   v_idx[h * v_stride + 0 .. v_cnt[h])  vertical token columns, ascending,
+ *                                        global positions in [0, S)
+ *   s_off[h * s_stride + 0 .. s_cnt[h])  slash offsets in 64-token block units
+ *                                        (offset o: key block = query block - o,
+ *                                        P:249), ascending, in [0, S/64)
+ * Offset 0 (the diagonal) must be present for every head: it guarantees every
+ * query attends at least itself (reading R7).  mt_build_vs_index
+ * produces it; callers may also supply their own lists (v_stride >= S,
+ * s_stride >= S/64 when written by mt_build_vs_index). */
+typedef struct {
+  int32_t* v_cnt; /* [Hq] */
+  int32_t* v_idx; /* [Hq][v_stride] */
+  int64_t v_stride;
+  int32_t* s_cnt; /* [Hq] */
+  int32_t* s_off; /* [Hq][s_stride] */
+  int64_t s_stride;
+} mt_vs_index;
+
+/* ------------------------------------------------------- sparse attention */
+/* Workspace (bytes) needed by mt_sparse_attn_fwd / mt_attn_fwd_step for a
+ * layout of `world` ranks (world = 1 on one GPU). */
+size_t mt_sparse_attn_fwd_workspace_bytes(const mt_shape* shape, int world);
+
+/* Single-GPU sparse attention forward, Alg. 1 line "y <- sparse(softmax(QK^T /
+ * sqrt(d)) V, i_vs)" over the key set of each query n in block g:
+ *   K_n = { m : floor(m/64) = g - o for some o in i_s, m <= n }
+ *         U { m in i_v : floor(m/64) < g }      (I9)
+ * q [S][Hq][128], k/v [S][Hkv][128] bf16 in; o [S][Hq][128] bf16 and
+ * lse [Hq][S] float32 (natural log) out.  Errors: MT_ESHAPE, MT_EWINDOW,
+ * MT_EUNSUPPORTED, MT_EWORKSPACE, MT_ECUDA. */
+mt_status mt_sparse_attn_fwd(const mt_shape* shape, const void* q, const void* k, const void* v,
+                             const mt_vs_index* idx, void* o, float* lse, void* ws,
+                             size_t ws_bytes, mt_stream_t stream);
+
+/* One ring step of the forward (Alg. 2) for rank `rank` of a
+ * `world`-rank block-striped layout, holding the KV chunk of origin `origin`:
+ * computes the partial attention of the rank's local queries q_loc over the
+ * chunk's keys and merges it into (o_acc, lse) (merge_out_and_lse).
+ *   first != 0 : (o_acc, lse) are initialised instead of read;
+ *   last  != 0 : the merged result is written as bf16 to o (o_acc not written).
+ * q_loc [S/W][Hq][128], k_chunk/v_chunk [S/W][Hkv][128] bf16; o_acc
+ * [S/W][Hq][128] float32; lse [Hq][S/W] float32.  `shape->seq_len` is the
+ * GLOBAL S.  The ring entry points call this; it is exported so a single GPU
+ * can emulate every (rank, step) of a ring (tests). */
+mt_status mt_attn_fwd_step(const mt_shape* shape, int world, int rank, int origin, int first,
+                           int last, const void* q_loc, const void* k_chunk,
+                           const void* v_chunk, const mt_vs_index* idx, void* o, float* o_acc,
+                           float* lse, void* ws, size_t ws_bytes, mt_stream_t stream);
+
 /* ------------------------------------------------------------------ tests */
 /* Hardware self-test hook (not part of the attention API): one 128-row tcgen05
  * MMA configuration on one CTA, see csrc/selftest.cu for the variants.

@@ -48,7 +48,7 @@ def lib() -> ctypes.CDLL:
         _lib.mt_last_error.restype = ctypes.c_char_p
         for name, argtypes in _SIGS.items():
             fn = getattr(_lib, name)
-            fn.restype = ctypes.c_int
+            fn.restype = _RESTYPE.get(name, ctypes.c_int)
             fn.argtypes = argtypes
     return _lib
 
@@ -65,7 +65,11 @@ SZ = ctypes.c_size_t
 
 _SIGS: dict[str, list] = {
     "mt_selftest_mma": [I, P, P, P, P],
+    "mt_sparse_attn_fwd_workspace_bytes": [P, I],
+    "mt_sparse_attn_fwd": [P, P, P, P, P, P, P, P, SZ, P],
+    "mt_attn_fwd_step": [P, I, I, I, I, I, P, P, P, P, P, P, P, P, SZ, P],
 }
+_RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t}
 
 
 def declared_symbols() -> list[str]:

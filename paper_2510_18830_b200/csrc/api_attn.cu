@@ -1,0 +1,104 @@
+// api_attn.cu — C-ABI entry points for the sparse attention forward/backward
+// (include/mtsa.h).  Validation is synchronous; compute is enqueued on the
+// caller's stream.
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace mt {
+
+size_t vs_plan_bytes(int64_t S, int Hq, int W);
+mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const int32_t* v_cnt,
+                        const int32_t* v_idx, int64_t v_stride, const int32_t* s_cnt,
+                        const int32_t* s_off, int s_stride, void* ws, cudaStream_t st);
+mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* q,
+                        const void* k, const void* v, void* o, float* o_acc, float* lse,
+                        int first, int last, int num_sms, cudaStream_t st);
+
+int device_num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+mt_status check_device() {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(MT_ECUDA, "no CUDA device");
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(MT_EUNSUPPORTED, "device is sm_%d%d; this library is built for sm_100a", major,
+                minor);
+  return MT_OK;
+}
+
+mt_status check_shape(const mt_shape* sh, int W) {
+  if (!sh) return fail(MT_ESHAPE, "shape is NULL");
+  if (sh->head_dim != 128) return fail(MT_EUNSUPPORTED, "head_dim must be 128 (got %d)", sh->head_dim);
+  if (sh->block != 64) return fail(MT_EUNSUPPORTED, "block must be 64 (got %d)", sh->block);
+  if (sh->n_q_heads <= 0 || sh->n_kv_heads <= 0 || sh->n_q_heads % sh->n_kv_heads)
+    return fail(MT_ESHAPE, "bad head counts Hq=%d Hkv=%d", sh->n_q_heads, sh->n_kv_heads);
+  if (sh->seq_len < 64 || sh->seq_len % 64)
+    return fail(MT_EWINDOW, "seq_len %lld must be a positive multiple of 64",
+                (long long)sh->seq_len);
+  if (W <= 0) return fail(MT_ESHAPE, "world must be >= 1");
+  if (sh->seq_len % (64LL * W))
+    return fail(MT_ELAYOUT, "seq_len %lld is not a multiple of 64 * world (%d)",
+                (long long)sh->seq_len, W);
+  if (sh->seq_len / 64 > (1LL << 24)) return fail(MT_ESHAPE, "seq_len too large");
+  return MT_OK;
+}
+
+mt_status check_index(const mt_vs_index* idx, const mt_shape* sh) {
+  if (!idx || !idx->v_cnt || !idx->v_idx || !idx->s_cnt || !idx->s_off)
+    return fail(MT_ESHAPE, "index pointers must be non-NULL");
+  if (idx->v_stride < 1 || idx->s_stride < 1 || idx->s_stride > (1LL << 30))
+    return fail(MT_ESHAPE, "bad index strides");
+  (void)sh;
+  return MT_OK;
+}
+
+}  // namespace mt
+
+using namespace mt;
+
+extern "C" size_t mt_sparse_attn_fwd_workspace_bytes(const mt_shape* sh, int world) {
+  if (!sh || world <= 0) return 0;
+  return vs_plan_bytes(sh->seq_len, sh->n_q_heads, world);
+}
+
+extern "C" mt_status mt_attn_fwd_step(const mt_shape* sh, int world, int rank, int origin,
+                                      int first, int last, const void* q_loc,
+                                      const void* k_chunk, const void* v_chunk,
+                                      const mt_vs_index* idx, void* o, float* o_acc, float* lse,
+                                      void* ws, size_t ws_bytes, mt_stream_t stream) {
+  MT_TRY(check_shape(sh, world));
+  MT_TRY(check_index(idx, sh));
+  if (rank < 0 || rank >= world || origin < 0 || origin >= world)
+    return fail(MT_ESHAPE, "rank/origin out of range");
+  if (!q_loc || !k_chunk || !v_chunk || !lse) return fail(MT_ESHAPE, "NULL tensor");
+  if (last && !o) return fail(MT_ESHAPE, "o must be non-NULL when last");
+  if (!(first && last) && !o_acc) return fail(MT_ESHAPE, "o_acc must be non-NULL");
+  const size_t need = mt_sparse_attn_fwd_workspace_bytes(sh, world);
+  if (!ws || ws_bytes < need)
+    return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  MT_TRY(check_device());
+  VSPlan plan;
+  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, world, idx->v_cnt,
+                       idx->v_idx, idx->v_stride, idx->s_cnt, idx->s_off, (int)idx->s_stride, ws,
+                       stream));
+  const int nloc = (int)(sh->seq_len / 64 / world);
+  return attn_fwd_step(plan, rank, origin, nloc, q_loc, k_chunk, v_chunk, o, o_acc, lse, first,
+                       last, device_num_sms(), stream);
+}
+
+extern "C" mt_status mt_sparse_attn_fwd(const mt_shape* sh, const void* q, const void* k,
+                                        const void* v, const mt_vs_index* idx, void* o,
+                                        float* lse, void* ws, size_t ws_bytes,
+                                        mt_stream_t stream) {
+  return mt_attn_fwd_step(sh, 1, 0, 0, 1, 1, q, k, v, idx, o, nullptr, lse, ws, ws_bytes, stream);
+}

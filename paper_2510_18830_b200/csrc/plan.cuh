@@ -1,0 +1,35 @@
+// plan.cuh — device-side view of a vertical-slash index as consumed by the
+// sparse attention kernels.
+//
+// The global index (Alg. 1 output): per q head h, sorted vertical
+// token columns i_v[h] and sorted slash block offsets i_s[h] (offset o selects
+// key block g - o for query block g).  The kernels never materialise
+// sparseformat's per-query-block lists (convert_index P:845); they derive
+// them on the fly from:
+//   s_off/s_cnt : i_s[h] ascending
+//   s_bits      : i_s[h] as a bitmap over [0, nb)      (membership test, I9)
+//   vptr/vcol   : i_v[h] grouped by KV origin s = (m/64) mod W, ascending
+//                 inside each group (per-origin lists of I10)
+#pragma once
+#include <cstdint>
+
+namespace mt {
+
+struct VSPlan {
+  int64_t S;        // global sequence length
+  int Hq, Hkv, W;   // heads, world size (ranks of the block-striped layout)
+  int nb;           // global 64-token blocks = S / 64
+  int s_stride;     // row stride of s_off (>= nb)
+  int bits_words;   // 32-bit words per head in s_bits
+  const int32_t* s_cnt;
+  const int32_t* s_off;
+  const uint32_t* s_bits;
+  const int32_t* vptr;  // [Hq][W + 1]
+  const int32_t* vcol;  // [Hq][S] (global column ids, grouped by origin)
+};
+
+__device__ __forceinline__ bool plan_has_slash(const VSPlan& p, int h, int o) {
+  return (p.s_bits[(int64_t)h * p.bits_words + (o >> 5)] >> (o & 31)) & 1u;
+}
+
+}  // namespace mt

@@ -1,0 +1,118 @@
+"""Torch-facing wrappers over the C ABI (include/mtsa.h).
+
+Argument marshalling only (pointers, sizes, the current CUDA stream); every
+step of the hot path runs inside libmtsa.so.  Tensors must already live on the
+GPU in the documented layouts; nothing here falls back to CPU code.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+BLOCK = 64
+HEAD_DIM = 128
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("tensor must be on the GPU")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def shape(seq_len: int, n_q_heads: int, n_kv_heads: int) -> _lib.Shape:
+    return _lib.Shape(seq_len, n_q_heads, n_kv_heads, HEAD_DIM, BLOCK)
+
+
+@dataclass
+class VSIndex:
+    """Device-resident vertical-slash index (mt_vs_index)."""
+    v_cnt: torch.Tensor   # [Hq] int32
+    v_idx: torch.Tensor   # [Hq][v_stride] int32
+    s_cnt: torch.Tensor   # [Hq] int32
+    s_off: torch.Tensor   # [Hq][s_stride] int32
+
+    @staticmethod
+    def empty(seq_len: int, n_q_heads: int, device="cuda") -> "VSIndex":
+        nb = seq_len // BLOCK
+        z = lambda *s: torch.zeros(*s, dtype=torch.int32, device=device)
+        return VSIndex(z(n_q_heads), z(n_q_heads, seq_len), z(n_q_heads), z(n_q_heads, nb))
+
+    @staticmethod
+    def from_lists(i_v, i_s, seq_len: int, device="cuda") -> "VSIndex":
+        """Upload explicit per-head lists (e.g. a controlled-density pattern)."""
+        Hq = len(i_v)
+        idx = VSIndex.empty(seq_len, Hq, device="cpu")
+        for h in range(Hq):
+            a, b = torch.as_tensor(i_v[h], dtype=torch.int32), torch.as_tensor(i_s[h], dtype=torch.int32)
+            idx.v_cnt[h], idx.s_cnt[h] = a.numel(), b.numel()
+            idx.v_idx[h, : a.numel()] = a
+            idx.s_off[h, : b.numel()] = b
+        return VSIndex(*(t.to(device) for t in (idx.v_cnt, idx.v_idx, idx.s_cnt, idx.s_off)))
+
+    def to_lists(self):
+        vc, vi, sc, so = (t.cpu() for t in (self.v_cnt, self.v_idx, self.s_cnt, self.s_off))
+        iv = [vi[h, : int(vc[h])].numpy().copy() for h in range(vc.numel())]
+        is_ = [so[h, : int(sc[h])].numpy().copy() for h in range(sc.numel())]
+        return iv, is_
+
+    def c_struct(self) -> "MTIndex":
+        return MTIndex(_ptr(self.v_cnt), _ptr(self.v_idx), self.v_idx.shape[1],
+                       _ptr(self.s_cnt), _ptr(self.s_off), self.s_off.shape[1])
+
+
+class MTIndex(ctypes.Structure):
+    _fields_ = [("v_cnt", ctypes.c_void_p), ("v_idx", ctypes.c_void_p), ("v_stride", ctypes.c_int64),
+                ("s_cnt", ctypes.c_void_p), ("s_off", ctypes.c_void_p), ("s_stride", ctypes.c_int64)]
+
+
+_WS: dict = {}
+
+
+def workspace(nbytes: int, device=None) -> torch.Tensor:
+    """Cached byte workspace on the current device (grown on demand)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    buf = _WS.get(dev)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        _WS[dev] = buf
+    return buf
+
+
+def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, idx: VSIndex):
+    """Single-GPU VS sparse attention forward -> (o bf16 [S][Hq][128], lse f32 [Hq][S])."""
+    S, Hq, _ = q.shape
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    nbytes = L.mt_sparse_attn_fwd_workspace_bytes(ctypes.byref(sh), 1)
+    ws = workspace(nbytes)
+    o = torch.empty_like(q)
+    lse = torch.empty(Hq, S, dtype=torch.float32, device=q.device)
+    ci = idx.c_struct()
+    _lib.check(L.mt_sparse_attn_fwd(ctypes.byref(sh), _ptr(q), _ptr(k), _ptr(v), ctypes.byref(ci),
+                                    _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream()))
+    return o, lse
+
+
+def attn_fwd_step(seq_len: int, world: int, rank: int, origin: int, first: bool, last: bool,
+                  q_loc, k_chunk, v_chunk, idx: VSIndex, o, o_acc, lse):
+    """One ring step (mt_attn_fwd_step); tensors are rank-local (striped)."""
+    sh = shape(seq_len, q_loc.shape[1], k_chunk.shape[1])
+    L = _lib.lib()
+    nbytes = L.mt_sparse_attn_fwd_workspace_bytes(ctypes.byref(sh), world)
+    ws = workspace(nbytes)
+    ci = idx.c_struct()
+    _lib.check(L.mt_attn_fwd_step(ctypes.byref(sh), world, rank, origin, int(first), int(last),
+                                  _ptr(q_loc), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(ci),
+                                  _ptr(o), _ptr(o_acc), _ptr(lse), _ptr(ws), ws.numel(), _stream()))
