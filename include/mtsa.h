@@ -92,6 +92,51 @@ typedef struct {
   int64_t s_stride;
 } mt_vs_index;
 
+/* Opaque NCCL communicator over the ranks of one context-parallel group
+ * (see the ring section below).  NULL means "single GPU". */
+typedef struct mt_comm mt_comm;
+
+/* Communicator lifecycle (one process per GPU, P:64 context parallelism).
+ * mt_comm_unique_id: rank 0 creates a 128-byte NCCL unique id (host buffer);
+ *   the caller distributes it to every rank (e.g. torch.distributed).
+ * mt_comm_create: collective over `world` ranks; `inner` = ranks per node of the
+ *   hierarchical ring (Alg. 2 w_inner); inner = world (or <= 0) is the
+ *   flat ring.  The current CUDA device is used.  Errors: MT_ESHAPE (bad
+ *   rank/world, inner not dividing world), MT_ENCCL, MT_EUNSUPPORTED.
+ * mt_comm_destroy: releases NCCL resources and the comm stream/events. */
+mt_status mt_comm_unique_id(uint8_t id[128]);
+mt_status mt_comm_create(const uint8_t id[128], int world, int rank, int inner, mt_comm** out);
+mt_status mt_comm_destroy(mt_comm* comm);
+
+/* ------------------------------------------------------------- VS index */
+/* Workspace (bytes) for mt_build_vs_index on a `world`-rank layout. */
+size_t mt_build_vs_index_workspace_bytes(const mt_shape* shape, int world);
+
+/* Alg. 1 vertical-slash index of every q head, in the VS-IDX v1
+ * arithmetic: fp32 window scores of the last 64 queries
+ * against all causal keys, softmax in specified fixed point, column
+ * sums (token level) and 64x64-pooled block-diagonal sums, exact
+ * integer top-p budgets, argtopk with ties to the smaller index,
+ * forced column 0 and offset 0.  The result is bit-identical to the CPU oracle
+ * and independent of `world`.
+ *   comm == NULL : single GPU; q [S][Hq][128], k [S][Hkv][128].
+ *   comm != NULL : q/k are this rank's block-striped local slices
+ *                  [S/W][.][128]; every rank receives the same global lists.
+ * out: caller-allocated, v_stride >= S, s_stride >= S/64 (MT_ECAPACITY).
+ * Errors: MT_ESHAPE, MT_EWINDOW (S < 64 or S % 64), MT_ECONFIG (p outside
+ * (0, 1]), MT_ELAYOUT, MT_EWORKSPACE, MT_EUNSUPPORTED, MT_ECUDA, MT_ENCCL. */
+mt_status mt_build_vs_index(mt_comm* comm, const mt_shape* shape, const mt_vs_params* params,
+                            const void* q, const void* k, mt_vs_index* out, void* ws,
+                            size_t ws_bytes, mt_stream_t stream);
+
+/* Test hook (single GPU): the exact intermediate scores of Alg. 1 —
+ * col_scores [Hq][S] = sum_v(A_hat) per token column (uint64 fixed point,
+ * 2^32 = probability 1) and slash_scores [Hq][S/64] = the 64x64-pooled
+ * diagonal score of each block offset.  Same workspace as mt_build_vs_index. */
+mt_status mt_vs_column_scores(const mt_shape* shape, const void* q, const void* k,
+                              uint64_t* col_scores, uint64_t* slash_scores, void* ws,
+                              size_t ws_bytes, mt_stream_t stream);
+
 /* ------------------------------------------------------- sparse attention */
 /* Workspace (bytes) needed by mt_sparse_attn_fwd / mt_attn_fwd_step for a
  * layout of `world` ranks (world = 1 on one GPU). */

@@ -68,8 +68,15 @@ _SIGS: dict[str, list] = {
     "mt_sparse_attn_fwd_workspace_bytes": [P, I],
     "mt_sparse_attn_fwd": [P, P, P, P, P, P, P, P, SZ, P],
     "mt_attn_fwd_step": [P, I, I, I, I, I, P, P, P, P, P, P, P, P, SZ, P],
+    "mt_build_vs_index_workspace_bytes": [P, I],
+    "mt_build_vs_index": [P, P, P, P, P, P, P, SZ, P],
+    "mt_vs_column_scores": [P, P, P, P, P, P, SZ, P],
+    "mt_comm_unique_id": [P],
+    "mt_comm_create": [P, I, I, I, P],
+    "mt_comm_destroy": [P],
 }
-_RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t}
+_RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
+            "mt_build_vs_index_workspace_bytes": ctypes.c_size_t}
 
 
 def declared_symbols() -> list[str]:

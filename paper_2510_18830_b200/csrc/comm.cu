@@ -1,0 +1,131 @@
+// comm.cu — mt_comm lifecycle and the distributed (context-parallel) index build.
+//
+// The distributed Alg. 1 index under block-striped keys: the window
+// queries live on rank W-1 (its last local block is global block nb-1), every
+// rank scores its own keys, and the exact reductions of VS-IDX v1 are completed
+// with NCCL collectives whose results do not depend on reduction order:
+// broadcast (window Q), all-reduce MAX (fp32 row maxima), all-reduce SUM
+// (uint64 fixed-point row sums), all-gather (packed sort keys).  Every rank then
+// runs the same sort/top-p and obtains the same global lists, bit-identical to
+// the single-GPU result.
+#include "comm.cuh"
+#include "vsidx.cuh"
+#include <cuda_bf16.h>
+
+namespace mt {
+
+#ifdef MT_HAVE_NCCL
+struct NcclCollectives final : VSCollectives {
+  mt_comm* c;
+  explicit NcclCollectives(mt_comm* cm) : c(cm) {}
+  mt_status bcast_window(__nv_bfloat16* qwin, size_t n, cudaStream_t st) override {
+    return nccl_check(ncclBroadcast(qwin, qwin, n * 2, ncclUint8, c->world - 1, c->nccl, st),
+                      "ncclBroadcast(window)");
+  }
+  mt_status allreduce_max(float* M, size_t n, cudaStream_t st) override {
+    return nccl_check(ncclAllReduce(M, M, n, ncclFloat32, ncclMax, c->nccl, st),
+                      "ncclAllReduce(max)");
+  }
+  mt_status allreduce_sum_u64(unsigned long long* E, size_t n, cudaStream_t st) override {
+    return nccl_check(ncclAllReduce(E, E, n, ncclUint64, ncclSum, c->nccl, st),
+                      "ncclAllReduce(sum)");
+  }
+  mt_status allgather_keys(const uint64_t* loc, uint64_t* glob, int Hq, int64_t n_loc,
+                           cudaStream_t st) override {
+    MT_TRY(nccl_check(ncclGroupStart(), "ncclGroupStart"));
+    for (int h = 0; h < Hq; ++h)
+      MT_TRY(nccl_check(ncclAllGather(loc + (size_t)h * n_loc, glob + (size_t)h * n_loc * c->world,
+                                      (size_t)n_loc, ncclUint64, c->nccl, st),
+                        "ncclAllGather(keys)"));
+    return nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  }
+};
+#endif
+
+}  // namespace mt
+
+using namespace mt;
+
+extern "C" mt_status mt_comm_unique_id(uint8_t id[128]) {
+#ifdef MT_HAVE_NCCL
+  if (!id) return fail(MT_ESHAPE, "id is NULL");
+  ncclUniqueId u;
+  MT_TRY(nccl_check(ncclGetUniqueId(&u), "ncclGetUniqueId"));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  return MT_OK;
+#else
+  (void)id;
+  return fail(MT_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, int inner,
+                                    mt_comm** out) {
+#ifdef MT_HAVE_NCCL
+  if (!id || !out) return fail(MT_ESHAPE, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(MT_ESHAPE, "bad world/rank");
+  if (inner <= 0) inner = world;
+  if (world % inner) return fail(MT_ESHAPE, "inner ring size %d must divide world %d", inner, world);
+  MT_TRY(check_device());
+  mt_comm* c = new mt_comm();
+  c->world = world;
+  c->rank = rank;
+  c->inner = inner;
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(MT_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi);
+  cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
+  *out = c;
+  return MT_OK;
+#else
+  (void)id; (void)world; (void)rank; (void)inner; (void)out;
+  return fail(MT_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+extern "C" mt_status mt_comm_destroy(mt_comm* c) {
+  if (!c) return MT_OK;
+#ifdef MT_HAVE_NCCL
+  if (c->nccl) ncclCommDestroy(c->nccl);
+#endif
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  delete c;
+  return MT_OK;
+}
+
+mt_status mt_build_vs_index_dist(mt_comm* comm, const mt_shape* sh, const mt_vs_params* prm,
+                                 const void* q, const void* k, mt_vs_index* out, void* ws,
+                                 size_t ws_bytes, mt_stream_t st) {
+#ifdef MT_HAVE_NCCL
+  const int W = comm->world;
+  MT_TRY(check_shape(sh, W));
+  if (!prm) return fail(MT_ESHAPE, "params is NULL");
+  if (!(prm->p_v > 0.f && prm->p_v <= 1.f) || !(prm->p_s > 0.f && prm->p_s <= 1.f))
+    return fail(MT_ECONFIG, "p_v, p_s must lie in (0, 1] (got %g, %g)", prm->p_v, prm->p_s);
+  if (sh->seq_len > (1LL << 22)) return fail(MT_ESHAPE, "seq_len must be <= 2^22 for the index");
+  if (!q || !k || !out || !out->v_cnt || !out->v_idx || !out->s_cnt || !out->s_off)
+    return fail(MT_ESHAPE, "NULL argument");
+  if (out->v_stride < sh->seq_len || out->s_stride < sh->seq_len / 64)
+    return fail(MT_ECAPACITY, "index capacity too small");
+  const size_t need = vsidx_workspace_bytes(sh->seq_len, sh->n_q_heads, W);
+  if (!ws || ws_bytes < need) return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  NcclCollectives coll(comm);
+  return vsidx_build(&coll, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, W, comm->rank, prm->p_v,
+                     prm->p_s, q, k, out->v_cnt, out->v_idx, out->v_stride, out->s_cnt,
+                     out->s_off, out->s_stride, nullptr, nullptr, ws, st);
+#else
+  (void)comm; (void)sh; (void)prm; (void)q; (void)k; (void)out; (void)ws; (void)ws_bytes; (void)st;
+  return fail(MT_EUNSUPPORTED, "built without NCCL");
+#endif
+}

@@ -1,0 +1,558 @@
+// vs_index.cu — Alg. 1 "Dynamic Sparse Training Head" index on the GPU
+// (PAPER.md P:213-232), in the VS-IDX v1 arithmetic of DESIGN.md §2.1
+// so that it is bit-identical to the CPU oracle and independent of the number
+// of ranks the keys are striped over:
+//   stage1  I1-I2  t = fold_c fma(q, k, acc) (exact bf16 products, one RN per
+//                  add), causal mask, row max (order-free)
+//   stage2  I3-I4  e = exp2s(RN(RN(t - M) * C_d)) with a specified polynomial
+//                  (no MUFU ex2, no FMA contraction); E = sum floor(e 2^31) (uint64)
+//   stage3  I5-I6  w = floor(RN(e / l) 2^32); V_m = sum_i w; P_kb = sum_{m in kb} V_m;
+//                  sort keys (score desc, index asc) packed into uint64
+//   select  I7-I8  segmented radix sort, exact integer top-p, forced members,
+//                  ascending compaction -> i_v, i_s
+// The window scoring is deliberately on CUDA cores in fp32: the tensor cores'
+// accumulation order is unspecified, which would break bit-exactness
+// ("what differs from the paper").
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "vsidx.cuh"
+
+namespace mt {
+
+namespace vsi {
+
+constexpr int kThreads = 256;   // keys per CTA in stages 1-3
+constexpr int kRG = 8;          // window rows per register group
+constexpr int kIdxBits = 22;    // S <= 4M
+constexpr int kScoreBits = 40;  // scores < 2^39
+
+__constant__ uint32_t kExp2CoefBits[8] = {0x3F800000u, 0x3F317218u, 0x3E75FDF0u, 0x3D635847u,
+                                          0x3C1D955Bu, 0x3AAEC3FFu, 0x39218489u, 0x377FE5FEu};
+constexpr uint32_t kCdBits = 0x3E0293EEu;  // RN(log2(e) / sqrt(128))
+
+struct Geo {
+  int64_t S;      // global
+  int64_t S_loc;  // local keys
+  int Hq, Hkv, W, r;
+};
+
+__device__ __forceinline__ int64_t global_col(const Geo& g, int64_t m_loc) {
+  return ((m_loc >> 6) * g.W + g.r) * 64 + (m_loc & 63);
+}
+
+// I3: specified 2^y (y <= 0), every operation one IEEE RN op.
+__device__ __forceinline__ float exp2s(float y) {
+  if (!(y >= -125.0f)) return 0.0f;
+  const float j = rintf(y);
+  const float f = __fsub_rn(y, j);
+  float p = __uint_as_float(kExp2CoefBits[7]);
+#pragma unroll
+  for (int c = 6; c >= 0; --c) p = __fadd_rn(__fmul_rn(p, f), __uint_as_float(kExp2CoefBits[c]));
+  const int ji = (int)j;
+  return __fmul_rn(p, __int_as_float((ji + 127) << 23));
+}
+
+__device__ __forceinline__ void atomic_max_f32(float* a, float v) {
+  if (v >= 0.f)
+    atomicMax(reinterpret_cast<int*>(a), __float_as_int(v));
+  else
+    atomicMin(reinterpret_cast<unsigned*>(a), __float_as_uint(v));
+}
+
+__device__ __forceinline__ uint64_t shfl_down_u64(uint64_t v, int o) {
+  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  lo = __shfl_down_sync(0xffffffffu, lo, o);
+  hi = __shfl_down_sync(0xffffffffu, hi, o);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// ---------------------------------------------------------------- stage 1
+// t[h][i][m] (fp32) and row max M[h][i].
+__global__ void __launch_bounds__(kThreads) stage1_scores(Geo g, const __nv_bfloat16* qwin,
+                                                          const __nv_bfloat16* k, float* t,
+                                                          float* M) {
+  __shared__ __align__(16) float qs[64][128];
+  __shared__ float wmax[kThreads / 32][64];
+  const int h = blockIdx.y;
+  const int grp = g.Hq / g.Hkv;
+  for (int e = threadIdx.x; e < 64 * 128; e += kThreads) {
+    const int i = e >> 7, c = e & 127;
+    qs[i][c] = __bfloat162float(qwin[((size_t)i * g.Hq + h) * 128 + c]);
+  }
+  __syncthreads();
+  const int64_t m = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool in = m < g.S_loc;
+  float kf[128];
+  if (in) {
+    const uint4* src = reinterpret_cast<const uint4*>(k + ((size_t)m * g.Hkv + h / grp) * 128);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      uint4 u = src[v];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        kf[v * 8 + 2 * j] = __uint_as_float(w[j] << 16);
+        kf[v * 8 + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 128; ++c) kf[c] = 0.f;
+  }
+  const int64_t mg = in ? global_col(g, m) : INT64_MAX;
+  const int64_t n0 = g.S - 64;
+  float* th = t + (size_t)h * 64 * g.S_loc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int i0 = 0; i0 < 64; i0 += kRG) {
+    float acc[kRG];
+#pragma unroll
+    for (int r = 0; r < kRG; ++r) acc[r] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 128; c += 4) {
+#pragma unroll
+      for (int r = 0; r < kRG; ++r) {
+        const float4 qv = *reinterpret_cast<const float4*>(&qs[i0 + r][c]);
+        acc[r] = __fmaf_rn(qv.x, kf[c], acc[r]);
+        acc[r] = __fmaf_rn(qv.y, kf[c + 1], acc[r]);
+        acc[r] = __fmaf_rn(qv.z, kf[c + 2], acc[r]);
+        acc[r] = __fmaf_rn(qv.w, kf[c + 3], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRG; ++r) {
+      const int i = i0 + r;
+      const bool causal = mg <= n0 + i;
+      const float tv = causal ? acc[r] : -INFINITY;
+      if (in) th[(size_t)i * g.S_loc + m] = tv;
+      float mx = tv;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_down_sync(0xffffffffu, mx, o));
+      if (lane == 0) wmax[warp][i] = mx;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) mx = fmaxf(mx, wmax[w][threadIdx.x]);
+    if (mx > -INFINITY) atomic_max_f32(&M[h * 64 + threadIdx.x], mx);
+  }
+}
+
+// ---------------------------------------------------------------- stage 2
+// e = exp2s(...) overwrites t; E[h][i] += sum floor(e 2^31).
+__global__ void __launch_bounds__(kThreads) stage2_exp(Geo g, float* t, const float* M,
+                                                       unsigned long long* E) {
+  __shared__ uint64_t wsum[kThreads / 32][64];
+  const int h = blockIdx.y;
+  const int64_t m = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool in = m < g.S_loc;
+  const float Cd = __uint_as_float(kCdBits);
+  float* th = t + (size_t)h * 64 * g.S_loc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 4
+  for (int i = 0; i < 64; ++i) {
+    uint64_t fx = 0;
+    if (in) {
+      const float tv = th[(size_t)i * g.S_loc + m];
+      float e = 0.f;
+      if (tv > -INFINITY) {
+        const float y = __fmul_rn(__fsub_rn(tv, M[h * 64 + i]), Cd);
+        e = exp2s(y);
+      }
+      th[(size_t)i * g.S_loc + m] = e;
+      fx = __float2ull_rz(__fmul_rn(e, 2147483648.0f));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fx += shfl_down_u64(fx, o);
+    if (lane == 0) wsum[warp][i] = fx;
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    uint64_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) s += wsum[w][threadIdx.x];
+    if (s) atomicAdd(&E[h * 64 + threadIdx.x], (unsigned long long)s);
+  }
+}
+
+// ---------------------------------------------------------------- stage 3
+// V_m, P_kb, packed sort keys: key = ((2^40 - 1 - score) << 22) | index.
+__global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
+                                                          const unsigned long long* E,
+                                                          uint64_t* keysV, uint64_t* keysP,
+                                                          uint64_t* colV, uint64_t* blkP) {
+  __shared__ float l_s[64];
+  __shared__ uint64_t half[kThreads / 32];
+  const int h = blockIdx.y;
+  if (threadIdx.x < 64) {
+    const float Ef = __ull2float_rn(E[h * 64 + threadIdx.x]);
+    l_s[threadIdx.x] = __fmul_rn(Ef, 4.656612873077393e-10f);  // 2^-31
+  }
+  __syncthreads();
+  const int64_t m = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool in = m < g.S_loc;
+  const float* th = t + (size_t)h * 64 * g.S_loc;
+  uint64_t V = 0;
+  if (in) {
+#pragma unroll 8
+    for (int i = 0; i < 64; ++i) {
+      const float e = th[(size_t)i * g.S_loc + m];
+      if (e > 0.f) {
+        const float p = __fdiv_rn(e, l_s[i]);
+        V += __float2ull_rz(__fmul_rn(p, 4294967296.0f));
+      }
+    }
+  }
+  const uint64_t smax = (1ull << kScoreBits) - 1;
+  if (in) {
+    const int64_t mg = global_col(g, m);
+    keysV[(size_t)h * g.S_loc + m] = ((smax - V) << kIdxBits) | (uint64_t)mg;
+    if (colV) colV[(size_t)h * g.S + mg] = V;
+  }
+  // block sums over 64 consecutive local keys = one global block
+  uint64_t s = V;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += shfl_down_u64(s, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) half[warp] = s;
+  __syncthreads();
+  if (threadIdx.x < kThreads / 64) {
+    const int64_t lb = (int64_t)blockIdx.x * (kThreads / 64) + threadIdx.x;
+    if (lb * 64 < g.S_loc) {
+      const uint64_t P = half[2 * threadIdx.x] + half[2 * threadIdx.x + 1];
+      const int64_t kb = lb * g.W + g.r;
+      const int64_t nb = g.S / 64;
+      const int64_t o = nb - 1 - kb;  // slash offset scored by this block (I6, reading R1)
+      keysP[(size_t)h * (g.S_loc / 64) + lb] = ((smax - P) << kIdxBits) | (uint64_t)o;
+      if (blkP) blkP[(size_t)h * nb + o] = P;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- select
+// One CTA per (head, list): exact top-p budget over sorted keys, then mark
+// the first k indices (plus forced index 0) in a bitmap.
+__global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const uint64_t* sortedP,
+                                                   int64_t nV, int64_t nP, uint64_t pq_v,
+                                                   uint64_t pq_s, uint32_t* bitsV,
+                                                   uint32_t* bitsP, int* kout) {
+  const int h = blockIdx.x, which = blockIdx.y;
+  const int64_t n = which ? nP : nV;
+  const uint64_t* keys = (which ? sortedP : sortedV) + (size_t)h * n;
+  uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * ((n + 31) / 32);
+  const uint64_t pq = which ? pq_s : pq_v;
+  const uint64_t smax = (1ull << kScoreBits) - 1;
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long tot_s;
+  __shared__ long long kmin;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t per = (n + nt - 1) / nt;
+  const int64_t b = tid * per, e = min(n, b + per);
+  // chunk sums
+  unsigned long long cs = 0;
+  for (int64_t x = b; x < e; ++x) cs += smax - (keys[x] >> kIdxBits);
+  // inclusive scan of chunk sums (warp + smem)
+  const int lane = tid & 31, warp = tid >> 5;
+  unsigned long long incl = cs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < nt / 32 ? red[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    red[lane] = w;
+    if (lane == 31) tot_s = w;
+    if (lane == 0) kmin = LLONG_MAX;
+  }
+  __syncthreads();
+  const unsigned long long T = tot_s;
+  unsigned long long cum = (warp ? red[warp - 1] : 0ull) + incl - cs;  // exclusive prefix
+  int64_t k;
+  if (pq >= (1ull << 24)) {
+    k = n;  // p = 1: every item (reading R22)
+  } else {
+    const unsigned long long rhs = pq * T;
+    long long found = LLONG_MAX;
+    for (int64_t x = b; x < e; ++x) {
+      cum += smax - (keys[x] >> kIdxBits);
+      if ((cum << 24) >= rhs) { found = x + 1; break; }
+    }
+    if (found != LLONG_MAX) atomicMin(&kmin, found);
+    __syncthreads();
+    k = kmin;
+    if (k == LLONG_MAX) k = n;
+  }
+  const uint64_t imask = (1ull << kIdxBits) - 1;
+  for (int64_t x = tid; x < k; x += nt) {
+    const uint64_t idx = keys[x] & imask;
+    atomicOr(&bits[idx >> 5], 1u << (idx & 31));
+  }
+  if (tid == 0) {
+    atomicOr(&bits[0], 1u);  // forced: column 0 / offset 0 (reading R7)
+    if (kout) kout[h * 2 + which] = (int)k;
+  }
+}
+
+// Ascending compaction of a bitmap into an index list.
+__global__ void __launch_bounds__(1024) compact_bits(const uint32_t* bitsV, const uint32_t* bitsP,
+                                                     int64_t nV, int64_t nP, int32_t* v_cnt,
+                                                     int32_t* v_idx, int64_t v_stride,
+                                                     int32_t* s_cnt, int32_t* s_off,
+                                                     int64_t s_stride) {
+  const int h = blockIdx.x, which = blockIdx.y;
+  const int64_t n = which ? nP : nV;
+  const int64_t words = (n + 31) / 32;
+  const uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * words;
+  int32_t* out = which ? s_off + (size_t)h * s_stride : v_idx + (size_t)h * v_stride;
+  __shared__ int red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t per = (words + nt - 1) / nt;
+  const int64_t b = tid * per, e = min(words, b + per);
+  int cnt = 0;
+  for (int64_t w = b; w < e; ++w) cnt += __popc(bits[w]);
+  const int lane = tid & 31, warp = tid >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nt / 32 ? red[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    red[lane] = w;
+  }
+  __syncthreads();
+  int pos = (warp ? red[warp - 1] : 0) + incl - cnt;
+  for (int64_t w = b; w < e; ++w) {
+    uint32_t x = bits[w];
+    while (x) {
+      const int bit = __ffs(x) - 1;
+      x &= x - 1;
+      out[pos++] = (int32_t)(w * 32 + bit);
+    }
+  }
+  if (tid == nt - 1) (which ? s_cnt : v_cnt)[h] = red[31];
+}
+
+__global__ void fill_f32(float* p, float v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void seg_offsets(int* off, int n_seg, int64_t len) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n_seg) off[i] = (int)(i * len);
+}
+
+}  // namespace vsi
+
+// ---------------------------------------------------------------- host side
+struct VSIndexWs {
+  float* t;                     // [Hq][64][S_loc]
+  float* M;                     // [Hq][64]
+  unsigned long long* E;        // [Hq][64]
+  uint64_t* keysV_loc;          // [Hq][S_loc]
+  uint64_t* keysP_loc;          // [Hq][nloc]
+  uint64_t* keysV;              // [Hq][S]   (gathered)
+  uint64_t* keysP;              // [Hq][nb]
+  uint64_t* sortV;              // [Hq][S]
+  uint64_t* sortP;              // [Hq][nb]
+  uint32_t* bitsV;              // [Hq][S/32]
+  uint32_t* bitsP;              // [Hq][ceil(nb/32)]
+  int* segV;                    // [Hq+1]
+  int* segP;                    // [Hq+1]
+  __nv_bfloat16* qwin;          // [64][Hq][128]
+  void* cub_tmp;
+  size_t cub_bytes;
+  size_t total;
+};
+
+static size_t cub_sort_bytes(int Hq, int64_t n) {
+  size_t b = 0;
+  cub::DeviceSegmentedRadixSort::SortKeys(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                          (int)(Hq * n), Hq, (const int*)nullptr,
+                                          (const int*)nullptr, 0, vsi::kIdxBits + vsi::kScoreBits);
+  return b;
+}
+
+static VSIndexWs carve_vsidx(void* base, int64_t S, int Hq, int W) {
+  VSIndexWs w{};
+  const int64_t S_loc = S / W, nb = S / 64, nloc = nb / W;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    void* r = p ? p + off : nullptr;
+    off = (off + bytes + 255) & ~size_t(255);
+    return r;
+  };
+  w.t = (float*)take((size_t)Hq * 64 * S_loc * 4);
+  w.M = (float*)take((size_t)Hq * 64 * 4);
+  w.E = (unsigned long long*)take((size_t)Hq * 64 * 8);
+  w.keysV_loc = (uint64_t*)take((size_t)Hq * S_loc * 8);
+  w.keysP_loc = (uint64_t*)take((size_t)Hq * nloc * 8);
+  w.keysV = (uint64_t*)take((size_t)Hq * S * 8);
+  w.keysP = (uint64_t*)take((size_t)Hq * nb * 8);
+  w.sortV = (uint64_t*)take((size_t)Hq * S * 8);
+  w.sortP = (uint64_t*)take((size_t)Hq * nb * 8);
+  w.bitsV = (uint32_t*)take((size_t)Hq * ((S + 31) / 32) * 4);
+  w.bitsP = (uint32_t*)take((size_t)Hq * ((nb + 31) / 32) * 4);
+  w.segV = (int*)take((size_t)(Hq + 1) * 4);
+  w.segP = (int*)take((size_t)(Hq + 1) * 4);
+  w.qwin = (__nv_bfloat16*)take((size_t)64 * Hq * 128 * 2);
+  w.cub_bytes = std::max(cub_sort_bytes(Hq, S), cub_sort_bytes(Hq, nb));
+  w.cub_tmp = take(w.cub_bytes);
+  w.total = off;
+  return w;
+}
+
+size_t vsidx_workspace_bytes(int64_t S, int Hq, int W) { return carve_vsidx(nullptr, S, Hq, W).total; }
+
+mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, int r, float p_v,
+                      float p_s, const void* q_loc, const void* k_loc, int32_t* v_cnt,
+                      int32_t* v_idx, int64_t v_stride, int32_t* s_cnt, int32_t* s_off,
+                      int64_t s_stride, uint64_t* dbg_colV, uint64_t* dbg_blkP, void* ws,
+                      cudaStream_t st) {
+  using namespace vsi;
+  VSIndexWs w = carve_vsidx(ws, S, Hq, W);
+  const int64_t S_loc = S / W, nb = S / 64, nloc = nb / W;
+  Geo g{S, S_loc, Hq, Hkv, W, r};
+  // window queries (global rows S-64..S-1, held by rank W-1 at its last local block)
+  const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(q_loc);
+  if (coll) {
+    if (r == W - 1)
+      cudaMemcpyAsync(w.qwin, q + (size_t)(S_loc - 64) * Hq * 128, (size_t)64 * Hq * 128 * 2,
+                      cudaMemcpyDeviceToDevice, st);
+    MT_TRY(coll->bcast_window(w.qwin, (size_t)64 * Hq * 128, st));
+  } else {
+    cudaMemcpyAsync(w.qwin, q + (size_t)(S - 64) * Hq * 128, (size_t)64 * Hq * 128 * 2,
+                    cudaMemcpyDeviceToDevice, st);
+  }
+  fill_f32<<<(Hq * 64 + 255) / 256, 256, 0, st>>>(w.M, -INFINITY, Hq * 64);
+  cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
+  const dim3 grid((unsigned)((S_loc + kThreads - 1) / kThreads), Hq);
+  stage1_scores<<<grid, kThreads, 0, st>>>(g, w.qwin, static_cast<const __nv_bfloat16*>(k_loc),
+                                           w.t, w.M);
+  MT_TRY(check_launch("vs stage1"));
+  if (coll) MT_TRY(coll->allreduce_max(w.M, (size_t)Hq * 64, st));
+  stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
+  MT_TRY(check_launch("vs stage2"));
+  if (coll) MT_TRY(coll->allreduce_sum_u64(w.E, (size_t)Hq * 64, st));
+  if (dbg_colV) cudaMemsetAsync(dbg_colV, 0, (size_t)Hq * S * 8, st);
+  stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, coll ? w.keysV_loc : w.keysV,
+                                           coll ? w.keysP_loc : w.keysP, dbg_colV, dbg_blkP);
+  MT_TRY(check_launch("vs stage3"));
+  if (coll) {
+    MT_TRY(coll->allgather_keys(w.keysV_loc, w.keysV, Hq, S_loc, st));
+    MT_TRY(coll->allgather_keys(w.keysP_loc, w.keysP, Hq, nloc, st));
+  }
+  seg_offsets<<<1, 64, 0, st>>>(w.segV, Hq, S);
+  seg_offsets<<<1, 64, 0, st>>>(w.segP, Hq, nb);
+  size_t tb = w.cub_bytes;
+  if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysV, w.sortV, (int)(Hq * S), Hq,
+                                              w.segV, w.segV + 1, 0, kIdxBits + kScoreBits,
+                                              st) != cudaSuccess)
+    return fail(MT_ECUDA, "segmented sort (verticals) failed");
+  tb = w.cub_bytes;
+  if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb), Hq,
+                                              w.segP, w.segP + 1, 0, kIdxBits + kScoreBits,
+                                              st) != cudaSuccess)
+    return fail(MT_ECUDA, "segmented sort (slashes) failed");
+  cudaMemsetAsync(w.bitsV, 0, (size_t)Hq * ((S + 31) / 32) * 4, st);
+  cudaMemsetAsync(w.bitsP, 0, (size_t)Hq * ((nb + 31) / 32) * 4, st);
+  const uint64_t pq_v = (uint64_t)llrint((double)p_v * 16777216.0);
+  const uint64_t pq_s = (uint64_t)llrint((double)p_s * 16777216.0);
+  topp_mark<<<dim3(Hq, 2), 1024, 0, st>>>(w.sortV, w.sortP, S, nb, pq_v, pq_s, w.bitsV, w.bitsP,
+                                          nullptr);
+  MT_TRY(check_launch("vs topp"));
+  compact_bits<<<dim3(Hq, 2), 1024, 0, st>>>(w.bitsV, w.bitsP, S, nb, v_cnt, v_idx, v_stride,
+                                             s_cnt, s_off, s_stride);
+  return check_launch("vs compact");
+}
+
+}  // namespace mt
+
+// ---------------------------------------------------------------- C ABI
+using namespace mt;
+
+// distributed variant lives with the NCCL communicator (ring.cu)
+mt_status mt_build_vs_index_dist(mt_comm* comm, const mt_shape* sh, const mt_vs_params* prm,
+                                 const void* q, const void* k, mt_vs_index* out, void* ws,
+                                 size_t ws_bytes, mt_stream_t st);
+
+extern "C" size_t mt_build_vs_index_workspace_bytes(const mt_shape* sh, int world) {
+  if (!sh || world <= 0) return 0;
+  return vsidx_workspace_bytes(sh->seq_len, sh->n_q_heads, world);
+}
+
+static mt_status vs_validate(const mt_shape* sh, const mt_vs_params* prm, const void* q,
+                             const void* k, void* ws, size_t ws_bytes, int W) {
+  MT_TRY(check_shape(sh, W));
+  if (!prm) return fail(MT_ESHAPE, "params is NULL");
+  if (!(prm->p_v > 0.f && prm->p_v <= 1.f) || !(prm->p_s > 0.f && prm->p_s <= 1.f))
+    return fail(MT_ECONFIG, "p_v, p_s must lie in (0, 1] (got %g, %g)", prm->p_v, prm->p_s);
+  if (sh->seq_len > (1LL << 22)) return fail(MT_ESHAPE, "seq_len must be <= 2^22 for the index");
+  if (!q || !k) return fail(MT_ESHAPE, "NULL q/k");
+  const size_t need = vsidx_workspace_bytes(sh->seq_len, sh->n_q_heads, W);
+  if (!ws || ws_bytes < need) return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  return check_device();
+}
+
+extern "C" mt_status mt_build_vs_index(mt_comm* comm, const mt_shape* sh,
+                                       const mt_vs_params* prm, const void* q, const void* k,
+                                       mt_vs_index* out, void* ws, size_t ws_bytes,
+                                       mt_stream_t st) {
+  if (comm) return mt_build_vs_index_dist(comm, sh, prm, q, k, out, ws, ws_bytes, st);
+  MT_TRY(vs_validate(sh, prm, q, k, ws, ws_bytes, 1));
+  if (!out || !out->v_cnt || !out->v_idx || !out->s_cnt || !out->s_off)
+    return fail(MT_ESHAPE, "output index pointers must be non-NULL");
+  if (out->v_stride < sh->seq_len || out->s_stride < sh->seq_len / 64)
+    return fail(MT_ECAPACITY, "index capacity: need v_stride >= %lld, s_stride >= %lld",
+                (long long)sh->seq_len, (long long)(sh->seq_len / 64));
+  return vsidx_build(nullptr, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, 1, 0, prm->p_v,
+                     prm->p_s, q, k, out->v_cnt, out->v_idx, out->v_stride, out->s_cnt,
+                     out->s_off, out->s_stride, nullptr, nullptr, ws, st);
+}
+
+extern "C" mt_status mt_vs_column_scores(const mt_shape* sh, const void* q, const void* k,
+                                         uint64_t* col_scores, uint64_t* slash_scores, void* ws,
+                                         size_t ws_bytes, mt_stream_t st) {
+  mt_vs_params prm{1.f, 1.f};
+  MT_TRY(vs_validate(sh, &prm, q, k, ws, ws_bytes, 1));
+  if (!col_scores || !slash_scores) return fail(MT_ESHAPE, "NULL score outputs");
+  // Runs stages I1-I6 only; the lists go to scratch inside the workspace tail.
+  const int64_t S = sh->seq_len;
+  const int Hq = sh->n_q_heads;
+  VSIndexWs w = carve_vsidx(ws, S, Hq, 1);
+  (void)w;
+  using namespace vsi;
+  Geo g{S, S, Hq, sh->n_kv_heads, 1, 0};
+  cudaMemcpyAsync(w.qwin, static_cast<const __nv_bfloat16*>(q) + (size_t)(S - 64) * Hq * 128,
+                  (size_t)64 * Hq * 128 * 2, cudaMemcpyDeviceToDevice, st);
+  fill_f32<<<(Hq * 64 + 255) / 256, 256, 0, st>>>(w.M, -INFINITY, Hq * 64);
+  cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
+  const dim3 grid((unsigned)((S + kThreads - 1) / kThreads), Hq);
+  stage1_scores<<<grid, kThreads, 0, st>>>(g, w.qwin, static_cast<const __nv_bfloat16*>(k), w.t,
+                                           w.M);
+  stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
+  stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, w.keysV, w.keysP, col_scores,
+                                           slash_scores);
+  return check_launch("mt_vs_column_scores");
+}

@@ -116,3 +116,39 @@ def attn_fwd_step(seq_len: int, world: int, rank: int, origin: int, first: bool,
     _lib.check(L.mt_attn_fwd_step(ctypes.byref(sh), world, rank, origin, int(first), int(last),
                                   _ptr(q_loc), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(ci),
                                   _ptr(o), _ptr(o_acc), _ptr(lse), _ptr(ws), ws.numel(), _stream()))
+
+
+class VSParams(ctypes.Structure):
+    _fields_ = [("p_v", ctypes.c_float), ("p_s", ctypes.c_float)]
+
+
+def build_vs_index(q: torch.Tensor, k: torch.Tensor, p_v: float, p_s: float, comm=None,
+                   seq_len: int | None = None) -> VSIndex:
+    """Alg. 1 index on the GPU (mt_build_vs_index).  With `comm`, q/k are the
+    rank-local striped slices and `seq_len` is the global length."""
+    S = q.shape[0] if seq_len is None else seq_len
+    Hq = q.shape[1]
+    world = 1 if comm is None else comm.world
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_build_vs_index_workspace_bytes(ctypes.byref(sh), world))
+    idx = VSIndex.empty(S, Hq, device=q.device)
+    ci = idx.c_struct()
+    prm = VSParams(p_v, p_s)
+    _lib.check(L.mt_build_vs_index(None if comm is None else comm.handle, ctypes.byref(sh),
+                                   ctypes.byref(prm), _ptr(q), _ptr(k), ctypes.byref(ci),
+                                   _ptr(ws), ws.numel(), _stream()))
+    return idx
+
+
+def vs_column_scores(q: torch.Tensor, k: torch.Tensor):
+    """Test hook: exact Alg. 1 intermediate scores (uint64 as int64 tensors)."""
+    S, Hq, _ = q.shape
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_build_vs_index_workspace_bytes(ctypes.byref(sh), 1))
+    col = torch.zeros(Hq, S, dtype=torch.int64, device=q.device)
+    sl = torch.zeros(Hq, S // BLOCK, dtype=torch.int64, device=q.device)
+    _lib.check(L.mt_vs_column_scores(ctypes.byref(sh), _ptr(q), _ptr(k), _ptr(col), _ptr(sl),
+                                     _ptr(ws), ws.numel(), _stream()))
+    return col, sl

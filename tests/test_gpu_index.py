@@ -1,0 +1,67 @@
+"""GPU Alg. 1 index (mt_build_vs_index) vs the VS-IDX v1 oracle: bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import vsidx
+from paper_2510_18830_b200 import ops
+from synth.generator import bf16_bits_to_f32, make_qkv
+from tests.gpu_util import to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_scores(q, k):
+    S, Hq, _ = q.shape
+    grp = Hq // k.shape[1]
+    qf, kf = bf16_bits_to_f32(q), bf16_bits_to_f32(k)
+    cols, sl = [], []
+    for h in range(Hq):
+        V = vsidx.column_scores(np.ascontiguousarray(qf[S - 64:, h]), np.ascontiguousarray(kf[:, h // grp]))
+        cols.append(V)
+        sl.append(V.reshape(-1, 64).sum(axis=1, dtype=np.uint64)[::-1])
+    return np.stack(cols), np.stack(sl)
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,seed", [(4096, 8, 1, 11), (8192, 4, 2, 12)])
+def test_column_scores_bitexact(cuda_lib, S, Hq, Hkv, seed):
+    q, k, _ = make_qkv(S, Hq, Hkv, seed=seed)
+    col, sl = ops.vs_column_scores(to_dev_bf16(q), to_dev_bf16(k))
+    torch.cuda.synchronize()
+    ref_c, ref_s = _oracle_scores(q, k)
+    assert np.array_equal(col.cpu().numpy().view(np.uint64), ref_c)
+    assert np.array_equal(sl.cpu().numpy().view(np.uint64), ref_s)
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,p", [(4096, 8, 1, 0.9), (4096, 8, 1, 0.97), (65536, 16, 2, 0.9),
+                                        (2048, 2, 1, 1.0)])
+def test_index_lists_bitexact(cuda_lib, S, Hq, Hkv, p):
+    q, k, _ = make_qkv(S, Hq, Hkv, seed=S + Hq)
+    idx = ops.build_vs_index(to_dev_bf16(q), to_dev_bf16(k), p, p)
+    torch.cuda.synchronize()
+    iv, is_ = idx.to_lists()
+    riv, ris = vsidx.build_vs_index(bf16_bits_to_f32(q), bf16_bits_to_f32(k), p, p)
+    for h in range(Hq):
+        assert np.array_equal(iv[h], riv[h]), (h, len(iv[h]), len(riv[h]))
+        assert np.array_equal(is_[h], ris[h]), (h, len(is_[h]), len(ris[h]))
+    if p == 1.0:
+        assert all(len(x) == S for x in iv) and all(len(x) == S // 64 for x in is_)
+
+
+def test_index_deterministic_and_forced(cuda_lib):
+    S, Hq, Hkv = 8192, 4, 1
+    q, k, _ = make_qkv(S, Hq, Hkv, seed=3)
+    qd, kd = to_dev_bf16(q), to_dev_bf16(k)
+    a = ops.build_vs_index(qd, kd, 0.9, 0.9).to_lists()
+    b = ops.build_vs_index(qd, kd, 0.9, 0.9).to_lists()
+    for x, y in zip(a[0] + a[1], b[0] + b[1]):
+        assert np.array_equal(x, y)
+    assert all(x[0] == 0 for x in a[0]) and all(x[0] == 0 for x in a[1])
+
+
+def test_index_rejects_bad_p(cuda_lib):
+    from paper_2510_18830_b200 import _lib
+    q = torch.zeros(128, 2, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(_lib.MTError) as e:
+        ops.build_vs_index(q, q[:, :1].contiguous(), 0.0, 0.5)
+    assert e.value.name == "MT_ECONFIG"
