@@ -168,6 +168,42 @@ mt_status mt_attn_fwd_step(const mt_shape* shape, int world, int rank, int origi
                            const void* v_chunk, const mt_vs_index* idx, void* o, float* o_acc,
                            float* lse, void* ws, size_t ws_bytes, mt_stream_t stream);
 
+/* Workspace (bytes) of mt_sparse_attn_bwd (single GPU). */
+size_t mt_sparse_attn_bwd_workspace_bytes(const mt_shape* shape);
+
+/* Single-GPU sparse attention backward with the forward's index held fixed
+ * ("superposition of the forward-phase sparsity"): Eq. 1 and
+ * Eq. 12 restricted to each query's key set K_n:
+ *   P = exp(q k^T / sqrt(d) - LSE), D = rowsum(dO o O), dS = P o (dO v^T - D),
+ *   dV = P^T dO, dK = dS^T Q / sqrt(d), dQ = dS K / sqrt(d)
+ * (GQA: dK/dV of a kv head sum over its q heads).  o/lse are the forward's
+ * outputs; dq [S][Hq][128], dk/dv [S][Hkv][128] bf16 out (fp32 accumulation
+ * inside the workspace).  Errors as mt_sparse_attn_fwd. */
+mt_status mt_sparse_attn_bwd(const mt_shape* shape, const void* q, const void* k, const void* v,
+                             const void* o, const float* lse, const void* dO,
+                             const mt_vs_index* idx, void* dq, void* dk, void* dv, void* ws,
+                             size_t ws_bytes, mt_stream_t stream);
+
+/* Workspace (bytes) of mt_attn_fwd_step / mt_attn_bwd_step for `world` ranks. */
+size_t mt_attn_step_workspace_bytes(const mt_shape* shape, int world);
+
+/* Backward preprocessing for one rank: D_loc[h][n] = dO_n . O_n (float32
+ * [Hq][S/W]) — the sum_j dL/dA_ij A_ij term of Eq. 1. */
+mt_status mt_attn_bwd_preprocess(const mt_shape* shape, int world, const void* o_loc,
+                                 const void* dO_loc, float* D_loc, mt_stream_t stream);
+
+/* One ring step of the backward (Table 4 "attention computation for a chunk"
+ * plus "backward for vertical lines") for rank `rank` holding the
+ * KV chunk of origin `origin`: reduce-adds the contributions of the rank's
+ * local queries into dq_acc [S/W][Hq][128] (float32, local queries) and into
+ * dk_acc/dv_acc [S/W][Hkv][128] (float32, the chunk's keys).  Accumulators are
+ * caller-initialised.  Exported so one GPU can emulate every (rank, step). */
+mt_status mt_attn_bwd_step(const mt_shape* shape, int world, int rank, int origin,
+                           const void* q_loc, const void* k_chunk, const void* v_chunk,
+                           const void* dO_loc, const float* lse_loc, const float* D_loc,
+                           const mt_vs_index* idx, float* dq_acc, float* dk_acc, float* dv_acc,
+                           void* ws, size_t ws_bytes, mt_stream_t stream);
+
 /* ------------------------------------------------------------------ tests */
 /* Hardware self-test hook (not part of the attention API): one 128-row tcgen05
  * MMA configuration on one CTA, see csrc/selftest.cu for the variants.

@@ -102,3 +102,118 @@ extern "C" mt_status mt_sparse_attn_fwd(const mt_shape* sh, const void* q, const
                                         mt_stream_t stream) {
   return mt_attn_fwd_step(sh, 1, 0, 0, 1, 1, q, k, v, idx, o, nullptr, lse, ws, ws_bytes, stream);
 }
+
+// ------------------------------------------------------------------ backward
+namespace mt {
+mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* q,
+                        const void* k, const void* v, const void* dO, const float* lse,
+                        const float* D, float* dq, float* dk, float* dv, int num_sms,
+                        cudaStream_t st);
+mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
+                              cudaStream_t st);
+mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st);
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct BwdWs {
+  void* plan;
+  float* D;
+  float* dq;
+  float* dk;
+  float* dv;
+  size_t total;
+};
+
+static BwdWs carve_bwd(void* base, const mt_shape* sh) {
+  const int64_t S = sh->seq_len;
+  const int Hq = sh->n_q_heads, Hkv = sh->n_kv_heads;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    void* r = p ? p + off : nullptr;
+    off = align256(off + b);
+    return r;
+  };
+  BwdWs w{};
+  w.plan = take(vs_plan_bytes(S, Hq, 1));
+  w.D = (float*)take((size_t)Hq * S * 4);
+  w.dq = (float*)take((size_t)S * Hq * 128 * 4);
+  w.dk = (float*)take((size_t)S * Hkv * 128 * 4);
+  w.dv = (float*)take((size_t)S * Hkv * 128 * 4);
+  w.total = off;
+  return w;
+}
+}  // namespace mt
+
+extern "C" size_t mt_sparse_attn_bwd_workspace_bytes(const mt_shape* sh) {
+  if (!sh) return 0;
+  return carve_bwd(nullptr, sh).total;
+}
+
+extern "C" size_t mt_attn_step_workspace_bytes(const mt_shape* sh, int world) {
+  if (!sh || world <= 0) return 0;
+  return vs_plan_bytes(sh->seq_len, sh->n_q_heads, world);
+}
+
+extern "C" mt_status mt_sparse_attn_bwd(const mt_shape* sh, const void* q, const void* k,
+                                        const void* v, const void* o, const float* lse,
+                                        const void* dO, const mt_vs_index* idx, void* dq,
+                                        void* dk, void* dv, void* ws, size_t ws_bytes,
+                                        mt_stream_t stream) {
+  MT_TRY(check_shape(sh, 1));
+  MT_TRY(check_index(idx, sh));
+  if (!q || !k || !v || !o || !lse || !dO || !dq || !dk || !dv)
+    return fail(MT_ESHAPE, "NULL tensor");
+  BwdWs w = carve_bwd(ws, sh);
+  if (!ws || ws_bytes < w.total)
+    return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, w.total);
+  MT_TRY(check_device());
+  const int64_t S = sh->seq_len;
+  const int Hq = sh->n_q_heads, Hkv = sh->n_kv_heads;
+  VSPlan plan;
+  MT_TRY(vs_plan_build(&plan, S, Hq, Hkv, 1, idx->v_cnt, idx->v_idx, idx->v_stride, idx->s_cnt,
+                       idx->s_off, (int)idx->s_stride, w.plan, stream));
+  MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream));
+  cudaMemsetAsync(w.dq, 0, (size_t)S * Hq * 128 * 4, stream);
+  cudaMemsetAsync(w.dk, 0, (size_t)S * Hkv * 128 * 4, stream);
+  cudaMemsetAsync(w.dv, 0, (size_t)S * Hkv * 128 * 4, stream);
+  MT_TRY(attn_bwd_step(plan, 0, 0, (int)(S / 64), q, k, v, dO, lse, w.D, w.dq, w.dk, w.dv,
+                       device_num_sms(), stream));
+  MT_TRY(f32_to_bf16(w.dq, dq, S * Hq * 128, stream));
+  MT_TRY(f32_to_bf16(w.dk, dk, S * Hkv * 128, stream));
+  return f32_to_bf16(w.dv, dv, S * Hkv * 128, stream);
+}
+
+extern "C" mt_status mt_attn_bwd_preprocess(const mt_shape* sh, int world, const void* o_loc,
+                                            const void* dO_loc, float* D_loc,
+                                            mt_stream_t stream) {
+  MT_TRY(check_shape(sh, world));
+  if (!o_loc || !dO_loc || !D_loc) return fail(MT_ESHAPE, "NULL tensor");
+  return attn_bwd_preprocess(o_loc, dO_loc, D_loc, sh->seq_len / world, sh->n_q_heads, stream);
+}
+
+extern "C" mt_status mt_attn_bwd_step(const mt_shape* sh, int world, int rank, int origin,
+                                      const void* q_loc, const void* k_chunk,
+                                      const void* v_chunk, const void* dO_loc,
+                                      const float* lse_loc, const float* D_loc,
+                                      const mt_vs_index* idx, float* dq_acc, float* dk_acc,
+                                      float* dv_acc, void* ws, size_t ws_bytes,
+                                      mt_stream_t stream) {
+  MT_TRY(check_shape(sh, world));
+  MT_TRY(check_index(idx, sh));
+  if (rank < 0 || rank >= world || origin < 0 || origin >= world)
+    return fail(MT_ESHAPE, "rank/origin out of range");
+  if (!q_loc || !k_chunk || !v_chunk || !dO_loc || !lse_loc || !D_loc || !dq_acc || !dk_acc ||
+      !dv_acc)
+    return fail(MT_ESHAPE, "NULL tensor");
+  const size_t need = mt_attn_step_workspace_bytes(sh, world);
+  if (!ws || ws_bytes < need) return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  MT_TRY(check_device());
+  VSPlan plan;
+  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, world, idx->v_cnt,
+                       idx->v_idx, idx->v_stride, idx->s_cnt, idx->s_off, (int)idx->s_stride, ws,
+                       stream));
+  return attn_bwd_step(plan, rank, origin, (int)(sh->seq_len / 64 / world), q_loc, k_chunk,
+                       v_chunk, dO_loc, lse_loc, D_loc, dq_acc, dk_acc, dv_acc,
+                       device_num_sms(), stream);
+}

@@ -1,0 +1,676 @@
+// attn_bwd.cu — block-sparse vertical-slash attention backward for sm_100a, one
+// ring step.  PAPER.md Eq. 1 and Eq. 12:
+//   P = exp(S - LSE), dP = dO V^T, dS = P o (dP - D), D_n = dO_n . O_n,
+//   dV = P^T dO, dK = dS^T Q / sqrt(d), dQ = dS K / sqrt(d),
+// with the forward's sparsity ("superposition"): the same key sets.
+//
+// Key-major ("column-parallel") tiles: the 128 key rows of a tile stay in smem
+// and their dK/dV accumulate in TMEM over every (q head, query block) chunk
+// that attends them; dQ of each chunk is reduce-added to an fp32 accumulator.
+//   mode BLOCK: tile = kv head g x local key blocks (lb0, lb0+1) of the held
+//               chunk; chunks = (q head h of the group, local query block j)
+//               with g_q - kb = o for a selected slash o (o = t mod W).  dK/dV
+//               rows are owned by the tile -> plain read-add-write.
+//   mode BAR  : tile = q head h x 128 consecutive entries of the origin's
+//               vertical list; chunks = every later local query block; a
+//               (column, block) pair is live iff the column is not covered by a
+//               selected slash of that block (I9).  dK/dV -> atomic scatter-add
+//               (the paper's "backward for all vertical lines").
+// Per chunk (M = 128 keys, N = 64 queries):
+//   S^T = K Q^T, dP^T = V dO^T              (tcgen05 -> TMEM)
+//   P^T, dS^T (bf16, dS pre-scaled by 1/sqrt d) in registers -> smem
+//   dV += P^T dO, dK += dS^T Q              (TMEM accumulators, N = 128)
+//   dQ^T = K^T dS^T                          (TMEM, M = d) -> red.add to dQ
+// Warp roles: warp 0 producer (TMA / cp.async), warp 1 MMA issuer,
+// warps 2..5 softmax-backward + dQ drain + dK/dV epilogue.
+#include "common.cuh"
+#include "plan.cuh"
+#include "sm100.cuh"
+#include "tmap.cuh"
+
+namespace mt {
+
+namespace bwd {
+
+constexpr int kStages = 3;
+constexpr int kThreads = 192;
+constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
+constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
+constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
+
+enum : int { kModeBlock = 0, kModeBar = 1 };
+enum : int { kChunk = 0, kEnd = 1 };
+
+// TMEM columns
+constexpr uint32_t kColDK = 0, kColDV = 128, kColS = 256, kColDP = 320, kColDQ = 384;
+
+struct ChunkMeta {
+  int kind;
+  int h;        // q head
+  int j;        // local query block
+  uint32_t flags;  // BLOCK: bit0/1 slot0/1 live, bit2/3 slot0/1 diagonal
+  int stage;    // smem stage holding the chunk's Q / dO / LSE / D
+  int pad;
+};
+
+struct Smem {
+  uint8_t k[kTileKV];
+  uint8_t v[kTileKV];
+  uint8_t q[kStages][kTileQ];
+  uint8_t dO[kStages][kTileQ];
+  uint8_t pT[kTileP];
+  uint8_t dsT[kTileP];
+  float lse[kStages][64];
+  float dd[kStages][64];
+  ChunkMeta meta[kStages];
+  ChunkMeta smeta;          // handed to the softmax (single S buffer)
+  int cols[128];            // BAR: global column of each key row (-1 = padding)
+  int tile_rows;            // BAR: live rows in the tile
+  uint64_t full[kStages], empty[kStages];
+  uint64_t kvfull, kvempty, sfull, sfree, dsfull, dqfull;
+  uint32_t tmem_base;
+};
+
+struct Params {
+  VSPlan plan;
+  int mode;
+  int r, s, t;              // rank, origin, step residue
+  int nloc;                 // local blocks per rank (queries and keys)
+  int n_tiles;              // BLOCK: Hkv * ceil(nloc/2); BAR: upper bound (per-head lists)
+  float scale_log2;         // log2(e)/sqrt(d)
+  float inv_sqrt_d;
+  const __nv_bfloat16* k;   // held chunk [S_loc][Hkv][128]
+  const __nv_bfloat16* v;
+  const float* lse;         // [Hq][S_loc] natural log
+  const float* dvec;        // [Hq][S_loc] D = rowsum(dO o O)
+  float* dq;                // [S_loc][Hq][128] fp32 accumulator (reduce-add)
+  float* dk;                // [S_loc][Hkv][128] fp32 accumulator of the held chunk
+  float* dv;
+};
+
+// ---- tile decoding
+struct Tile {
+  bool ok;
+  int g;       // kv head
+  int h;       // BAR: q head
+  int lb0;     // BLOCK: first local key block
+  int e0, e1;  // BAR: entry range in vcol (absolute)
+};
+
+__device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
+  Tile T{};
+  const VSPlan& pl = P.plan;
+  const int W = pl.W;
+  if (P.mode == kModeBlock) {
+    const int npairs = (P.nloc + 1) / 2;
+    if (tile >= pl.Hkv * npairs) return T;
+    T.ok = true;
+    T.g = tile % pl.Hkv;
+    T.lb0 = 2 * (tile / pl.Hkv);  // early key blocks (most work) first
+    return T;
+  }
+  // BAR: walk heads, ceil(len/128) tiles each
+  int base = 0;
+  for (int h = 0; h < pl.Hq; ++h) {
+    const int b = pl.vptr[h * (W + 1) + P.s], e = pl.vptr[h * (W + 1) + P.s + 1];
+    const int n = (e - b + 127) / 128;
+    if (tile < base + n) {
+      T.ok = true;
+      T.h = h;
+      T.g = h / (pl.Hq / pl.Hkv);
+      T.e0 = b + (tile - base) * 128;
+      T.e1 = min(e, T.e0 + 128);
+      return T;
+    }
+    base += n;
+  }
+  return T;
+}
+
+// ------------------------------------------------------------------ producer
+__device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
+                         const CUtensorMap* tmdo, const CUtensorMap* tmk,
+                         const CUtensorMap* tmv) {
+  const int lane = lane_id();
+  const VSPlan& pl = P.plan;
+  const int W = pl.W;
+  const int grp = pl.Hq / pl.Hkv;
+  const int64_t S_loc = (int64_t)P.nloc * 64;
+  int stage = 0;
+  uint32_t ephase = 0, kve_phase = 0;
+  bool first_tile = true;
+  auto next_stage = [&]() {
+    if (++stage == kStages) { stage = 0; ephase ^= 1; }
+  };
+  auto emit = [&](int h, int j, uint32_t flags) {
+    mbar_wait(smem_u32(&sm.empty[stage]), ephase ^ 1);
+    if (lane == 0) {
+      ChunkMeta& m = sm.meta[stage];
+      m.kind = kChunk;
+      m.h = h;
+      m.j = j;
+      m.flags = flags;
+      const uint32_t bar = smem_u32(&sm.full[stage]);
+      mbar_expect_tx(bar, 2 * kTileQ + 512);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_3d(smem_u32(sm.q[stage] + c * 8192), tmq, bar, c * 64, h, j * 64);
+        tma_load_3d(smem_u32(sm.dO[stage] + c * 8192), tmdo, bar, c * 64, h, j * 64);
+      }
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
+              smem_u32(sm.lse[stage])),
+          "l"(P.lse + (int64_t)h * S_loc + (int64_t)j * 64), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
+              smem_u32(sm.dd[stage])),
+          "l"(P.dvec + (int64_t)h * S_loc + (int64_t)j * 64), "r"(bar)
+          : "memory");
+    }
+    __syncwarp();
+    next_stage();
+  };
+
+  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+    const Tile T = decode_tile(P, tile);
+    if (!T.ok) break;
+    // ---- K/V tile (held until every chunk of the tile finished)
+    if (!first_tile) {
+      mbar_wait(smem_u32(&sm.kvempty), kve_phase);
+      kve_phase ^= 1;
+    }
+    first_tile = false;
+    const uint32_t kvbar = smem_u32(&sm.kvfull);
+    if (P.mode == kModeBlock) {
+      const bool v1 = T.lb0 + 1 < P.nloc;
+      if (lane == 0) {
+        // a missing second slot re-loads block lb0: every K/V row must be finite
+        // because dQ^T = K^T dS^T contracts over all 128 rows (masked rows have dS = 0)
+        mbar_expect_tx(kvbar, 2 * kTileKV);
+        for (int sl = 0; sl < 2; ++sl)
+          for (int c = 0; c < 2; ++c) {
+            const uint32_t off = c * 16384 + sl * 8192;
+            const int blk = v1 ? T.lb0 + sl : T.lb0;
+            tma_load_3d(smem_u32(sm.k + off), tmk, kvbar, c * 64, T.g, blk * 64);
+            tma_load_3d(smem_u32(sm.v + off), tmv, kvbar, c * 64, T.g, blk * 64);
+          }
+      }
+      __syncwarp();
+    } else {
+      const int n = T.e1 - T.e0;
+      const int32_t* vc = pl.vcol + (int64_t)T.h * pl.S;
+      for (int rr = lane; rr < 128; rr += 32) {
+        int m = rr < n ? vc[T.e0 + rr] : -1;
+        sm.cols[rr] = m;
+      }
+      if (lane == 0) sm.tile_rows = n;
+      __syncwarp();
+      const uint32_t kb = smem_u32(sm.k), vb = smem_u32(sm.v);
+      const int m0 = sm.cols[0];
+      for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
+        const int row = pidx >> 4, c16 = pidx & 15;
+        int m = sm.cols[row];
+        if (m < 0) m = m0;  // padding rows duplicate a live row (masked later)
+        const int blk = m >> 6;
+        const int64_t lrow = (int64_t)((blk - P.s) / W) * 64 + (m & 63);
+        const size_t goff = ((size_t)lrow * pl.Hkv + T.g) * 128 + c16 * 8;
+        const uint32_t doff = (c16 >> 3) * 16384 + sw128(row, c16 & 7);
+        cp_async_16(kb + doff, P.k + goff);
+        cp_async_16(vb + doff, P.v + goff);
+      }
+      asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(kvbar) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(kvbar);
+    }
+
+    // ---- chunk stream
+    if (P.mode == kModeBlock) {
+      const bool v1 = T.lb0 + 1 < P.nloc;
+      const int kb0 = T.lb0 * W + P.s;
+      const int kb1 = v1 ? kb0 + W : -1;
+      for (int hh = 0; hh < grp; ++hh) {
+        const int h = T.g * grp + hh;
+        const int ns = pl.s_cnt[h];
+        const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
+        // query blocks gq = kb + o for o = t (mod W), merged over the two key slots
+        int ia = 0, ib = 0;
+        auto next_valid = [&](int i, int kb) {
+          if (kb < 0) return ns;
+          while (i < ns) {
+            const int o = offs[i];
+            if (kb + o >= pl.nb) return ns;  // ascending offsets: no later match
+            if ((o % W) == P.t) break;
+            ++i;
+          }
+          return i;
+        };
+        ia = next_valid(0, kb0);
+        ib = next_valid(0, kb1);
+        while (ia < ns || ib < ns) {
+          const int qa = ia < ns ? kb0 + offs[ia] : INT32_MAX;
+          const int qb = ib < ns ? kb1 + offs[ib] : INT32_MAX;
+          const int gq = min(qa, qb);
+          uint32_t flags = 0;
+          if (qa == gq) { flags |= 1u; if (offs[ia] == 0) flags |= 4u; ia = next_valid(ia + 1, kb0); }
+          if (qb == gq) { flags |= 2u; if (offs[ib] == 0) flags |= 8u; ib = next_valid(ib + 1, kb1); }
+          emit(h, (gq - P.r) / W, flags);
+        }
+      }
+    } else {
+      const int mfirst = sm.cols[0];
+      const int bfirst = mfirst >> 6;
+      // first rank-local query block with global block > bfirst
+      int j = (bfirst + 1 - P.r + W - 1) / W;
+      if (bfirst + 1 - P.r <= 0) j = 0;
+      for (; j < P.nloc; ++j) emit(T.h, j, 0u);
+    }
+    // ---- END
+    mbar_wait(smem_u32(&sm.empty[stage]), ephase ^ 1);
+    if (lane == 0) {
+      sm.meta[stage].kind = kEnd;
+      mbar_arrive(smem_u32(&sm.full[stage]));
+    }
+    __syncwarp();
+    next_stage();
+  }
+}
+
+// ------------------------------------------------------------------ MMA issuer
+__device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
+  const uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // S^T, dP^T
+  const uint32_t id_kv = make_idesc_bf16(128, 128, false, true);  // dV, dK
+  const uint32_t id_q = make_idesc_bf16(128, 64, true, true);     // dQ^T
+  const uint32_t k0 = smem_u32(sm.k), v0 = smem_u32(sm.v);
+  const uint32_t pT = smem_u32(sm.pT), dsT = smem_u32(sm.dsT);
+  int stage = 0;
+  uint32_t fphase = 0, kvf_phase = 0, sfree_phase = 0, dsf_phase = 0;
+  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+    const Tile T = decode_tile(P, tile);
+    if (!T.ok) break;
+    mbar_wait(smem_u32(&sm.kvfull), kvf_phase);
+    kvf_phase ^= 1;
+    if (P.mode == kModeBar) fence_proxy_async_smem();
+    tc_fence_after();
+    bool have_prev = false, acc_started = false;
+    int prev_stage = 0;
+    for (;;) {
+      mbar_wait(smem_u32(&sm.full[stage]), fphase);
+      const int kind = sm.meta[stage].kind;
+      tc_fence_after();
+      mbar_wait(smem_u32(&sm.sfree), sfree_phase ^ 1);
+      sfree_phase ^= 1;
+      sm.smeta = sm.meta[stage];
+      sm.smeta.stage = stage;
+      mbar_arrive(smem_u32(&sm.sfull));  // 1st arrival publishes smeta
+      if (kind == kChunk) {
+        const uint32_t qs = smem_u32(sm.q[stage]), dos = smem_u32(sm.dO[stage]);
+#pragma unroll
+        for (int kk = 0; kk < 128; kk += 16) {
+          const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
+          const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
+          mma_ss(tmem + kColS, make_sdesc(k0 + ko, 16, 1024), make_sdesc(qs + qo, 16, 1024),
+                 id_s, kk > 0);
+          mma_ss(tmem + kColDP, make_sdesc(v0 + ko, 16, 1024), make_sdesc(dos + qo, 16, 1024),
+                 id_s, kk > 0);
+        }
+        mma_commit(smem_u32(&sm.sfull));  // 2nd arrival: S^T, dP^T ready
+      } else {
+        mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
+      }
+      if (have_prev) {
+        mbar_wait(smem_u32(&sm.dsfull), dsf_phase);
+        dsf_phase ^= 1;
+        tc_fence_after();
+        const uint32_t qs = smem_u32(sm.q[prev_stage]), dos = smem_u32(sm.dO[prev_stage]);
+#pragma unroll
+        for (int kq = 0; kq < 64; kq += 16) {
+          const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
+          mma_ss(tmem + kColDV, make_sdesc(pT + kq * 2, 16, 1024),
+                 make_sdesc(dos + kq * 128, 8192, 1024), id_kv, acc);
+          mma_ss(tmem + kColDK, make_sdesc(dsT + kq * 2, 16, 1024),
+                 make_sdesc(qs + kq * 128, 8192, 1024), id_kv, acc);
+        }
+        acc_started = true;
+#pragma unroll
+        for (int kk = 0; kk < 128; kk += 16)
+          mma_ss(tmem + kColDQ, make_sdesc(k0 + kk * 128, 16384, 1024),
+                 make_sdesc(dsT + kk * 128, 8192, 1024), id_q, kk > 0);
+        mma_commit(smem_u32(&sm.dqfull));
+        mma_commit(smem_u32(&sm.empty[prev_stage]));
+      }
+      if (kind == kEnd) {
+        mbar_arrive(smem_u32(&sm.empty[stage]));
+        mbar_arrive(smem_u32(&sm.sfull));
+      }
+      have_prev = (kind == kChunk);
+      prev_stage = stage;
+      if (++stage == kStages) { stage = 0; fphase ^= 1; }
+      if (kind == kEnd) break;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ softmax-backward
+__device__ __forceinline__ void red_add_f32(float* addr, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+__device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
+  const int wq = warp_id() & 3;
+  const int row = wq * 32 + lane_id();   // key row of the tile == TMEM lane; d index for dQ^T
+  const int slot = row >> 6, kk = row & 63;
+  const uint32_t lb = (uint32_t)(wq * 32) << 16;
+  const VSPlan& pl = P.plan;
+  const int Hq = pl.Hq, W = pl.W;
+  const size_t qstride = (size_t)Hq * 128;
+  uint32_t sfull_phase = 0, dq_phase = 0;
+  const uint32_t prow = smem_u32(sm.pT) + row * 128, drow = smem_u32(sm.dsT) + row * 128;
+
+  // dQ^T row `row` (= d index) of the last chunk -> dQ[q][h][row] for its 64 queries
+  auto drain_dq = [&](int h, int j) {
+    mbar_wait(smem_u32(&sm.dqfull), dq_phase);
+    dq_phase ^= 1;
+    tc_fence_after();
+    uint32_t r0[32], r1[32];
+    tmem_ld32(tmem + lb + kColDQ, r0);
+    tmem_ld32(tmem + lb + kColDQ + 32, r1);
+    tmem_ld_wait();
+    float* base = P.dq + (size_t)j * 64 * qstride + (size_t)h * 128 + row;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) red_add_f32(base + c * qstride, __uint_as_float(r0[c]));
+#pragma unroll
+    for (int c = 0; c < 32; ++c) red_add_f32(base + (c + 32) * qstride, __uint_as_float(r1[c]));
+  };
+
+  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+    const Tile T = decode_tile(P, tile);
+    if (!T.ok) break;
+    int my_col = -2;  // BAR: resolved after the first chunk (cols[] published via kvfull->MMA)
+    int prev_h = -1, prev_j = -1;
+    for (;;) {
+      mbar_wait(smem_u32(&sm.sfull), sfull_phase);
+      sfull_phase ^= 1;
+      const ChunkMeta cm = sm.smeta;
+      if (cm.kind == kEnd) {
+        mbar_arrive(smem_u32(&sm.sfree));
+        break;
+      }
+      if (P.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
+      tc_fence_after();
+      uint32_t sv[64], dpv[64];
+      tmem_ld32(tmem + lb + kColS, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+      tmem_ld32(tmem + lb + kColS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+      tmem_ld32(tmem + lb + kColDP, *reinterpret_cast<uint32_t(*)[32]>(&dpv[0]));
+      tmem_ld32(tmem + lb + kColDP + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(smem_u32(&sm.sfree));
+      // which of the 64 queries see this key row
+      uint64_t vis;
+      if (P.mode == kModeBlock) {
+        const bool live = (cm.flags >> slot) & 1u;
+        const bool diag = (cm.flags >> (2 + slot)) & 1u;
+        vis = live ? (diag ? (~0ull << kk) : ~0ull) : 0ull;   // causal: query i >= key kk
+        if (slot == 1 && T.lb0 + 1 >= P.nloc) vis = 0ull;
+      } else {
+        bool live = my_col >= 0;
+        if (live) {
+          const int gq = cm.j * W + P.r;
+          const int blk = my_col >> 6;
+          live = blk < gq && !plan_has_slash(pl, cm.h, gq - blk);
+        }
+        vis = live ? ~0ull : 0ull;
+      }
+      const float* lse_s = sm.lse[cm.stage];
+      const float* d_s = sm.dd[cm.stage];
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int c = 0; c < 64; c += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c);
+        const float4 d4 = *reinterpret_cast<const float4*>(d_s + c);
+        const float la[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float da[4] = {d4.x, d4.y, d4.z, d4.w};
+        float p[4], ds[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = c + u;
+          const bool on = (vis >> q) & 1ull;
+          const float x = __uint_as_float(sv[q]) * P.scale_log2 - la[u] * 1.4426950408889634f;
+          p[u] = on ? exp2f(x) : 0.f;
+          ds[u] = on ? p[u] * (__uint_as_float(dpv[q]) - da[u]) * P.inv_sqrt_d : 0.f;
+        }
+        pk[c >> 1] = pack_bf16x2(p[0], p[1]);
+        pk[(c >> 1) + 1] = pack_bf16x2(p[2], p[3]);
+        dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
+        dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
+      }
+      // previous chunk's dV/dK/dQ MMAs must be done (P^T/dS^T smem + dQ^T TMEM free)
+      if (prev_h >= 0) drain_dq(prev_h, prev_j);
+#pragma unroll
+      for (int c16 = 0; c16 < 8; ++c16) {
+        const uint32_t sw = (uint32_t)((c16 ^ (row & 7)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + sw), "r"(pk[4 * c16]),
+                     "r"(pk[4 * c16 + 1]), "r"(pk[4 * c16 + 2]), "r"(pk[4 * c16 + 3])
+                     : "memory");
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + sw), "r"(dk[4 * c16]),
+                     "r"(dk[4 * c16 + 1]), "r"(dk[4 * c16 + 2]), "r"(dk[4 * c16 + 3])
+                     : "memory");
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(smem_u32(&sm.dsfull));
+      prev_h = cm.h;
+      prev_j = cm.j;
+    }
+    if (prev_h >= 0) drain_dq(prev_h, prev_j);  // also: every MMA of the tile is complete
+
+    // ---- dK / dV epilogue (tile rows): fp32 accumulate into the held chunk's dK/dV
+    bool live_row;
+    int64_t lrow;
+    if (P.mode == kModeBlock) {
+      live_row = prev_h >= 0 && !(slot == 1 && T.lb0 + 1 >= P.nloc);
+      lrow = (int64_t)(T.lb0 + slot) * 64 + kk;
+    } else {
+      const int m = my_col;  // cached: the producer may already be refilling cols[]
+      live_row = prev_h >= 0 && m >= 0;
+      lrow = live_row ? (int64_t)(((m >> 6) - P.s) / W) * 64 + (m & 63) : 0;
+    }
+    float* dkp = P.dk + ((size_t)lrow * pl.Hkv + T.g) * 128;
+    float* dvp = P.dv + ((size_t)lrow * pl.Hkv + T.g) * 128;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      uint32_t a[32], b[32];
+      tmem_ld32(tmem + lb + kColDK + c0, a);
+      tmem_ld32(tmem + lb + kColDV + c0, b);
+      tmem_ld_wait();
+      if (!live_row) continue;
+      if (P.mode == kModeBlock) {
+        float4* k4 = reinterpret_cast<float4*>(dkp + c0);
+        float4* v4 = reinterpret_cast<float4*>(dvp + c0);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float4 x = k4[c], y = v4[c];
+          x.x += __uint_as_float(a[4 * c]);
+          x.y += __uint_as_float(a[4 * c + 1]);
+          x.z += __uint_as_float(a[4 * c + 2]);
+          x.w += __uint_as_float(a[4 * c + 3]);
+          y.x += __uint_as_float(b[4 * c]);
+          y.y += __uint_as_float(b[4 * c + 1]);
+          y.z += __uint_as_float(b[4 * c + 2]);
+          y.w += __uint_as_float(b[4 * c + 3]);
+          k4[c] = x;
+          v4[c] = y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          red_add_f32(dkp + c0 + c, __uint_as_float(a[c]));
+          red_add_f32(dvp + c0 + c, __uint_as_float(b[c]));
+        }
+      }
+    }
+    tc_fence_before();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
+                    const __grid_constant__ CUtensorMap tmdo,
+                    const __grid_constant__ CUtensorMap tmk,
+                    const __grid_constant__ CUtensorMap tmv) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  const int warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(smem_u32(&sm.full[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), 1);
+    }
+    mbar_init(smem_u32(&sm.kvfull), 1);
+    mbar_init(smem_u32(&sm.kvempty), 1);
+    mbar_init(smem_u32(&sm.sfull), 2);
+    mbar_init(smem_u32(&sm.sfree), 128);
+    mbar_init(smem_u32(&sm.dsfull), 128);
+    mbar_init(smem_u32(&sm.dqfull), 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(smem_u32(&sm.tmem_base), 512);
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch_desc(&tmq);
+    tma_prefetch_desc(&tmdo);
+    if (P.mode == kModeBlock) {
+      tma_prefetch_desc(&tmk);
+      tma_prefetch_desc(&tmv);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  if (warp == 0) {
+    producer(sm, P, &tmq, &tmdo, &tmk, &tmv);
+  } else if (warp == 1) {
+    if (lane_id() == 0) mma_issuer(sm, P, tmem);
+    __syncwarp();
+  } else {
+    softmax_bwd(sm, P, tmem);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// D_n = dO_n . O_n (Eq. 1's sum_j dL/dA_ij A_ij), one warp per (token, head) row.
+__global__ void bwd_preprocess_kernel(const __nv_bfloat16* o, const __nv_bfloat16* dO, float* D,
+                                      int64_t rows, int Hq, int64_t S_loc) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const uint2 a = reinterpret_cast<const uint2*>(o + w * 128)[lane];
+  const uint2 b = reinterpret_cast<const uint2*>(dO + w * 128)[lane];
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const float2 x = __bfloat1622float2(a2[u]), y = __bfloat1622float2(b2[u]);
+    s += x.x * y.x + x.y * y.y;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) {
+    const int64_t tok = w / Hq;
+    const int h = (int)(w % Hq);
+    D[(int64_t)h * S_loc + tok] = s;
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* x, __nv_bfloat16* y, int64_t n) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    uint2 o;
+    o.x = pack_bf16x2(v.x, v.y);
+    o.y = pack_bf16x2(v.z, v.w);
+    *reinterpret_cast<uint2*>(y + i) = o;
+  } else {
+    for (int64_t j = i; j < n; ++j) y[j] = __float2bfloat16_rn(x[j]);
+  }
+}
+
+}  // namespace bwd
+
+size_t bwd_smem_bytes() { return sizeof(bwd::Smem) + 1024; }
+
+mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
+                              cudaStream_t st) {
+  const int64_t rows = S_loc * Hq;
+  const int threads = 256;
+  const int64_t blocks = (rows * 32 + threads - 1) / threads;
+  bwd::bwd_preprocess_kernel<<<(unsigned)blocks, threads, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dO), D, rows, Hq,
+      S_loc);
+  return check_launch("bwd_preprocess");
+}
+
+mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st) {
+  const int64_t threads = 256, per = threads * 4;
+  bwd::f32_to_bf16_kernel<<<(unsigned)((n + per - 1) / per), (unsigned)threads, 0, st>>>(
+      x, static_cast<__nv_bfloat16*>(y), n);
+  return check_launch("f32_to_bf16");
+}
+
+// One ring step of the backward: block part then bar part, accumulating into
+// dq (local queries, fp32) and dk/dv (held chunk, fp32).
+mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* q,
+                        const void* k, const void* v, const void* dO, const float* lse,
+                        const float* D, float* dq, float* dk, float* dv, int num_sms,
+                        cudaStream_t st) {
+  using namespace bwd;
+  Params P{};
+  P.plan = plan;
+  P.r = r;
+  P.s = s;
+  P.t = ((r - s) % plan.W + plan.W) % plan.W;
+  P.nloc = nloc;
+  P.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
+  P.inv_sqrt_d = 1.f / sqrtf(128.f);
+  P.k = static_cast<const __nv_bfloat16*>(k);
+  P.v = static_cast<const __nv_bfloat16*>(v);
+  P.lse = lse;
+  P.dvec = D;
+  P.dq = dq;
+  P.dk = dk;
+  P.dv = dv;
+  const uint64_t S_loc = (uint64_t)nloc * 64;
+  CUtensorMap tmq, tmdo, tmk, tmv;
+  if (make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
+      make_tmap_bf16_3d(&tmdo, dO, 128, plan.Hq, S_loc, 64, 1, 64) ||
+      make_tmap_bf16_3d(&tmk, k, 128, plan.Hkv, S_loc, 64, 1, 64) ||
+      make_tmap_bf16_3d(&tmv, v, 128, plan.Hkv, S_loc, 64, 1, 64))
+    return fail(MT_ECUDA, "cuTensorMapEncodeTiled failed");
+  const size_t smem = bwd_smem_bytes();
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_bwd) failed");
+    attr_done = true;
+  }
+  // block (slash) part
+  P.mode = kModeBlock;
+  P.n_tiles = plan.Hkv * ((nloc + 1) / 2);
+  int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
+  if (grid > 0) attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv);
+  MT_TRY(check_launch("attn_bwd_kernel(block)"));
+  // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
+  P.mode = kModeBar;
+  P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128);
+  grid = num_sms;
+  attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv);
+  return check_launch("attn_bwd_kernel(bar)");
+}
+
+}  // namespace mt

@@ -152,3 +152,35 @@ def vs_column_scores(q: torch.Tensor, k: torch.Tensor):
     _lib.check(L.mt_vs_column_scores(ctypes.byref(sh), _ptr(q), _ptr(k), _ptr(col), _ptr(sl),
                                      _ptr(ws), ws.numel(), _stream()))
     return col, sl
+
+
+def sparse_attn_bwd(q, k, v, o, lse, dO, idx: VSIndex):
+    """Single-GPU backward -> (dq, dk, dv) bf16."""
+    S, Hq, _ = q.shape
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_sparse_attn_bwd_workspace_bytes(ctypes.byref(sh)))
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ci = idx.c_struct()
+    _lib.check(L.mt_sparse_attn_bwd(ctypes.byref(sh), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                    _ptr(dO), ctypes.byref(ci), _ptr(dq), _ptr(dk), _ptr(dv),
+                                    _ptr(ws), ws.numel(), _stream()))
+    return dq, dk, dv
+
+
+def attn_bwd_preprocess(seq_len: int, world: int, o_loc, dO_loc, D_loc):
+    sh = shape(seq_len, o_loc.shape[1], 1)
+    _lib.check(_lib.lib().mt_attn_bwd_preprocess(ctypes.byref(sh), world, _ptr(o_loc), _ptr(dO_loc),
+                                                 _ptr(D_loc), _stream()))
+
+
+def attn_bwd_step(seq_len: int, world: int, rank: int, origin: int, q_loc, k_chunk, v_chunk,
+                  dO_loc, lse_loc, D_loc, idx: VSIndex, dq_acc, dk_acc, dv_acc):
+    sh = shape(seq_len, q_loc.shape[1], k_chunk.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_attn_step_workspace_bytes(ctypes.byref(sh), world))
+    ci = idx.c_struct()
+    _lib.check(L.mt_attn_bwd_step(ctypes.byref(sh), world, rank, origin, _ptr(q_loc), _ptr(k_chunk),
+                                  _ptr(v_chunk), _ptr(dO_loc), _ptr(lse_loc), _ptr(D_loc),
+                                  ctypes.byref(ci), _ptr(dq_acc), _ptr(dk_acc), _ptr(dv_acc),
+                                  _ptr(ws), ws.numel(), _stream()))

@@ -51,7 +51,7 @@ CONFIGS = {
 # Generator strength `a` per sequence length, calibrated so the VS index at
 # p_v = p_s = 0.9 selects about 5% of the causal area ("sparsity 0.95").
 # See DESIGN.md §3 for the calibration run; realised density is always reported.
-DEFAULT_A = {4096: 17.0, 65536: 19.0, 131072: 19.5, 524288: 20.5, 1048576: 21.0}
+DEFAULT_A = {4096: 17.0, 65536: 19.0, 131072: 19.25, 524288: 20.5, 1048576: 21.0}
 DEFAULT_B = 12.0
 
 
