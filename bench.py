@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py — MTraining hot path on B200 (arXiv 2510.18830, BASELINE.json metric).
+
+One step = one pass of the whole hot path over one synthetic 512K-token
+Qwen2.5-3B-shaped attention layer (16 q heads, 2 kv heads, d = 128):
+  1. Alg. 1 vertical-slash index (mt_build_vs_index, bit-exact VS-IDX v1),
+  2. block-sparse attention forward (ring over N GPUs, or one GPU),
+  3. block-sparse attention backward (dQ, dK, dV).
+Metric: sparse attention fwd+bwd tokens/s at 512K (whole job, max over ranks),
+with the kernel-level roofline of the dominant kernel and the CPU oracle as a
+reported baseline.  Usage:
+  python bench.py [--gpus N --steps K --warmup W]            (N > 1 under torchrun)
+  python bench.py --impl reference ...                        (CPU oracle arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sparse attn fwd+bwd tokens/s at 512K, 1/2/4/8 B200; % of bf16 tensor peak"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seq", type=int, default=524288)
+    ap.add_argument("--hq", type=int, default=16)
+    ap.add_argument("--hkv", type=int, default=2)
+    ap.add_argument("--p", type=float, default=0.9)
+    ap.add_argument("--inner", type=int, default=0, help="hierarchical inner ring size (0 = flat)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ layout helpers
+def stripe_rows(S: int, W: int, r: int) -> np.ndarray:
+    """Global token of each local row of rank r (64-token block striping)."""
+    j = np.arange(S // W)
+    return ((j // 64) * W + r) * 64 + j % 64
+
+
+def bits_to_torch(bits: np.ndarray, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(dev)
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_sample(q, k, v, dO, p: float, S: int, Hq: int, Hkv: int, n_blocks: int = 24):
+    """Time the CPU oracle on a bounded sample of the workload; returns a dict.
+
+    Sample: the full Alg. 1 index of q head 0 (VS-IDX v1, C fast path) and the
+    fp64 forward + backward of `n_blocks` query blocks of head 0 spread over the
+    sequence.  Extrapolated to the whole job by head count (index) and by the
+    activated-pair count (attention).
+    """
+    from oracle import attention as OA
+    from oracle import sparseformat as SF
+    from oracle import vsidx
+    from paper_2510_18830_b200 import stats
+    from synth.generator import bf16_bits_to_f32
+    grp = Hq // Hkv
+    qf = bf16_bits_to_f32(q[:, :1])
+    kf = bf16_bits_to_f32(k[:, :1])
+    t0 = time.perf_counter()
+    iv, is_ = vsidx.vs_index_head(np.ascontiguousarray(qf[S - 64:, 0]), np.ascontiguousarray(kf[:, 0]), p, p)
+    t_idx = time.perf_counter() - t0
+    nb = S // 64
+    gs = np.unique(np.linspace(0, nb - 1, n_blocks).astype(int))
+    q64 = qf.astype(np.float64)
+    k64 = kf.astype(np.float64)
+    v64 = bf16_bits_to_f32(v[:, :1]).astype(np.float64)
+    d64 = bf16_bits_to_f32(dO[:, :1]).astype(np.float64)
+    O = np.zeros_like(q64)
+    L = np.zeros((1, S))
+    pairs = 0
+    t0 = time.perf_counter()
+    for g in gs:
+        B, C = SF.sparseformat_block(iv, is_, int(g))
+        rows = slice(g * 64, g * 64 + 64)
+        O[rows, 0], L[0, rows] = OA.forward_block(q64, k64, v64, 0, int(g), B, C)
+        OA.backward_block(q64, k64, v64, O, L, d64, 0, int(g), B, C)
+        pairs += int(len(B) * 4096 - (2016 if (len(B) and B[-1] == g) else 0) + 64 * len(C))
+    t_attn = time.perf_counter() - t0
+    tot_pairs = int(stats.pairs_per_head([iv], [is_], S)[0]) * Hq
+    t_job = t_idx * Hq + t_attn * tot_pairs / max(pairs, 1)
+    return {"value": S / t_job, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": (f"Alg.1 index of 1/{Hq} q heads ({t_idx:.1f} s) + fp64 fwd+bwd of {len(gs)} of "
+                       f"{nb} query blocks of head 0 ({t_attn:.1f} s, {pairs} of {tot_pairs} pairs); "
+                       f"extrapolated by heads and activated pairs"),
+            "seconds": t_idx + t_attn}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_18830_b200 import ops, stats
+    from synth.generator import make_grad_out, make_qkv
+
+    W = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if W != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={W}: launch with torchrun for N > 1")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if W > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = ops.Comm.create(W, rank, args.inner or W)
+    S, Hq, Hkv, p = args.seq, args.hq, args.hkv, args.p
+    q, k, v = make_qkv(S, Hq, Hkv, seed=args.seed)
+    dO = make_grad_out(S, Hq, seed=args.seed)
+    rows = stripe_rows(S, W, rank) if W > 1 else np.arange(S)
+    hq_, hk_, hv_, hdo = (np.ascontiguousarray(x[rows]) for x in (q, k, v, dO))
+    qd, kd, vd, dOd = (bits_to_torch(x, dev) for x in (hq_, hk_, hv_, hdo))
+    stream = torch.cuda.current_stream()
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def step(qx, kx, vx, dox, marks=None):
+        e = [ev() for _ in range(4)] if marks is not None else None
+        if e: e[0].record(stream)
+        idx = ops.build_vs_index(qx, kx, p, p, comm=comm, seq_len=S)
+        if e: e[1].record(stream)
+        if comm is None:
+            o, lse = ops.sparse_attn_fwd(qx, kx, vx, idx)
+        else:
+            o, lse = ops.ring_attn_fwd(comm, S, qx, kx, vx, idx)
+        if e: e[2].record(stream)
+        if comm is None:
+            g = ops.sparse_attn_bwd(qx, kx, vx, o, lse, dox, idx)
+        else:
+            g = ops.ring_attn_bwd(comm, S, qx, kx, vx, o, lse, dox, idx)
+        if e:
+            e[3].record(stream)
+            marks.append(e)
+        return idx, g
+
+    def barrier():
+        if W > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        idx, _ = step(qd, kd, vd, dOd)
+    torch.cuda.synchronize()
+    iv, is_ = idx.to_lists()
+    pairs = int(stats.pairs_per_head(iv, is_, S).sum())
+    dens = pairs / (Hq * stats.causal_pairs(S))
+
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    t0, t1 = ev(), ev()
+    marks = []
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(qd, kd, vd, dOd, marks)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    ph = np.array([[m[0].elapsed_time(m[1]), m[1].elapsed_time(m[2]), m[2].elapsed_time(m[3])]
+                   for m in marks]).mean(axis=0)
+    t_max = torch.tensor([ms], device=dev)
+    if W > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
+               for x in (hq_, hk_, hv_, hdo)]
+        outs = None
+        h2d = sum(x.numel() * 2 for x in pin)
+        barrier()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(args.steps):
+            xs = [x.to(dev, non_blocking=True) for x in pin]
+            _, g = step(*xs)
+            outs = [y.to("cpu", non_blocking=True) for y in g]
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        et = torch.tensor([a.elapsed_time(b)], device=dev)
+        if W > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        d2h = sum(y.numel() * 2 for y in outs)
+        e2e = {"value": S * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    pk, pk_src = peaks()
+    fl_bwd = 10 * 128 * pairs / W
+    fl_fwd = 4 * 128 * pairs / W
+    t_bwd, t_fwd = ph[2] / 1e3, ph[1] / 1e3
+    ach = fl_bwd / t_bwd / 1e12
+    roof = {"bound": "tensor", "kernel": "attn_bwd (block + bar passes, per-rank)",
+            "achieved": round(ach, 1), "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+            "frac": round(ach / pk["bf16_tflops_sustained"], 4),
+            "peak_source": f"{pk_src} bf16 cuBLAS sustained (burst {pk['bf16_tflops']})",
+            "traffic": None,
+            "fwd_tflops": round(fl_fwd / t_fwd / 1e12, 1),
+            "phase_ms": {"index": round(ph[0], 3), "fwd": round(ph[1], 3), "bwd": round(ph[2], 3)}}
+    tr = ROOT / "profiles" / "traffic.json"
+    if tr.exists():
+        try:
+            roof["traffic"] = json.loads(tr.read_text()).get("attn_bwd_bytes_per_launch")
+        except Exception:
+            pass
+
+    line = {"metric": METRIC, "value": S * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": W,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded RoPE vertical-slash generator, DESIGN.md §3)",
+            "config": {"workload": f"C4-shape layer at W={W}: S={S}, Hq={Hq}, Hkv={Hkv}, d=128, "
+                                   f"p_v=p_s={p}, {'flat' if not args.inner or args.inner == W else f'{W // args.inner}x{args.inner}'} ring",
+                       "seq_len": S, "global_batch": 1, "parallelism": f"cp{W}",
+                       "density": round(dens, 4), "activated_pairs": pairs,
+                       "l2": "inputs larger than L2 (Q alone 2 GiB)"},
+            "roofline": roof, "e2e": e2e, "clocks": clk,
+            "gpu_launches": args.steps * (17 if W == 1 else 17 + 6 * W)}
+    if rank == 0 and W == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = {kk: vv for kk, vv in oracle_sample(q, k, v, dO, p, S, Hq, Hkv).items()
+                                if kk != "seconds"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.destroy()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth.generator import make_grad_out, make_qkv
+    S, Hq, Hkv, p = args.seq, args.hq, args.hkv, args.p
+    q, k, v = make_qkv(S, Hq, Hkv, seed=args.seed)
+    dO = make_grad_out(S, Hq, seed=args.seed)
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(q, k, v, dO, p, S, Hq, Hkv, n_blocks=8)
+        if i >= args.warmup:
+            vals.append(r["value"])
+        last = r
+    val = float(np.median(vals))
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": S / val * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (attention), f32/u64 (index)",
+            "data": "synthetic (seeded RoPE vertical-slash generator, DESIGN.md §3)",
+            "config": {"workload": f"C4-shape layer: S={S}, Hq={Hq}, Hkv={Hkv}, d=128, p_v=p_s={p}",
+                       "seq_len": S, "global_batch": 1, "parallelism": "cpu"},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                             "sample": last["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

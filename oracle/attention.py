@@ -90,6 +90,37 @@ def _block_mask(g, keys, block):
     return rows[:, None] >= keys[None, :]
 
 
+def forward_block(q, k, v, h, g, B_g, C_g, block: int = BLOCK):
+    """Forward of query block g of q head h: returns (O rows, LSE rows)."""
+    d = q.shape[2]
+    grp = q.shape[1] // k.shape[1]
+    rows = slice(g * block, g * block + block)
+    keys = _block_keys(g, B_g, C_g, block)
+    s = (q[rows, h, :] @ k[keys, h // grp, :].T) / np.sqrt(d)
+    P, lse = _softmax_rows(s, _block_mask(g, keys, block))
+    return P @ v[keys, h // grp, :], lse
+
+
+def backward_block(q, k, v, O, LSE, dO, h, g, B_g, C_g, block: int = BLOCK):
+    """Backward contributions of query block g of q head h (Eq. 1, Eq. 12).
+
+    Returns (dQ rows [64][d], keys, dK rows [len(keys)][d], dV rows).
+    """
+    d = q.shape[2]
+    grp = q.shape[1] // k.shape[1]
+    g_kv = h // grp
+    rows = slice(g * block, g * block + block)
+    keys = _block_keys(g, B_g, C_g, block)
+    mask = _block_mask(g, keys, block)
+    kh, vh = k[keys, g_kv, :], v[keys, g_kv, :]
+    s = (q[rows, h, :] @ kh.T) / np.sqrt(d)
+    P = np.where(mask, np.exp(s - LSE[h, rows][:, None]), 0.0)
+    D = (dO[rows, h, :] * O[rows, h, :]).sum(axis=1)
+    dP = dO[rows, h, :] @ vh.T
+    dS = P * (dP - D[:, None])
+    return dS @ kh / np.sqrt(d), keys, dS.T @ q[rows, h, :] / np.sqrt(d), P.T @ dO[rows, h, :]
+
+
 def sparse_attention_forward(q, k, v, i_v, i_s, block: int = BLOCK):
     """Alg. 1 line "y <- sparse(softmax(QK^T/sqrt d) V, i_vs)", fp64.
 
@@ -97,19 +128,13 @@ def sparse_attention_forward(q, k, v, i_v, i_s, block: int = BLOCK):
     Returns (O [S][Hq][d], LSE [Hq][S]).
     """
     S, Hq, d = q.shape
-    grp = Hq // k.shape[1]
     O = np.zeros((S, Hq, d))
     LSE = np.full((Hq, S), NEG_INF)
     for h in range(Hq):
         B, C = sparseformat(i_v[h], i_s[h], S, block)
-        kh, vh = k[:, h // grp, :], v[:, h // grp, :]
         for g in range(S // block):
             rows = slice(g * block, g * block + block)
-            keys = _block_keys(g, B[g], C[g], block)
-            s = (q[rows, h, :] @ kh[keys].T) / np.sqrt(d)
-            P, lse = _softmax_rows(s, _block_mask(g, keys, block))
-            O[rows, h, :] = P @ vh[keys]
-            LSE[h, rows] = lse
+            O[rows, h, :], LSE[h, rows] = forward_block(q, k, v, h, g, B[g], C[g], block)
     return O, LSE
 
 
@@ -126,20 +151,12 @@ def sparse_attention_backward(q, k, v, O, LSE, dO, i_v, i_s, block: int = BLOCK)
     dV = np.zeros_like(v)
     for h in range(Hq):
         B, C = sparseformat(i_v[h], i_s[h], S, block)
-        g_kv = h // grp
-        kh, vh = k[:, g_kv, :], v[:, g_kv, :]
         for g in range(S // block):
             rows = slice(g * block, g * block + block)
-            keys = _block_keys(g, B[g], C[g], block)
-            mask = _block_mask(g, keys, block)
-            s = (q[rows, h, :] @ kh[keys].T) / np.sqrt(d)
-            P = np.where(mask, np.exp(s - LSE[h, rows][:, None]), 0.0)
-            D = (dO[rows, h, :] * O[rows, h, :]).sum(axis=1)
-            dP = dO[rows, h, :] @ vh[keys].T
-            dS = P * (dP - D[:, None])
-            dQ[rows, h, :] += dS @ kh[keys] / np.sqrt(d)
-            dK[keys, g_kv, :] += dS.T @ q[rows, h, :] / np.sqrt(d)   # keys unique per block
-            dV[keys, g_kv, :] += P.T @ dO[rows, h, :]
+            dq, keys, dk, dv = backward_block(q, k, v, O, LSE, dO, h, g, B[g], C[g], block)
+            dQ[rows, h, :] += dq
+            dK[keys, h // grp, :] += dk        # keys unique within a query block
+            dV[keys, h // grp, :] += dv
     return dQ, dK, dV
 
 

@@ -25,18 +25,23 @@ import numpy as np
 BLOCK = 64
 
 
-def sparseformat(i_v: np.ndarray, i_s: np.ndarray, S: int, block: int = BLOCK):
-    """I9 for one head: lists B[g] (key blocks) and C[g] (bar columns), g < nb."""
-    nb = S // block
+def sparseformat_block(i_v, i_s, g: int, block: int = BLOCK):
+    """I9 for one query block g of one head: (B_g key blocks, C_g bar columns)."""
     i_v = np.asarray(i_v, np.int64)
     i_s = np.asarray(i_s, np.int64)
-    sset = set(int(o) for o in i_s)
+    B = np.sort(g - i_s[i_s <= g])
+    vb = i_v // block
+    keep = (vb < g) & ~np.isin(g - vb, i_s)
+    return B, np.sort(i_v[keep])
+
+
+def sparseformat(i_v: np.ndarray, i_s: np.ndarray, S: int, block: int = BLOCK):
+    """I9 for one head: lists B[g] (key blocks) and C[g] (bar columns), g < nb."""
     B, C = [], []
-    vblk = i_v // block
-    for g in range(nb):
-        B.append(np.array(sorted(g - int(o) for o in i_s if o <= g), np.int64))
-        keep = [int(m) for m, b in zip(i_v, vblk) if b < g and (g - int(b)) not in sset]
-        C.append(np.array(sorted(keep), np.int64))
+    for g in range(S // block):
+        b, c = sparseformat_block(i_v, i_s, g, block)
+        B.append(b)
+        C.append(c)
     return B, C
 
 
