@@ -204,6 +204,41 @@ mt_status mt_attn_bwd_step(const mt_shape* shape, int world, int rank, int origi
                            const mt_vs_index* idx, float* dq_acc, float* dk_acc, float* dv_acc,
                            void* ws, size_t ws_bytes, mt_stream_t stream);
 
+/* ------------------------------------------------------------- sparse ring */
+/* Workspace (bytes) of mt_ring_attn_fwd (backward = 0) / mt_ring_attn_bwd
+ * (backward = 1) on `world` ranks. */
+size_t mt_ring_attn_workspace_bytes(const mt_shape* shape, int world, int backward);
+
+/* Balanced sparse ring attention forward (Alg. 2)
+ * on the communicator's ranks: rank r holds the block-striped slices
+ * q_loc [S/W][Hq][128], k_loc/v_loc [S/W][Hkv][128] (global 64-token block b
+ * on rank b mod W at local block b / W).  KV chunks circulate over NCCL
+ * send/recv — flat ring (comm inner == world) or hierarchical inner/outer ring —
+ * overlapped with the per-step sparse forward; o_loc [S/W][Hq][128] bf16 and
+ * lse_loc [Hq][S/W] float32 out.  idx is the GLOBAL index (identical on every
+ * rank, e.g. from mt_build_vs_index with the same comm).  Collective: every
+ * rank must call it.  Errors: as mt_sparse_attn_fwd, MT_ELAYOUT, MT_ENCCL. */
+mt_status mt_ring_attn_fwd(mt_comm* comm, const mt_shape* shape, const void* q_loc,
+                           const void* k_loc, const void* v_loc, const mt_vs_index* idx,
+                           void* o_loc, float* lse_loc, void* ws, size_t ws_bytes,
+                           mt_stream_t stream);
+
+/* Balanced sparse ring attention backward (Table 4): KV circulates as
+ * in the forward; at every step the dK/dV partial of the held chunk is sent to
+ * the chunk's owner over NCCL (reading R17) while the next step computes; dQ
+ * stays local.  Outputs dq_loc [S/W][Hq][128], dk_loc/dv_loc [S/W][Hkv][128]
+ * bf16 for the rank's own striped rows.  Collective. */
+mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* shape, const void* q_loc,
+                           const void* k_loc, const void* v_loc, const void* o_loc,
+                           const float* lse_loc, const void* dO_loc, const mt_vs_index* idx,
+                           void* dq_loc, void* dk_loc, void* dv_loc, void* ws, size_t ws_bytes,
+                           mt_stream_t stream);
+
+/* Host-only: the ring schedule — out[t * world + x] = origin of the KV chunk
+ * rank x holds at step t, for a ring of `world` ranks with `inner` ranks per
+ * node (inner == world: flat).  out must hold world * world ints. */
+mt_status mt_ring_schedule(int world, int inner, int32_t* out);
+
 /* ------------------------------------------------------------------ tests */
 /* Hardware self-test hook (not part of the attention API): one 128-row tcgen05
  * MMA configuration on one CTA, see csrc/selftest.cu for the variants.

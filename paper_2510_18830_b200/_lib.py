@@ -79,11 +79,16 @@ _SIGS: dict[str, list] = {
     "mt_attn_step_workspace_bytes": [P, I],
     "mt_attn_bwd_preprocess": [P, I, P, P, P, P],
     "mt_attn_bwd_step": [P, I, I, I, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
+    "mt_ring_attn_workspace_bytes": [P, I, I],
+    "mt_ring_attn_fwd": [P, P, P, P, P, P, P, P, P, SZ, P],
+    "mt_ring_attn_bwd": [P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
+    "mt_ring_schedule": [I, I, P],
 }
 _RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
             "mt_build_vs_index_workspace_bytes": ctypes.c_size_t,
             "mt_sparse_attn_bwd_workspace_bytes": ctypes.c_size_t,
-            "mt_attn_step_workspace_bytes": ctypes.c_size_t}
+            "mt_attn_step_workspace_bytes": ctypes.c_size_t,
+            "mt_ring_attn_workspace_bytes": ctypes.c_size_t}
 
 
 def declared_symbols() -> list[str]:

@@ -79,9 +79,17 @@ extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, 
     delete c;
     return fail(MT_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
+  if (ncclCommSplit(c->nccl, 0, rank, &c->nccl2, nullptr) != ncclSuccess ||
+      ncclCommSplit(c->nccl, 0, rank, &c->nccl3, nullptr) != ncclSuccess) {
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return fail(MT_ENCCL, "ncclCommSplit failed");
+  }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi);
+  cudaStreamCreateWithPriority(&c->comm_stream2, cudaStreamNonBlocking, hi);
+  cudaStreamCreateWithPriority(&c->comm_stream3, cudaStreamNonBlocking, hi);
   cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
   *out = c;
@@ -95,9 +103,13 @@ extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, 
 extern "C" mt_status mt_comm_destroy(mt_comm* c) {
   if (!c) return MT_OK;
 #ifdef MT_HAVE_NCCL
+  if (c->nccl3) ncclCommDestroy(c->nccl3);
+  if (c->nccl2) ncclCommDestroy(c->nccl2);
   if (c->nccl) ncclCommDestroy(c->nccl);
 #endif
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->comm_stream2) cudaStreamDestroy(c->comm_stream2);
+  if (c->comm_stream3) cudaStreamDestroy(c->comm_stream3);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   delete c;

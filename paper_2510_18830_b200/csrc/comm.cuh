@@ -9,10 +9,14 @@
 
 struct mt_comm {
 #ifdef MT_HAVE_NCCL
-  ncclComm_t nccl = nullptr;
+  ncclComm_t nccl = nullptr;   // inner (node) ring KV exchange, index collectives
+  ncclComm_t nccl2 = nullptr;  // outer ring KV exchange (hierarchical)
+  ncclComm_t nccl3 = nullptr;  // backward dK/dV partials to their owners
 #endif
   int world = 1, rank = 0, inner = 1;
-  cudaStream_t comm_stream = nullptr;  // P2P stream (ring exchanges)
+  cudaStream_t comm_stream = nullptr;   // inner ring P2P
+  cudaStream_t comm_stream2 = nullptr;  // outer ring P2P
+  cudaStream_t comm_stream3 = nullptr;  // dK/dV partial P2P
   cudaEvent_t ev_ready = nullptr;      // compute -> comm ordering
   cudaEvent_t ev_done = nullptr;       // comm -> compute ordering
 };

@@ -184,3 +184,61 @@ def attn_bwd_step(seq_len: int, world: int, rank: int, origin: int, q_loc, k_chu
                                   _ptr(v_chunk), _ptr(dO_loc), _ptr(lse_loc), _ptr(D_loc),
                                   ctypes.byref(ci), _ptr(dq_acc), _ptr(dk_acc), _ptr(dv_acc),
                                   _ptr(ws), ws.numel(), _stream()))
+
+
+class Comm:
+    """mt_comm over a torch.distributed process group (one process per GPU)."""
+
+    def __init__(self, handle, world: int, rank: int, inner: int):
+        self.handle, self.world, self.rank, self.inner = handle, world, rank, inner
+
+    @staticmethod
+    def create(world: int, rank: int, inner: int | None = None, group=None) -> "Comm":
+        import torch.distributed as dist
+        L = _lib.lib()
+        buf = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _lib.check(L.mt_comm_unique_id(buf))
+        ids = [bytes(buf)] if rank == 0 else [None]
+        dist.broadcast_object_list(ids, src=0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(ids[0])
+        h = ctypes.c_void_p()
+        inner = world if not inner else inner
+        _lib.check(L.mt_comm_create(uid, world, rank, inner, ctypes.byref(h)))
+        return Comm(h, world, rank, inner)
+
+    def destroy(self):
+        if self.handle:
+            _lib.check(_lib.lib().mt_comm_destroy(self.handle))
+            self.handle = None
+
+
+def ring_schedule(world: int, inner: int | None = None):
+    """Host-side schedule from the library: held[t][x] = origin at rank x, step t."""
+    out = (ctypes.c_int32 * (world * world))()
+    _lib.check(_lib.lib().mt_ring_schedule(world, inner or world, out))
+    return [[out[t * world + x] for x in range(world)] for t in range(world)]
+
+
+def ring_attn_fwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, idx: VSIndex):
+    sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 0))
+    o = torch.empty_like(q_loc)
+    lse = torch.empty(q_loc.shape[1], q_loc.shape[0], dtype=torch.float32, device=q_loc.device)
+    ci = idx.c_struct()
+    _lib.check(L.mt_ring_attn_fwd(comm.handle, ctypes.byref(sh), _ptr(q_loc), _ptr(k_loc), _ptr(v_loc),
+                                  ctypes.byref(ci), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream()))
+    return o, lse
+
+
+def ring_attn_bwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, o_loc, lse_loc, dO_loc, idx: VSIndex):
+    sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 1))
+    dq, dk, dv = torch.empty_like(q_loc), torch.empty_like(k_loc), torch.empty_like(v_loc)
+    ci = idx.c_struct()
+    _lib.check(L.mt_ring_attn_bwd(comm.handle, ctypes.byref(sh), _ptr(q_loc), _ptr(k_loc), _ptr(v_loc),
+                                  _ptr(o_loc), _ptr(lse_loc), _ptr(dO_loc), ctypes.byref(ci),
+                                  _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream()))
+    return dq, dk, dv

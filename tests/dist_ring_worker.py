@@ -1,0 +1,94 @@
+"""torchrun worker: distributed index + flat/hierarchical ring fwd/bwd vs the oracle.
+
+Launched by tests/test_gpu_ring.py (and usable by hand):
+  torchrun --nproc-per-node N tests/dist_ring_worker.py --inner G --seq S
+Exit code 0 = every check passed (rank 0 prints a JSON summary).
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2510_18830_b200 import ops  # noqa: E402
+from synth.generator import bf16_bits_to_f32, make_grad_out, make_qkv  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--inner", type=int, default=0)
+    ap.add_argument("--seq", type=int, default=4096)
+    ap.add_argument("--p", type=float, default=0.9)
+    a = ap.parse_args()
+    W, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = ops.Comm.create(W, rank, a.inner or W)
+    S, Hq, Hkv = a.seq, 4, 2
+    q, k, v = make_qkv(S, Hq, Hkv, seed=31, a=12.0)
+    dO = make_grad_out(S, Hq, seed=31)
+    j = np.arange(S // W)
+    rows = ((j // 64) * W + rank) * 64 + j % 64
+    t = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).to(dev)
+    ql, kl, vl, dl = (t(x[rows]) for x in (q, k, v, dO))
+    ok = {}
+    # distributed index == single-GPU index (bit-exact, W-invariant)
+    idx = ops.build_vs_index(ql, kl, a.p, a.p, comm=comm, seq_len=S)
+    idx1 = ops.build_vs_index(t(q), t(k), a.p, a.p)
+    iv, is_ = idx.to_lists()
+    iv1, is1 = idx1.to_lists()
+    ok["index_w_invariant"] = all(np.array_equal(x, y) for x, y in zip(iv + is_, iv1 + is1))
+    # ring forward / backward
+    o, lse = ops.ring_attn_fwd(comm, S, ql, kl, vl, idx)
+    dq, dk, dv = ops.ring_attn_bwd(comm, S, ql, kl, vl, o, lse, dl, idx)
+    torch.cuda.synchronize()
+
+    def gather(x, axis=0):
+        parts = [torch.empty_like(x) for _ in range(W)]
+        dist.all_gather(parts, x.contiguous())
+        return [p_.float().cpu().numpy() for p_ in parts]
+
+    go, gl = gather(o), gather(lse)
+    gq, gk, gv = gather(dq), gather(dk), gather(dv)
+    if rank == 0:
+        from oracle import attention as OA
+        f64 = lambda x: bf16_bits_to_f32(x).astype(np.float64)
+        O, L = OA.sparse_attention_forward(f64(q), f64(k), f64(v), iv, is_)
+        ref = OA.sparse_attention_backward(f64(q), f64(k), f64(v), O, L, f64(dO), iv, is_)
+        def unstripe(parts, shape, lse_=False):
+            out = np.zeros(shape)
+            for r in range(W):
+                rr = ((j // 64) * W + r) * 64 + j % 64
+                if lse_:
+                    out[:, rr] = parts[r]
+                else:
+                    out[rr] = parts[r]
+            return out
+        def nerr(g, r_):
+            return max(np.abs(g[:, h] - r_[:, h]).max() / np.abs(r_[:, h]).max() for h in range(r_.shape[1]))
+        errs = {"o": nerr(unstripe(go, O.shape), O),
+                "lse": float(np.abs(unstripe(gl, L.shape, True) - L).max()),
+                "dq": nerr(unstripe(gq, ref[0].shape), ref[0]),
+                "dk": nerr(unstripe(gk, ref[1].shape), ref[1]),
+                "dv": nerr(unstripe(gv, ref[2].shape), ref[2])}
+        ok["fwd"] = errs["o"] <= 2e-2 and errs["lse"] <= 1e-3
+        ok["bwd"] = max(errs["dq"], errs["dk"], errs["dv"]) <= 2e-2
+        print(json.dumps({"world": W, "inner": a.inner or W, "ok": ok,
+                          "errs": {k_: float(v_) for k_, v_ in errs.items()}}), flush=True)
+    flag = torch.tensor([1 if all(ok.values()) else 0], device=dev)
+    dist.broadcast(flag, 0)
+    comm.destroy()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()
