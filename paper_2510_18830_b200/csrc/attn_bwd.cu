@@ -277,11 +277,21 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
 
 // ------------------------------------------------------------------ MMA issuer
 __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
+  const bool leader = elect_one();
   const uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // S^T, dP^T
   const uint32_t id_kv = make_idesc_bf16(128, 128, false, true);  // dV, dK
   const uint32_t id_q = make_idesc_bf16(128, 64, true, true);     // dQ^T
-  const uint32_t k0 = smem_u32(sm.k), v0 = smem_u32(sm.v);
-  const uint32_t pT = smem_u32(sm.pT), dsT = smem_u32(sm.dsT);
+  // descriptor bases; each MMA only adds an immediate to the address field
+  const uint64_t dK = make_sdesc(smem_u32(sm.k), 16, 1024);         // K-major K (S^T)
+  const uint64_t dV = make_sdesc(smem_u32(sm.v), 16, 1024);         // K-major V (dP^T)
+  const uint64_t dKmn = make_sdesc(smem_u32(sm.k), 16384, 1024);    // MN-major K^T (dQ^T)
+  const uint64_t dQ0 = make_sdesc(smem_u32(sm.q[0]), 16, 1024);
+  const uint64_t dO0 = make_sdesc(smem_u32(sm.dO[0]), 16, 1024);
+  const uint64_t dQmn0 = make_sdesc(smem_u32(sm.q[0]), 8192, 1024);
+  const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
+  const uint64_t dPT = make_sdesc(smem_u32(sm.pT), 16, 1024);
+  const uint64_t dDST = make_sdesc(smem_u32(sm.dsT), 16, 1024);
+  const uint64_t dDSTmn = make_sdesc(smem_u32(sm.dsT), 8192, 1024);
   int stage = 0;
   uint32_t fphase = 0, kvf_phase = 0, sfree_phase = 0, dsf_phase = 0;
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
@@ -299,48 +309,45 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       tc_fence_after();
       mbar_wait(smem_u32(&sm.sfree), sfree_phase ^ 1);
       sfree_phase ^= 1;
-      sm.smeta = sm.meta[stage];
-      sm.smeta.stage = stage;
-      mbar_arrive(smem_u32(&sm.sfull));  // 1st arrival publishes smeta
+      if (leader) sm.smeta = sm.meta[stage];
+      if (leader) sm.smeta.stage = stage;
+      if (leader) mbar_arrive(smem_u32(&sm.sfull));  // 1st arrival publishes smeta
       if (kind == kChunk) {
-        const uint32_t qs = smem_u32(sm.q[stage]), dos = smem_u32(sm.dO[stage]);
+        const uint64_t dq = sdesc_add(dQ0, stage * kTileQ), ddo = sdesc_add(dO0, stage * kTileQ);
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16) {
           const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
           const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
-          mma_ss(tmem + kColS, make_sdesc(k0 + ko, 16, 1024), make_sdesc(qs + qo, 16, 1024),
-                 id_s, kk > 0);
-          mma_ss(tmem + kColDP, make_sdesc(v0 + ko, 16, 1024), make_sdesc(dos + qo, 16, 1024),
-                 id_s, kk > 0);
+          if (leader) mma_ss(tmem + kColS, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
+          if (leader) mma_ss(tmem + kColDP, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
         }
-        mma_commit(smem_u32(&sm.sfull));  // 2nd arrival: S^T, dP^T ready
+        if (leader) mma_commit(smem_u32(&sm.sfull));  // 2nd arrival: S^T, dP^T ready
       } else {
-        mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
+        if (leader) mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
       }
       if (have_prev) {
         mbar_wait(smem_u32(&sm.dsfull), dsf_phase);
         dsf_phase ^= 1;
         tc_fence_after();
-        const uint32_t qs = smem_u32(sm.q[prev_stage]), dos = smem_u32(sm.dO[prev_stage]);
+        const uint64_t dqm = sdesc_add(dQmn0, prev_stage * kTileQ);
+        const uint64_t dom = sdesc_add(dOmn0, prev_stage * kTileQ);
 #pragma unroll
         for (int kq = 0; kq < 64; kq += 16) {
           const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
-          mma_ss(tmem + kColDV, make_sdesc(pT + kq * 2, 16, 1024),
-                 make_sdesc(dos + kq * 128, 8192, 1024), id_kv, acc);
-          mma_ss(tmem + kColDK, make_sdesc(dsT + kq * 2, 16, 1024),
-                 make_sdesc(qs + kq * 128, 8192, 1024), id_kv, acc);
+          if (leader) mma_ss(tmem + kColDV, sdesc_add(dPT, kq * 2), sdesc_add(dom, kq * 128), id_kv, acc);
+          if (leader) mma_ss(tmem + kColDK, sdesc_add(dDST, kq * 2), sdesc_add(dqm, kq * 128), id_kv, acc);
         }
         acc_started = true;
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16)
-          mma_ss(tmem + kColDQ, make_sdesc(k0 + kk * 128, 16384, 1024),
-                 make_sdesc(dsT + kk * 128, 8192, 1024), id_q, kk > 0);
-        mma_commit(smem_u32(&sm.dqfull));
-        mma_commit(smem_u32(&sm.empty[prev_stage]));
+          if (leader) mma_ss(tmem + kColDQ, sdesc_add(dKmn, kk * 128), sdesc_add(dDSTmn, kk * 128), id_q,
+                 kk > 0);
+        if (leader) mma_commit(smem_u32(&sm.dqfull));
+        if (leader) mma_commit(smem_u32(&sm.empty[prev_stage]));
       }
       if (kind == kEnd) {
-        mbar_arrive(smem_u32(&sm.empty[stage]));
-        mbar_arrive(smem_u32(&sm.sfull));
+        if (leader) mbar_arrive(smem_u32(&sm.empty[stage]));
+        if (leader) mbar_arrive(smem_u32(&sm.sfull));
       }
       have_prev = (kind == kChunk);
       prev_stage = stage;
@@ -518,9 +525,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tmdo,
                     const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                      ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // dynamic shared memory starts 1024-aligned (no static __shared__ in this kernel);
+  // using it directly keeps LDS/STS (not generic) addressing for every Smem field
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = warp_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -551,8 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     producer(sm, P, &tmq, &tmdo, &tmk, &tmv);
   } else if (warp == 1) {
-    if (lane_id() == 0) mma_issuer(sm, P, tmem);
-    __syncwarp();
+    mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
   } else {
     softmax_bwd(sm, P, tmem);
   }

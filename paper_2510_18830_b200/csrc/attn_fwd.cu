@@ -1,23 +1,28 @@
-// attn_fwd.cu — block-sparse vertical-slash attention forward for sm_100a,
-// one ring step (Alg. 2 "block_bar_sparse_attention_forward" P:878
-// followed by "merge_out_and_lse" P:879; on one GPU W = 1 and the single step
-// is Alg. 1's "sparse(softmax(QK^T/sqrt d)V, i_vs)").
+// attn_fwd.cu — block-sparse vertical-slash attention forward for sm_100a, one
+// ring step (Alg. 2 "block_bar_sparse_attention_forward" P:878 then
+// "merge_out_and_lse" P:879; with W = 1 the single step is Alg. 1's
+// "sparse(softmax(QK^T/sqrt d)V, i_vs)").
 //
-// Work unit (tile): 128 query rows = two 64-row slots = local query blocks
-// (j0, j0+1) of ONE q head h (global blocks g0 = j0 W + r, g1 = g0 + W).  For the
-// held KV chunk of origin s the tile visits, in one merged stream:
-//   BLOCK chunks: local key block lb of every slash offset o = t (mod W) that
-//                 either slot needs (kb = g - o), TMA-staged, 64 contiguous keys;
-//   BAR chunks  : up to 64 gathered vertical columns of origin s that either
-//                 slot needs and no selected slash covers (I9), cp.async-staged.
-// Per chunk: S = Q K^T (tcgen05, M=128 N=64 K=128, fp32 in TMEM), online
-// softmax in registers (one thread per row; per-slot masks, causal diagonal),
-// P (bf16) -> smem, O += P V (tcgen05, M=128 N=128 K=64, O in TMEM).
+// Transposed ("key-major") tiles so the 64-granular pattern costs no MMA waste:
+//   tile  = one 64-query block g of one q head h (N = 64 of every MMA);
+//   chunk = 128 keys that ALL belong to this block's key set: two 64-key slash
+//           blocks of B_g (TMA), or up to 128 gathered vertical columns of C_g
+//           (cp.async), restricted to the held KV origin (I9/I10);
+//   S^T = K Q^T          tcgen05 M=128 (keys) N=64 K=128 (d)      -> TMEM
+//   P^T = 2^(S^T c - m_q) in registers (thread = key row, 32 query columns)
+//   O^T += V^T P^T       tcgen05 M=128 (d)    N=64 K=128 (keys)   -> TMEM
+// The column stabiliser m_q is the exact max of the tile's first chunk (every
+// query sees >= 1 key there); later chunks move it (with an O^T / l rescale)
+// only if a score exceeds it by 2^64 — a rare slow path.  Row sums l_q are
+// per-thread partials reduced once per tile.
 //
-// Warp roles (192 threads, 1 CTA/SM, persistent over tiles):
-//   warp 0      producer: builds the chunk stream from the VSPlan, TMA/cp.async
-//   warp 1      MMA issuer (one elected lane)
-//   warps 2..5  softmax + epilogue (row = 32 * (warp % 4) + lane = TMEM lane)
+// Warp roles (384 threads, 1 CTA / SM, persistent; setmaxnreg moves registers
+// from warpgroup 0 to the softmax warpgroups):
+//   warp 0       producer (chunk stream from the VSPlan, TMA / cp.async)
+//   warp 1       MMA issuer (one lane)
+//   warps 2, 3   idle
+//   warps 4..11  two softmax warpgroups; warpgroup g takes the tile's chunks
+//                k = g (mod 2); warp w covers TMEM lanes 32*(w%4)..
 #include "common.cuh"
 #include "plan.cuh"
 #include "sm100.cuh"
@@ -27,86 +32,139 @@ namespace mt {
 
 namespace fwd {
 
-constexpr int kStages = 4;
-constexpr int kThreads = 192;
-constexpr uint32_t kTileQ = 128 * 128 * 2;   // 32 KB
-constexpr uint32_t kTileKV = 64 * 128 * 2;   // 16 KB
+constexpr int kKSt = 3, kVSt = 2;
+constexpr int kThreads = 384;  // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
+constexpr int kSoftmax = 256;
+constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB
+constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB
+constexpr float kOverflow = 64.f;            // log2 headroom before the stabiliser moves
 
-enum : int { kBlock = 0, kBar = 1, kEnd = 2 };
+enum : int { kBlk = 0, kBar = 1, kEnd = 2 };
 
-struct ChunkMeta {
+struct alignas(16) ChunkMeta {
   int kind;
-  int lb;            // local key block (kBlock)
-  uint32_t flags;    // bit0/1: slot0/1 uses it; bit2/3: slot0/1 diagonal (kBlock)
+  int n;           // kBar: live rows
+  uint32_t flags;  // kBlk: bit0 rows 64..127 live, bit1 rows 0..63 diagonal, bit2 rows 64..127 diagonal
+  int lb0, lb1;
+  int rows[128];   // kBar local rows (producer only)
+};
+
+struct SMeta {
+  int kind, n;
+  uint32_t flags;
   int pad;
-  uint64_t mask[2];  // per-slot column masks (kBar)
-  int rows[64];      // local key rows (kBar)
 };
 
 struct Smem {
+  uint8_t k[kKSt][kTileKV];
+  uint8_t v[kVSt][kTileKV];
   uint8_t q[kTileQ];
-  uint8_t k[kStages][kTileKV];
-  uint8_t v[kStages][kTileKV];
-  uint8_t p[kTileP];
-  ChunkMeta meta[kStages];
-  ChunkMeta smeta[2];        // copy handed to the softmax per S buffer
-  int stage_rows[128];       // producer staging for bar columns
-  uint32_t stage_bits[128];
-  uint64_t full[kStages], empty[kStages];
-  uint64_t sfull[2], sfree[2];
-  uint64_t qfull, qempty, pfull, pvdone;
+  uint8_t p[2][kTileP];
+  ChunkMeta meta[kKSt];
+  SMeta smeta[2];
+  alignas(16) float red[2][4][32];  // column-max partials (two 32-column halves)
+  alignas(16) float lsum[2][4][64]; // per WG, per lane quadrant: row-sum partials
+  alignas(16) float m[64];          // column stabiliser (log2 domain), read as float4
+  alignas(16) float wa[64];         // rescale factors / epilogue merge weights
+  alignas(16) float wb[64];
+  int stage_rows[192];
+  int ovf;
+  uint64_t kfull[kKSt], kempty[kKSt], vfull[kVSt], vempty[kVSt];
+  uint64_t sfull[2], sfree[2], pfull[2], obar[2];
+  uint64_t qfull, qempty, mready;
   uint32_t tmem_base;
 };
 
 struct Params {
   VSPlan plan;
-  int r, s, t;               // rank, origin of the held chunk, ring step (= (r - s) mod W)
-  int nloc;                  // local query blocks = S_loc / 64
+  int r, s, t;
+  int nloc;
   int n_tiles;
-  int first, last;           // merge mode
-  float scale_log2;          // log2(e) / sqrt(d)
-  const __nv_bfloat16* k;    // held chunk [S_loc][Hkv][128]
+  int first, last;
+  float scale_log2;
+  const __nv_bfloat16* k;
   const __nv_bfloat16* v;
-  __nv_bfloat16* o;          // [S_loc][Hq][128]  (written when last)
-  float* o_acc;              // [S_loc][Hq][128]  (ring accumulator when !last or !first)
-  float* lse;                // [Hq][S_loc]       (running / final LSE, natural log)
+  __nv_bfloat16* o;
+  float* o_acc;
+  float* lse;
+  int* fix_count;  // tiles flagged for the exact fix-up pass (stabiliser overflow)
+  int* fix_list;
 };
 
-__device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h, int& j0) {
-  const int npairs = (P.nloc + 1) / 2;
-  const int pr = npairs - 1 - tile / P.plan.Hq;   // heavy (late) query blocks first
-  h = tile % P.plan.Hq;
-  j0 = 2 * pr;
+constexpr uint32_t kColO = 0, kColS = 64;  // TMEM: O^T [0,64), S^T buffers [64,128) [128,192)
+
+__device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h, int& j) {
+  const int Hq = P.plan.Hq;
+  j = P.nloc - 1 - tile / Hq;  // late query blocks (most keys) first
+  h = tile % Hq;
 }
 
 // ------------------------------------------------------------------ producer
+// K of chunk c is issued as soon as its K slot frees (after S^T(c-3)); V lags by
+// one chunk (issued after K(c+1)) because its slot frees later (after the O^T two
+// data chunks back).  K slots (and the chunk meta) are indexed by every chunk
+// including END markers; V slots only by data chunks, so an END never advances
+// a V barrier ahead of the producer (parity aliasing).
 __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
                          const CUtensorMap* tmk, const CUtensorMap* tmv) {
   const int lane = lane_id();
   const VSPlan& pl = P.plan;
   const int W = pl.W;
   const int grp = pl.Hq / pl.Hkv;
-  int stage = 0;
-  uint32_t ephase = 0;  // phase parity of empty[] waits
+  uint32_t c = 0;  // chunk counter (incl. END markers)
   uint32_t qe_phase = 0;
   bool first_tile = true;
+  // pending V load (the previous chunk)
+  bool vpend = false;
+  uint32_t vp_c = 0, dv = 0;  // pending chunk, data-chunk counter (V slots)
+  int vp_gkv = 0;
 
-  auto next_stage = [&]() {
-    if (++stage == kStages) { stage = 0; ephase ^= 1; }
+  auto kacquire = [&]() {
+    mbar_wait(smem_u32(&sm.kempty[c % kKSt]), ((c / kKSt) & 1) ^ 1);
   };
-  auto acquire = [&]() { mbar_wait(smem_u32(&sm.empty[stage]), ephase ^ 1); };
+  auto flush_v = [&]() {
+    if (!vpend) return;
+    vpend = false;
+    const uint32_t vs = dv % kVSt, ks = vp_c % kKSt;
+    mbar_wait(smem_u32(&sm.vempty[vs]), ((dv / kVSt) & 1) ^ 1);
+    ++dv;
+    const ChunkMeta& m = sm.meta[ks];
+    const uint32_t vb = smem_u32(&sm.vfull[vs]);
+    if (m.kind == kBlk) {
+      if (lane == 0) {
+        mbar_expect_tx(vb, kTileKV);
+        for (int cc = 0; cc < 2; ++cc)
+          for (int x = 0; x < 2; ++x)
+            tma_load_3d(smem_u32(sm.v[vs] + cc * 16384 + x * 8192), tmv, vb, cc * 64, vp_gkv,
+                        (x ? m.lb1 : m.lb0) * 64);
+      }
+    } else if (m.kind == kBar) {
+      const uint32_t vbase = smem_u32(sm.v[vs]);
+      for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
+        const int row = pidx >> 4, c16 = pidx & 15;
+        const size_t goff = ((size_t)m.rows[row] * pl.Hkv + vp_gkv) * 128 + c16 * 8;
+        cp_async_16(vbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.v + goff);
+      }
+      asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(vb) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(vb);
+    }
+    __syncwarp();
+  };
+  auto push = [&](int gkv, bool data) {  // chunk c's K is issued; its V becomes pending
+    flush_v();
+    vpend = data;
+    vp_c = c;
+    vp_gkv = gkv;
+    ++c;
+  };
 
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-    int h, j0;
-    tile_coords(P, tile, h, j0);
-    const int j1 = j0 + 1;
-    const bool v1 = j1 < P.nloc;
-    const int g0 = j0 * W + P.r;
-    const int g1 = v1 ? j1 * W + P.r : -1;
+    int h, j;
+    tile_coords(P, tile, h, j);
+    const int g = j * W + P.r;
     const int gkv = h / grp;
-
-    // ---- Q tile (two 64-row slots x two 64-column chunks)
     if (!first_tile) {
       mbar_wait(smem_u32(&sm.qempty), qe_phase);
       qe_phase ^= 1;
@@ -114,411 +172,429 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     first_tile = false;
     if (lane == 0) {
       const uint32_t bar = smem_u32(&sm.qfull);
-      mbar_expect_tx(bar, v1 ? kTileQ : kTileQ / 2);
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d(smem_u32(sm.q + c * 16384), tmq, bar, c * 64, h, j0 * 64);
-        if (v1) tma_load_3d(smem_u32(sm.q + c * 16384 + 8192), tmq, bar, c * 64, h, j1 * 64);
-      }
+      mbar_expect_tx(bar, kTileQ);
+      for (int cc = 0; cc < 2; ++cc)
+        tma_load_3d(smem_u32(sm.q + cc * 8192), tmq, bar, cc * 64, h, j * 64);
     }
-
-    // ---- slash blocks: offsets o = t (mod W); kb = g - o, merged over both slots
+    // ---- slash blocks of residue t, two per chunk
     {
       const int ns = pl.s_cnt[h];
       const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
-      // walk candidates in ascending kb: slot1 kb = g1 - o, slot0 kb = g0 - o.
-      // Both sequences are produced by walking offsets descending.
-      int ia = ns - 1, ib = ns - 1;  // ia: slot0 pointer, ib: slot1 pointer
-      auto next_valid = [&](int i, int g) {
-        while (i >= 0) {
-          const int o = offs[i];
-          if (o <= g && (o % W) == P.t) break;
-          --i;
+      auto next = [&](int from) {
+        while (from < ns) {
+          const int o = offs[from];
+          if (o > g) return ns;
+          if ((o % W) == P.t) return from;
+          ++from;
         }
-        return i;
+        return ns;
       };
-      ia = next_valid(ia, g0);
-      ib = v1 ? next_valid(ib, g1) : -1;
-      while (ia >= 0 || ib >= 0) {
-        const int kba = ia >= 0 ? g0 - offs[ia] : INT32_MAX;
-        const int kbb = ib >= 0 ? g1 - offs[ib] : INT32_MAX;
-        const int kb = min(kba, kbb);
+      int i = next(0);
+      while (i < ns) {
+        const int o0 = offs[i];
+        const int i1 = next(i + 1);
+        const int o1 = i1 < ns ? offs[i1] : -1;
+        i = i1 < ns ? next(i1 + 1) : ns;
+        const int lb0 = (g - o0 - P.s) / W;
+        const int lb1 = o1 >= 0 ? (g - o1 - P.s) / W : lb0;
         uint32_t flags = 0;
-        if (kba == kb) { flags |= 1u; if (kb == g0) flags |= 4u; ia = next_valid(ia - 1, g0); }
-        if (kbb == kb) { flags |= 2u; if (kb == g1) flags |= 8u; ib = next_valid(ib - 1, g1); }
-        const int lb = (kb - P.s) / W;
-        acquire();
+        if (o1 >= 0) flags |= 1u;
+        if (o0 == 0) flags |= 2u;
+        if (o1 == 0) flags |= 4u;
+        kacquire();
         if (lane == 0) {
-          ChunkMeta& m = sm.meta[stage];
-          m.kind = kBlock;
-          m.lb = lb;
+          const uint32_t ks = c % kKSt;
+          ChunkMeta& m = sm.meta[ks];
+          m.kind = kBlk;
           m.flags = flags;
-          const uint32_t bar = smem_u32(&sm.full[stage]);
-          mbar_expect_tx(bar, 2 * kTileKV);
-          for (int c = 0; c < 2; ++c) {
-            tma_load_3d(smem_u32(sm.k[stage] + c * 8192), tmk, bar, c * 64, gkv, lb * 64);
-            tma_load_3d(smem_u32(sm.v[stage] + c * 8192), tmv, bar, c * 64, gkv, lb * 64);
-          }
+          m.lb0 = lb0;
+          m.lb1 = lb1;
+          const uint32_t kb = smem_u32(&sm.kfull[ks]);
+          mbar_expect_tx(kb, kTileKV);
+          for (int cc = 0; cc < 2; ++cc)
+            for (int x = 0; x < 2; ++x)
+              tma_load_3d(smem_u32(sm.k[ks] + cc * 16384 + x * 8192), tmk, kb, cc * 64, gkv,
+                          (x ? lb1 : lb0) * 64);
         }
         __syncwarp();
-        next_stage();
+        push(gkv, true);
       }
     }
-
-    // ---- bars: vertical columns of origin s, block < g, offset not a selected slash
+    // ---- bars of origin s: block < g, offset not a selected slash; 128 per chunk
     {
       const int32_t* vc = pl.vcol + (int64_t)h * pl.S;
       const int vb = pl.vptr[h * (W + 1) + P.s];
       const int ve = pl.vptr[h * (W + 1) + P.s + 1];
-      const int glim = v1 ? g1 : g0;
-      int nstaged = 0;  // columns staged in sm.stage_rows (warp-uniform)
+      int nst = 0;
       auto emit = [&](int n) {
-        // emit the first n (<= 64) staged columns as one BAR chunk
-        acquire();
-        ChunkMeta& m = sm.meta[stage];
-        uint32_t b0 = 0, c0 = 0;
-        // lane l covers columns l and l + 32
-        const int ca = lane, cb = lane + 32;
-        int ra = sm.stage_rows[ca < n ? ca : 0];
-        int rb = sm.stage_rows[cb < n ? cb : 0];
-        if (ca < n) { b0 = sm.stage_bits[ca]; }
-        if (cb < n) { c0 = sm.stage_bits[cb]; }
-        m.rows[ca] = ra;
-        m.rows[cb] = rb;
-        const uint32_t lo0 = __ballot_sync(0xffffffffu, b0 & 1u);
-        const uint32_t lo1 = __ballot_sync(0xffffffffu, (b0 >> 1) & 1u);
-        const uint32_t hi0 = __ballot_sync(0xffffffffu, c0 & 1u);
-        const uint32_t hi1 = __ballot_sync(0xffffffffu, (c0 >> 1) & 1u);
+        kacquire();
+        const uint32_t ks = c % kKSt;
+        ChunkMeta& m = sm.meta[ks];
+        for (int x = lane; x < 128; x += 32) m.rows[x] = sm.stage_rows[x < n ? x : 0];
         if (lane == 0) {
           m.kind = kBar;
-          m.mask[0] = (uint64_t)lo0 | ((uint64_t)hi0 << 32);
-          m.mask[1] = (uint64_t)lo1 | ((uint64_t)hi1 << 32);
+          m.n = n;
         }
         __syncwarp();
-        // gather K/V rows: 64 rows x 16 pieces of 16 B each, for K and V
-        const uint32_t kbase = smem_u32(sm.k[stage]), vbase = smem_u32(sm.v[stage]);
-        for (int pidx = lane; pidx < 64 * 16; pidx += 32) {
+        const uint32_t kbase = smem_u32(sm.k[ks]);
+        for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
           const int row = pidx >> 4, c16 = pidx & 15;
-          const int src = m.rows[row];
-          const size_t goff = ((size_t)src * pl.Hkv + gkv) * 128 + c16 * 8;
-          const uint32_t doff = (c16 >> 3) * 8192 + sw128(row, c16 & 7);
-          cp_async_16(kbase + doff, P.k + goff);
-          cp_async_16(vbase + doff, P.v + goff);
+          const size_t goff = ((size_t)m.rows[row] * pl.Hkv + gkv) * 128 + c16 * 8;
+          cp_async_16(kbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.k + goff);
         }
-        const uint32_t bar = smem_u32(&sm.full[stage]);
-        asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+        const uint32_t kb = smem_u32(&sm.kfull[ks]);
+        asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(kb) : "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar);
-        next_stage();
-        // shift the remaining staged columns down
-        const int rem = nstaged - n;
+        if (lane == 0) mbar_arrive(kb);
+        push(gkv, true);
+        const int rem = nst - n;  // shift the remaining staged columns down
+        int t0 = 0;
+        if (lane < rem) t0 = sm.stage_rows[n + lane];
         __syncwarp();
-        int tr0 = 0, tr1 = 0;
-        uint32_t tb0 = 0, tb1 = 0;
-        if (lane < rem) { tr0 = sm.stage_rows[n + lane]; tb0 = sm.stage_bits[n + lane]; }
-        if (lane + 32 < rem) { tr1 = sm.stage_rows[n + lane + 32]; tb1 = sm.stage_bits[n + lane + 32]; }
+        if (lane < rem) sm.stage_rows[lane] = t0;
         __syncwarp();
-        if (lane < rem) { sm.stage_rows[lane] = tr0; sm.stage_bits[lane] = tb0; }
-        if (lane + 32 < rem) { sm.stage_rows[lane + 32] = tr1; sm.stage_bits[lane + 32] = tb1; }
-        __syncwarp();
-        nstaged = rem;
+        nst = rem;
       };
       for (int base = vb; base < ve; base += 32) {
         const int i = base + lane;
-        int m = 0;
-        bool in0 = false, in1 = false;
-        bool more = false;
+        bool keep = false, more = false;
+        int lrow = 0;
         if (i < ve) {
-          m = vc[i];
+          const int m = vc[i];
           const int blk = m >> 6;
-          if (blk < glim) {
+          if (blk < g) {
             more = true;
-            in0 = blk < g0 && !plan_has_slash(pl, h, g0 - blk);
-            in1 = v1 && blk < g1 && !plan_has_slash(pl, h, g1 - blk);
+            keep = !plan_has_slash(pl, h, g - blk);
+            lrow = ((blk - P.s) / W) * 64 + (m & 63);
           }
         }
-        const bool keep = in0 || in1;
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        const int pos = __popc(bal & ((1u << lane) - 1u));
-        if (keep) {
-          const int blk = m >> 6;
-          sm.stage_rows[nstaged + pos] = ((blk - P.s) / W) * 64 + (m & 63);
-          sm.stage_bits[nstaged + pos] = (in0 ? 1u : 0u) | (in1 ? 2u : 0u);
-        }
+        if (keep) sm.stage_rows[nst + __popc(bal & ((1u << lane) - 1u))] = lrow;
         __syncwarp();
-        nstaged += __popc(bal);
-        if (nstaged >= 64) emit(64);
-        if (!__any_sync(0xffffffffu, more)) break;  // sorted: later columns are beyond glim
+        nst += __popc(bal);
+        if (nst >= 128) emit(128);
+        if (!__any_sync(0xffffffffu, more)) break;
       }
-      if (nstaged > 0) emit(nstaged);
+      if (nst > 0) emit(nst);
     }
-
-    // ---- END marker
-    acquire();
+    // ---- END
+    kacquire();
     if (lane == 0) {
-      sm.meta[stage].kind = kEnd;
-      mbar_arrive(smem_u32(&sm.full[stage]));
+      const uint32_t ks = c % kKSt;
+      sm.meta[ks].kind = kEnd;
+      mbar_arrive(smem_u32(&sm.kfull[ks]));
     }
     __syncwarp();
-    next_stage();
+    push(gkv, false);  // flushes the tile's last V
   }
+  flush_v();
 }
 
 // ------------------------------------------------------------------ MMA issuer
+// Chunk k of a tile goes to S^T / P^T buffer k & 1, i.e. to softmax warpgroup
+// k & 1: the two warpgroups alternate chunks so one computes while the tensor
+// core works for the other.  END is published to both warpgroups.
 __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
-  const uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
-  const uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);
-  const uint32_t tm_o = tmem;           // O: columns [0, 128)
-  int stage = 0;
-  uint32_t fphase = 0;
-  int b = 0;
-  uint32_t sfree_phase[2] = {0, 0};
-  uint32_t pfull_phase = 0, qfull_phase = 0;
-  const uint32_t q0 = smem_u32(sm.q), p0 = smem_u32(sm.p);
-
+  const bool leader = elect_one();
+  const uint32_t id_s = make_idesc_bf16(128, 64, false, false);
+  const uint32_t id_o = make_idesc_bf16(128, 64, true, true);
+  // descriptor bases; each MMA only adds an immediate to the address field
+  const uint64_t dq0 = make_sdesc(smem_u32(sm.q), 16, 1024);
+  const uint64_t dk0 = make_sdesc(smem_u32(sm.k[0]), 16, 1024);
+  const uint64_t dv0 = make_sdesc(smem_u32(sm.v[0]), 16384, 1024);
+  const uint64_t dp0 = make_sdesc(smem_u32(sm.p[0]), 8192, 1024);
+  uint32_t c = 0, dc = 0, qf_phase = 0;
+  uint32_t su0 = 0, su1 = 0, pu0 = 0, pu1 = 0;  // per-buffer use counts (S events, P data)
+  auto wait_sfree = [&](uint32_t b) {
+    if (b == 0) { mbar_wait(smem_u32(&sm.sfree[0]), (su0 & 1) ^ 1); ++su0; }
+    else        { mbar_wait(smem_u32(&sm.sfree[1]), (su1 & 1) ^ 1); ++su1; }
+  };
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-    mbar_wait(smem_u32(&sm.qfull), qfull_phase);
-    qfull_phase ^= 1;
+    mbar_wait(smem_u32(&sm.qfull), qf_phase);
+    qf_phase ^= 1;
     tc_fence_after();
     bool have_prev = false, o_started = false;
-    int prev_stage = 0;
+    uint32_t prev_vs = 0, prev_b = 0, k = 0;
+    int prev_kind = kBlk;
     for (;;) {
-      mbar_wait(smem_u32(&sm.full[stage]), fphase);
-      const ChunkMeta& m = sm.meta[stage];
-      const int kind = m.kind;
+      const uint32_t ks = c % kKSt;
+      mbar_wait(smem_u32(&sm.kfull[ks]), (c / kKSt) & 1);
+      const int kind = sm.meta[ks].kind;
       if (kind == kBar) fence_proxy_async_smem();
       tc_fence_after();
-      // S buffer b must be free (softmax done reading it)
-      mbar_wait(smem_u32(&sm.sfree[b]), sfree_phase[b] ^ 1);
-      sfree_phase[b] ^= 1;
-      sm.smeta[b].kind = kind;
-      sm.smeta[b].flags = m.flags;
-      sm.smeta[b].mask[0] = m.mask[0];
-      sm.smeta[b].mask[1] = m.mask[1];
-      mbar_arrive(smem_u32(&sm.sfull[b]));  // 1st of 2 arrivals: publishes smeta[b]
       if (kind != kEnd) {
-        const uint32_t kb0 = smem_u32(sm.k[stage]);
-        const uint32_t tm_s = tmem + 128 + 64 * b;
+        const uint32_t b = k & 1;
+        wait_sfree(b);
+        if (leader) sm.smeta[b].kind = kind;
+        if (leader) sm.smeta[b].n = sm.meta[ks].n;
+        if (leader) sm.smeta[b].flags = sm.meta[ks].flags;
+        if (leader) mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
+        const uint64_t dk = sdesc_add(dk0, ks * kTileKV);
+        const uint32_t ts = tmem + kColS + 64 * b;
 #pragma unroll
-        for (int kk = 0; kk < 128; kk += 16) {
-          const uint64_t ad = make_sdesc(q0 + (kk >> 6) * 16384 + (kk & 63) * 2, 16, 1024);
-          const uint64_t bd = make_sdesc(kb0 + (kk >> 6) * 8192 + (kk & 63) * 2, 16, 1024);
-          mma_ss(tm_s, ad, bd, idesc_s, kk > 0);
-        }
-        mma_commit(smem_u32(&sm.sfull[b]));  // 2nd arrival: S ready
+        for (int kk = 0; kk < 128; kk += 16)
+          if (leader) mma_ss(ts, sdesc_add(dk, (kk >> 6) * 16384 + (kk & 63) * 2),
+                 sdesc_add(dq0, (kk >> 6) * 8192 + (kk & 63) * 2), id_s, kk > 0);
+        if (leader) mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T ready
+        if (leader) mma_commit(smem_u32(&sm.kempty[ks]));
       } else {
-        mma_commit(smem_u32(&sm.qempty));  // all S MMAs of this tile done -> Q reusable
+        if (leader) mma_commit(smem_u32(&sm.qempty));  // every S^T of the tile issued before
+        if (leader) mbar_arrive(smem_u32(&sm.kempty[ks]));
       }
-      // O += P(prev) V(prev)
-      if (have_prev) {
-        mbar_wait(smem_u32(&sm.pfull), pfull_phase);
-        pfull_phase ^= 1;
+      if (have_prev) {  // O^T += V^T P^T of the previous data chunk
+        mbar_wait(smem_u32(&sm.vfull[prev_vs]), ((dc - 1) / kVSt) & 1);
+        if (prev_kind == kBar) fence_proxy_async_smem();
+        if (prev_b == 0) { mbar_wait(smem_u32(&sm.pfull[0]), pu0 & 1); ++pu0; }
+        else             { mbar_wait(smem_u32(&sm.pfull[1]), pu1 & 1); ++pu1; }
         tc_fence_after();
-        const uint32_t vb0 = smem_u32(sm.v[prev_stage]);
+        const uint64_t dv = sdesc_add(dv0, prev_vs * kTileKV);
+        const uint64_t dp = sdesc_add(dp0, prev_b * kTileP);
 #pragma unroll
-        for (int kk = 0; kk < 64; kk += 16) {
-          const uint64_t ad = make_sdesc(p0 + kk * 2, 16, 1024);
-          const uint64_t bd = make_sdesc(vb0 + kk * 128, 8192, 1024);
-          mma_ss(tm_o, ad, bd, idesc_o, (o_started || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < 128; kk += 16)
+          if (leader) mma_ss(tmem + kColO, sdesc_add(dv, kk * 128), sdesc_add(dp, kk * 128), id_o,
+                 (o_started || kk > 0) ? 1u : 0u);
         o_started = true;
-        mma_commit(smem_u32(&sm.pvdone));
-        mma_commit(smem_u32(&sm.empty[prev_stage]));
+        if (leader) mma_commit(smem_u32(&sm.obar[prev_b]));
+        if (leader) mma_commit(smem_u32(&sm.vempty[prev_vs]));
       }
+      ++c;
       if (kind == kEnd) {
-        mbar_arrive(smem_u32(&sm.empty[stage]));
-        mbar_arrive(smem_u32(&sm.sfull[b]));
+        for (uint32_t b = 0; b < 2; ++b) {
+          wait_sfree(b);
+          if (leader) sm.smeta[b].kind = kEnd;
+          if (leader) mbar_arrive(smem_u32(&sm.sfull[b]));
+          if (leader) mbar_arrive(smem_u32(&sm.sfull[b]));
+        }
+        break;
       }
-      have_prev = (kind != kEnd);
-      prev_stage = stage;
-      b ^= 1;
-      if (++stage == kStages) { stage = 0; fphase ^= 1; }
-      if (kind == kEnd) break;
+      have_prev = true;
+      prev_b = k & 1;
+      prev_vs = dc % kVSt;
+      prev_kind = kind;
+      ++dc;
+      ++k;
     }
   }
 }
 
 // ------------------------------------------------------------------ softmax + epilogue
+// Reduce 32 columns across the 32 lanes of a warp (recursive halving, 31
+// shuffles): afterwards lane L holds the reduction of column L.
+template <bool kMax>
+__device__ __forceinline__ float warp_colreduce(float* x) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = lane & w;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = upper ? x[i] : x[i + w];
+      const float keep = upper ? x[i + w] : x[i];
+      const float got = __shfl_xor_sync(0xffffffffu, send, w);
+      x[i] = kMax ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  return x[0];
+}
+
+__device__ __forceinline__ float4 lds_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Warpgroup `wg` owns S^T / P^T buffer wg and processes the tile's chunks
+// k = wg (mod 2), all 64 query columns; warp w covers TMEM lanes 32*(w%4)...
+// The stabiliser m_q is the exact column max of the tile's chunk 0 (computed by
+// warpgroup 0, handed to warpgroup 1 through the mready mbarrier).  A score
+// more than 2^64 above it marks the tile for the exact fix-up pass.
 __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
-  const int wq = warp_id() & 3;                 // TMEM lane quadrant
-  const int row = wq * 32 + lane_id();          // tile row == TMEM lane
-  const int slot = row >> 6, i = row & 63;
-  const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-  const VSPlan& pl = P.plan;
-  const int Hq = pl.Hq;
+  const int w = warp_id();
+  const int quad = w & 3, wg = (w - 4) >> 2;
+  const int lane = lane_id();
+  const int row = quad * 32 + lane;  // key row of S^T (and d row of O^T)
+  const uint32_t lb = ((uint32_t)(quad * 32) << 16);
+  const int Hq = P.plan.Hq;
   const int64_t S_loc = (int64_t)P.nloc * 64;
-  int b = 0;
-  uint32_t sfull_phase[2] = {0, 0};
-  uint32_t pv_waits = 0;
-  const uint32_t prow = smem_u32(sm.p) + row * 128;
+  const uint32_t sfull = smem_u32(&sm.sfull[wg]), sfree = smem_u32(&sm.sfree[wg]);
+  const uint32_t pfull = smem_u32(&sm.pfull[wg]), obar = smem_u32(&sm.obar[wg]);
+  const uint32_t mready = smem_u32(&sm.mready);
+  const uint32_t prow = smem_u32(sm.p[wg]) + row * 128;
+  uint32_t su = 0, pc = 0, pw = 0, mr_phase = 0;
 
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-    int h, j0;
-    tile_coords(P, tile, h, j0);
-    const int jx = j0 + slot;
-    const bool valid = jx < P.nloc;
-    float m_run = -INFINITY, l_run = 0.f;
-    int nchunks = 0;
+    int h, j;
+    tile_coords(P, tile, h, j);
+    float l[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) l[i] = 0.f;
+    bool m_synced = false;
+    bool ovf = false;
     for (;;) {
-      mbar_wait(smem_u32(&sm.sfull[b]), sfull_phase[b]);
-      sfull_phase[b] ^= 1;
-      const int kind = sm.smeta[b].kind;
-      if (kind == kEnd) {
-        mbar_arrive(smem_u32(&sm.sfree[b]));
-        b ^= 1;
+      mbar_wait(sfull, su & 1);
+      ++su;
+      const SMeta cm = sm.smeta[wg];
+      if (cm.kind == kEnd) {
+        mbar_arrive(sfree);
         break;
       }
-      const uint32_t flags = sm.smeta[b].flags;
-      const uint64_t cmask = sm.smeta[b].mask[slot];
       tc_fence_after();
       uint32_t sr[64];
-      tmem_ld32(tmem + lane_base + 128 + 64 * b, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld32(tmem + lb + kColS + 64 * wg, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(tmem + lb + kColS + 64 * wg + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(smem_u32(&sm.sfree[b]));
-      // masks
-      bool use;
-      uint64_t vis;  // visible columns of this row
-      if (kind == kBlock) {
-        use = (flags >> slot) & 1u;
-        const bool diag = (flags >> (2 + slot)) & 1u;
-        vis = diag ? ((i == 63) ? ~0ull : ((2ull << i) - 1ull)) : ~0ull;
+      mbar_arrive(sfree);
+      const int kk = row & 63;
+      bool live, diag;
+      if (cm.kind == kBlk) {
+        live = row < 64 || (cm.flags & 1u);
+        diag = (row < 64) ? (cm.flags & 2u) : (cm.flags & 4u);
       } else {
-        vis = cmask;
-        use = true;
+        live = row < cm.n;
+        diag = false;
       }
-      if (!use || !valid) vis = 0ull;
       float x[64];
-      float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        x[c] = ((vis >> c) & 1ull) ? __uint_as_float(sr[c]) * P.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, x[c]);
+      for (int i = 0; i < 64; ++i) {
+        const bool ok = live && (!diag || kk <= i);
+        x[i] = ok ? __uint_as_float(sr[i]) * P.scale_log2 : -INFINITY;
       }
-      // conditional rescale: move the stabiliser only when the max grew by > 8 (log2)
-      float alpha = 1.f;
-      bool resc = false;
-      if (mx > m_run + 8.f || (m_run == -INFINITY && mx > -INFINITY)) {
-        const float m_new = mx;
-        alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_new);
-        resc = (m_run != -INFINITY);
-        m_run = m_new;
+      if (!m_synced) {
+        if (wg == 0) {
+          // exact column max of this chunk over the 128 rows (4 warps)
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float tmp[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tmp[i] = x[half * 32 + i];
+            sm.red[half][quad][lane] = warp_colreduce<true>(tmp);
+          }
+          named_bar_sync(1, 128);
+          if (quad < 2) {
+            const int half = quad;
+            sm.m[half * 32 + lane] =
+                fmaxf(fmaxf(sm.red[half][0][lane], sm.red[half][1][lane]),
+                      fmaxf(sm.red[half][2][lane], sm.red[half][3][lane]));
+          }
+          named_bar_sync(1, 128);
+          mbar_arrive(mready);
+        } else {
+          mbar_wait(mready, mr_phase);
+        }
+        m_synced = true;
       }
-      float lsum = 0.f;
       uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        const float p0 = (x[c] == -INFINITY) ? 0.f : exp2f(x[c] - m_run);
-        const float p1 = (x[c + 1] == -INFINITY) ? 0.f : exp2f(x[c + 1] - m_run);
-        lsum += p0 + p1;
-        pk[c >> 1] = pack_bf16x2(p0, p1);
+      for (int i = 0; i < 64; i += 4) {
+        const float4 m4 = lds_f4(&sm.m[i]);
+        ovf |= (x[i] > m4.x + kOverflow) | (x[i + 1] > m4.y + kOverflow) |
+               (x[i + 2] > m4.z + kOverflow) | (x[i + 3] > m4.w + kOverflow);
+        const float p0 = ex2(x[i] - m4.x), p1 = ex2(x[i + 1] - m4.y);
+        const float p2 = ex2(x[i + 2] - m4.z), p3 = ex2(x[i + 3] - m4.w);
+        l[i] += p0;
+        l[i + 1] += p1;
+        l[i + 2] += p2;
+        l[i + 3] += p3;
+        pk[i >> 1] = pack_bf16x2(p0, p1);
+        pk[(i >> 1) + 1] = pack_bf16x2(p2, p3);
       }
-      l_run = l_run * alpha + lsum;
-      // previous PV must be complete: P buffer free, O stable
-      if (nchunks > 0) {
-        mbar_wait(smem_u32(&sm.pvdone), pv_waits & 1);
-        ++pv_waits;
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, resc)) {
-          const float a = resc ? alpha : 1.f;
-#pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_base + c0, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * a);
-            tmem_st32(tmem + lane_base + c0, o);
-          }
-          tmem_st_wait();
-        }
+      while (pw < pc) {  // the O^T that last read this P^T buffer is complete
+        mbar_wait(obar, pw & 1);
+        ++pw;
       }
-      // P row -> smem (K-major SW128: 8 x 16-byte pieces)
 #pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) {
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ((c16 ^ (row & 7)) << 4)),
-                     "r"(pk[4 * c16]), "r"(pk[4 * c16 + 1]), "r"(pk[4 * c16 + 2]),
-                     "r"(pk[4 * c16 + 3])
+      for (int u = 0; u < 8; ++u)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                         prow + (((uint32_t)u ^ (uint32_t)(row & 7)) << 4)),
+                     "r"(pk[4 * u]), "r"(pk[4 * u + 1]), "r"(pk[4 * u + 2]), "r"(pk[4 * u + 3])
                      : "memory");
-      }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(smem_u32(&sm.pfull));
-      ++nchunks;
-      b ^= 1;
+      mbar_arrive(pfull);
+      ++pc;
     }
+    // keep the once-per-tile mready phase aligned even without data chunks
+    if (!m_synced) {
+      if (wg == 0) mbar_arrive(mready);
+      else mbar_wait(mready, mr_phase);
+    }
+    mr_phase ^= 1;
+    if (ovf) sm.ovf = 1;
 
-    // ---- epilogue: O' = O / l, LSE' = (m + log2 l) ln 2; merge into the running result
-    float inv_l = 0.f, lse_new = -INFINITY;
-    if (nchunks > 0) {
-      mbar_wait(smem_u32(&sm.pvdone), pv_waits & 1);
-      ++pv_waits;
-      tc_fence_after();
+    // ---- epilogue (both warpgroups): l_q, O = O^T / l, LSE, merge with the running result
+    while (pw < pc) {
+      mbar_wait(obar, pw & 1);
+      ++pw;
     }
-    if (l_run > 0.f) {
-      inv_l = 1.f / l_run;
-      lse_new = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-    }
-    const int64_t tok = (int64_t)jx * 64 + i;
-    float* lse_p = valid ? P.lse + (int64_t)h * S_loc + tok : nullptr;
-    float lse_old = -INFINITY;
-    if (!P.first && valid) lse_old = *lse_p;
-    const float lse_m = fmaxf(lse_old, lse_new);
-    float w_old = 0.f, w_new = 0.f, lse_out = -INFINITY;
-    if (lse_m > -INFINITY) {
-      const float eo = (lse_old == -INFINITY) ? 0.f : __expf(lse_old - lse_m);
-      const float en = (lse_new == -INFINITY) ? 0.f : __expf(lse_new - lse_m);
-      const float tot = eo + en;
-      lse_out = lse_m + __logf(tot);
-      w_old = eo / tot;
-      w_new = en / tot * inv_l;
-    }
-    const size_t obase = ((size_t)tok * Hq + h) * 128;
-#pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      uint32_t o[32];
-      if (nchunks > 0) {
-        tmem_ld32(tmem + lane_base + c0, o);
-        tmem_ld_wait();
-      } else {
+    tc_fence_after();
+    named_bar_sync(3, kSoftmax);  // every O^T of the tile complete, ovf flags posted
+    sm.lsum[wg][quad][lane] = warp_colreduce<false>(&l[0]);
+    sm.lsum[wg][quad][32 + lane] = warp_colreduce<false>(&l[32]);
+    const bool tile_ovf = sm.ovf != 0;
+    named_bar_sync(3, kSoftmax);
+    const int64_t tok0 = (int64_t)j * 64;
+    if (wg == 0 && quad < 2) {
+      const int q = quad * 32 + lane;
+      float lq = 0.f;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) o[c] = 0u;
-      }
-      if (!valid) continue;
-      float res[32];
-      if (!P.first) {
-        const float4* src = reinterpret_cast<const float4*>(P.o_acc + obase + c0);
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float4 a = src[c];
-          res[4 * c] = a.x * w_old;
-          res[4 * c + 1] = a.y * w_old;
-          res[4 * c + 2] = a.z * w_old;
-          res[4 * c + 3] = a.w * w_old;
+        for (int b = 0; b < 4; ++b) lq += sm.lsum[a][b][q];
+      float* lp = P.lse + (int64_t)h * S_loc + tok0 + q;
+      float wa = 0.f, wb = 0.f;
+      if (!tile_ovf) {
+        float lse_new = -INFINITY, inv_l = 0.f;
+        if (lq > 0.f) {
+          inv_l = 1.f / lq;
+          lse_new = (sm.m[q] + __log2f(lq)) * 0.69314718055994531f;
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) res[c] = 0.f;
+        const float lse_old = P.first ? -INFINITY : *lp;
+        const float mx = fmaxf(lse_old, lse_new);
+        float out = -INFINITY;
+        if (mx > -INFINITY) {
+          const float eo = lse_old == -INFINITY ? 0.f : __expf(lse_old - mx);
+          const float en = lse_new == -INFINITY ? 0.f : __expf(lse_new - mx);
+          out = mx + __logf(eo + en);
+          wa = eo / (eo + en);
+          wb = en / (eo + en) * inv_l;
+        }
+        *lp = out;
       }
-#pragma unroll
-      for (int c = 0; c < 32; ++c) res[c] += __uint_as_float(o[c]) * w_new;
-      if (P.last) {
-        uint4* dst = reinterpret_cast<uint4*>(P.o + obase + c0);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          dst[c] = make_uint4(pack_bf16x2(res[8 * c], res[8 * c + 1]),
-                              pack_bf16x2(res[8 * c + 2], res[8 * c + 3]),
-                              pack_bf16x2(res[8 * c + 4], res[8 * c + 5]),
-                              pack_bf16x2(res[8 * c + 6], res[8 * c + 7]));
-      } else {
-        float4* dst = reinterpret_cast<float4*>(P.o_acc + obase + c0);
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          dst[c] = make_float4(res[4 * c], res[4 * c + 1], res[4 * c + 2], res[4 * c + 3]);
+      sm.wa[q] = wa;
+      sm.wb[q] = wb;
+      if (q == 0 && tile_ovf) P.fix_list[atomicAdd(P.fix_count, 1)] = tile;
+    }
+    named_bar_sync(3, kSoftmax);
+    if (!tile_ovf) {  // flagged tiles are written by the exact fix-up pass
+      const int col0 = wg * 32;
+      uint32_t o[32];
+      tmem_ld32(tmem + lb + kColO + col0, o);
+      tmem_ld_wait();
+      const size_t qstride = (size_t)Hq * 128;
+      const size_t base = (size_t)tok0 * qstride + (size_t)h * 128 + row;  // O[tok][h][d=row]
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        const int q = col0 + i;
+        float val = __uint_as_float(o[i]) * sm.wb[q];
+        if (!P.first) val += sm.wa[q] * P.o_acc[base + (size_t)q * qstride];
+        if (P.last)
+          P.o[base + (size_t)q * qstride] = __float2bfloat16_rn(val);
+        else
+          P.o_acc[base + (size_t)q * qstride] = val;
       }
     }
-    if (valid) *lse_p = lse_out;
     tc_fence_before();
+    if (threadIdx.x == 128) sm.ovf = 0;
+    named_bar_sync(3, kSoftmax);  // m / wa / wb / lsum / ovf are reused by the next tile
   }
 }
 
@@ -526,23 +602,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                      ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // dynamic shared memory starts 1024-aligned (no static __shared__ in this kernel);
+  // using it directly keeps LDS/STS (not generic) addressing for every Smem field
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = warp_id();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), 1);
+    for (int s = 0; s < kKSt; ++s) {
+      mbar_init(smem_u32(&sm.kfull[s]), 1);
+      mbar_init(smem_u32(&sm.kempty[s]), 1);
+    }
+    for (int s = 0; s < kVSt; ++s) {
+      mbar_init(smem_u32(&sm.vfull[s]), 1);
+      mbar_init(smem_u32(&sm.vempty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.sfull[b]), 2);
-      mbar_init(smem_u32(&sm.sfree[b]), 128);
+      mbar_init(smem_u32(&sm.sfree[b]), 128);  // buffer b belongs to softmax warpgroup b
+      mbar_init(smem_u32(&sm.pfull[b]), 128);
+      mbar_init(smem_u32(&sm.obar[b]), 1);
     }
     mbar_init(smem_u32(&sm.qfull), 1);
     mbar_init(smem_u32(&sm.qempty), 1);
-    mbar_init(smem_u32(&sm.pfull), 128);
-    mbar_init(smem_u32(&sm.pvdone), 1);
+    mbar_init(smem_u32(&sm.mready), 128);
+    sm.ovf = 0;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(smem_u32(&sm.tmem_base), 256);
@@ -555,13 +639,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-
-  if (warp == 0) {
-    producer(sm, P, &tmq, &tmk, &tmv);
-  } else if (warp == 1) {
-    if (lane_id() == 0) mma_issuer(sm, P, tmem);
-    __syncwarp();
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+    if (warp == 0) {
+      producer(sm, P, &tmq, &tmk, &tmv);
+    } else if (warp == 1) {
+      mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
+    }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
     softmax_epilogue(sm, P, tmem);
   }
   tc_fence_before();
@@ -570,11 +656,102 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 256);
 }
 
+// ------------------------------------------------------------------ exact fix-up
+// Tiles whose scores exceeded the first-chunk stabiliser by > 2^64 are redone
+// here with an exact two-pass softmax on CUDA cores (one warp per query, lane =
+// 4 head dims).  Never taken on realistic inputs; it keeps the kernel correct
+// on adversarial ones.
+template <typename F>
+__device__ __forceinline__ void for_each_key(const Params& P, int h, int g, int i, F&& fn) {
+  const VSPlan& pl = P.plan;
+  const int W = pl.W;
+  const int ns = pl.s_cnt[h];
+  const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
+  for (int x = 0; x < ns; ++x) {
+    const int o = offs[x];
+    if (o > g) break;
+    if ((o % W) != P.t) continue;
+    const int lb = (g - o - P.s) / W;
+    const int lim = (o == 0) ? i : 63;  // diagonal block: causal
+    for (int kk = 0; kk <= lim; ++kk) fn(lb * 64 + kk);
+  }
+  const int32_t* vc = pl.vcol + (int64_t)h * pl.S;
+  const int vb = pl.vptr[h * (W + 1) + P.s], ve = pl.vptr[h * (W + 1) + P.s + 1];
+  for (int e = vb; e < ve; ++e) {
+    const int m = vc[e];
+    const int blk = m >> 6;
+    if (blk >= g) break;
+    if (plan_has_slash(pl, h, g - blk)) continue;
+    fn(((blk - P.s) / W) * 64 + (m & 63));
+  }
+}
+
+__global__ void __launch_bounds__(256) attn_fwd_fixup(const __grid_constant__ Params P,
+                                                      const __nv_bfloat16* __restrict__ q) {
+  const int n = *P.fix_count;
+  const int lane = lane_id(), w = warp_id();
+  const VSPlan& pl = P.plan;
+  const int grp = pl.Hq / pl.Hkv;
+  const int64_t S_loc = (int64_t)P.nloc * 64;
+  for (int f = blockIdx.x; f < n; f += gridDim.x) {
+    int h, j;
+    tile_coords(P, P.fix_list[f], h, j);
+    const int g = j * pl.W + P.r, gkv = h / grp;
+    for (int i = w; i < 64; i += 8) {
+      const int64_t tok = (int64_t)j * 64 + i;
+      float qv[4];
+      const __nv_bfloat16* qr = q + ((size_t)tok * pl.Hq + h) * 128 + lane * 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) qv[u] = __bfloat162float(qr[u]);
+      auto score = [&](int row) {
+        const __nv_bfloat16* kr = P.k + ((size_t)row * pl.Hkv + gkv) * 128 + lane * 4;
+        float sdot = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sdot += qv[u] * __bfloat162float(kr[u]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+        return sdot * P.scale_log2;
+      };
+      float mx = -INFINITY;
+      for_each_key(P, h, g, i, [&](int row) { mx = fmaxf(mx, score(row)); });
+      float l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for_each_key(P, h, g, i, [&](int row) {
+        const float p = exp2f(score(row) - mx);
+        l += p;
+        const __nv_bfloat16* vr = P.v + ((size_t)row * pl.Hkv + gkv) * 128 + lane * 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += p * __bfloat162float(vr[u]);
+      });
+      const float lse_new = l > 0.f ? (mx + log2f(l)) * 0.69314718055994531f : -INFINITY;
+      float* lp = P.lse + (int64_t)h * S_loc + tok;
+      const float lse_old = P.first ? -INFINITY : *lp;
+      const float m2 = fmaxf(lse_old, lse_new);
+      float wa = 0.f, wb = 0.f, out = -INFINITY;
+      if (m2 > -INFINITY) {
+        const float eo = lse_old == -INFINITY ? 0.f : expf(lse_old - m2);
+        const float en = lse_new == -INFINITY ? 0.f : expf(lse_new - m2);
+        out = m2 + logf(eo + en);
+        wa = eo / (eo + en);
+        wb = l > 0.f ? en / (eo + en) / l : 0.f;
+      }
+      const size_t base = ((size_t)tok * pl.Hq + h) * 128 + lane * 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float val = acc[u] * wb;
+        if (!P.first) val += wa * P.o_acc[base + u];
+        if (P.last) P.o[base + u] = __float2bfloat16_rn(val);
+        else P.o_acc[base + u] = val;
+      }
+      __syncwarp();
+      if (lane == 0) *lp = out;
+    }
+  }
+}
+
 }  // namespace fwd
 
 size_t fwd_smem_bytes() { return sizeof(fwd::Smem) + 1024; }
 
-// One ring step of the forward (or the whole forward when W = 1).
 mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* q,
                         const void* k, const void* v, void* o, float* o_acc, float* lse,
                         int first, int last, int num_sms, cudaStream_t st) {
@@ -585,7 +762,7 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.s = s;
   P.t = ((r - s) % plan.W + plan.W) % plan.W;
   P.nloc = nloc;
-  P.n_tiles = plan.Hq * ((nloc + 1) / 2);
+  P.n_tiles = plan.Hq * nloc;
   P.first = first;
   P.last = last;
   P.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
@@ -594,6 +771,8 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.o = static_cast<__nv_bfloat16*>(o);
   P.o_acc = o_acc;
   P.lse = lse;
+  P.fix_count = plan.scratch;
+  P.fix_list = plan.scratch + 16;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmk, tmv;
   if (make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
@@ -605,12 +784,15 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   if (!attr_done) {
     if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
-      return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_fwd) failed");
+      return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_fwd) failed (smem %zu)", smem);
     attr_done = true;
   }
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
+  cudaMemsetAsync(P.fix_count, 0, sizeof(int), st);
   if (grid > 0) attn_fwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv);
-  return check_launch("attn_fwd_kernel");
+  MT_TRY(check_launch("attn_fwd_kernel"));
+  attn_fwd_fixup<<<num_sms, 256, 0, st>>>(P, static_cast<const __nv_bfloat16*>(q));
+  return check_launch("attn_fwd_fixup");
 }
 
 }  // namespace mt

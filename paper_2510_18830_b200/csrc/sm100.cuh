@@ -13,11 +13,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cstdio>
 
 #ifndef MT_SPIN_TIMEOUT_CYCLES
 // Bounded waits: a stuck pipeline traps (a CUDA error the host sees) instead of
-// hanging the GPU.  ~8 s at 2 GHz.
-#define MT_SPIN_TIMEOUT_CYCLES (1ull << 34)
+// hanging the GPU.  ~2 s at 2 GHz.
+#define MT_SPIN_TIMEOUT_CYCLES (1ull << 32)
 #endif
 
 namespace mt {
@@ -64,11 +65,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Debug breadcrumbs (per block, 4 words): roles may record progress here; the
+// timeout message prints them.
+__device__ volatile int g_mt_dbg[1024][4];
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const unsigned long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > MT_SPIN_TIMEOUT_CYCLES) __trap();
+    if (clock64() - t0 > MT_SPIN_TIMEOUT_CYCLES) {
+      const int b = blockIdx.x & 1023;
+      printf("mt: mbarrier timeout smem=0x%x parity=%u block=%d thread=%d dbg=%d,%d,%d,%d\n",
+             bar, parity, (int)blockIdx.x, (int)threadIdx.x, g_mt_dbg[b][0], g_mt_dbg[b][1],
+             g_mt_dbg[b][2], g_mt_dbg[b][3]);
+      __trap();
+    }
   }
 }
 // cp.async (LDGSTS) completion -> mbarrier arrive (non-counting variant: the
@@ -156,6 +167,12 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)1u << 46;  // version (sm_100)
   d |= (uint64_t)2u << 61;  // SWIZZLE_128B
   return d;
+}
+
+// Advance a descriptor's start address by `bytes` (16-byte multiple).  Valid
+// while the address field does not overflow (shared memory < 256 KB).
+__device__ __forceinline__ uint64_t sdesc_add(uint64_t d, uint32_t bytes) {
+  return d + (uint64_t)(bytes >> 4);
 }
 
 // D[tmem] (+)= A[smem] * B[smem]

@@ -87,6 +87,8 @@ size_t vs_plan_bytes(int64_t S, int Hq, int W) {
   b += (size_t)Hq * (W + 1) * 4;
   b = (b + 255) & ~size_t(255);
   b += (size_t)Hq * S * 4;
+  b = (b + 255) & ~size_t(255);
+  b += (size_t)(16 + (int64_t)Hq * nb) * 4;  // scratch
   return (b + 255) & ~size_t(255);
 }
 
@@ -102,6 +104,8 @@ mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const in
   int32_t* vptr = reinterpret_cast<int32_t*>(p + off);
   off = (off + (size_t)Hq * (W + 1) * 4 + 255) & ~size_t(255);
   int32_t* vcol = reinterpret_cast<int32_t*>(p + off);
+  off = (off + (size_t)Hq * S * 4 + 255) & ~size_t(255);
+  int32_t* scratch = reinterpret_cast<int32_t*>(p + off);
   VSPlan pl{};
   pl.S = S;
   pl.Hq = Hq;
@@ -115,6 +119,7 @@ mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const in
   pl.s_bits = bits;
   pl.vptr = vptr;
   pl.vcol = vcol;
+  pl.scratch = scratch;
   vs_plan_kernel<<<Hq, kThreads, 0, st>>>(pl, v_cnt, v_idx, v_stride, bits, vptr, vcol);
   MT_TRY(check_launch("vs_plan_kernel"));
   *out = pl;
