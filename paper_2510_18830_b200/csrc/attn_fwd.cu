@@ -20,7 +20,8 @@
 // from warpgroup 0 to the softmax warpgroups):
 //   warp 0       producer (chunk stream from the VSPlan, TMA / cp.async)
 //   warp 1       MMA issuer (one lane)
-//   warps 2, 3   idle
+//   warp 2       V producer (decoupled from K through a metadata ring)
+//   warp 3       idle
 //   warps 4..11  two softmax warpgroups; warpgroup g takes the tile's chunks
 //                k = g (mod 2); warp w covers TMEM lanes 32*(w%4)..
 #include "common.cuh"
@@ -42,13 +43,23 @@ constexpr float kOverflow = 64.f;            // log2 headroom before the stabili
 
 enum : int { kBlk = 0, kBar = 1, kEnd = 2 };
 
-struct alignas(16) ChunkMeta {
+struct alignas(16) ChunkMeta {  // per K slot: what the MMA / softmax need
   int kind;
   int n;           // kBar: live rows
   uint32_t flags;  // kBlk: bit0 rows 64..127 live, bit1 rows 0..63 diagonal, bit2 rows 64..127 diagonal
-  int lb0, lb1;
-  int rows[128];   // kBar local rows (producer only)
+  int pad;
 };
+
+struct alignas(16) VMeta {  // per data chunk: what the producers need to stage K/V
+  int kind;
+  int n;
+  int lb0, lb1;
+  int gkv;
+  int pad[3];
+  int rows[128];   // kBar local rows
+};
+
+constexpr int kVM = 4;  // V-metadata ring depth
 
 struct SMeta {
   int kind, n;
@@ -62,6 +73,7 @@ struct Smem {
   uint8_t q[kTileQ];
   uint8_t p[2][kTileP];
   ChunkMeta meta[kKSt];
+  VMeta vmeta[kVM];
   SMeta smeta[2];
   alignas(16) float red[2][4][32];  // column-max partials (two 32-column halves)
   alignas(16) float lsum[2][4][64]; // per WG, per lane quadrant: row-sum partials
@@ -72,6 +84,7 @@ struct Smem {
   int ovf;
   uint64_t kfull[kKSt], kempty[kKSt], vfull[kVSt], vempty[kVSt];
   uint64_t sfull[2], sfree[2], pfull[2], obar[2];
+  uint64_t vmfull[kVM], vmfree[kVM];
   uint64_t qfull, qempty, mready;
   uint32_t tmem_base;
 };
@@ -100,64 +113,33 @@ __device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h, i
   h = tile % Hq;
 }
 
-// ------------------------------------------------------------------ producer
-// K of chunk c is issued as soon as its K slot frees (after S^T(c-3)); V lags by
-// one chunk (issued after K(c+1)) because its slot frees later (after the O^T two
-// data chunks back).  K slots (and the chunk meta) are indexed by every chunk
-// including END markers; V slots only by data chunks, so an END never advances
-// a V barrier ahead of the producer (parity aliasing).
-__device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
-                         const CUtensorMap* tmk, const CUtensorMap* tmv) {
+// ------------------------------------------------------------------ producers
+// Warp 0 builds the chunk stream and issues K (slot frees after S^T three chunks
+// back); warp 2 issues V (slot frees after the O^T two data chunks back).  They
+// are decoupled by a 4-entry ring of V metadata, so a late V slot never delays
+// the next K.  K slots (and the per-chunk meta the MMA reads) are indexed by
+// every chunk including END markers; V slots only by data chunks.
+__device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
+                           const CUtensorMap* tmk) {
   const int lane = lane_id();
   const VSPlan& pl = P.plan;
   const int W = pl.W;
   const int grp = pl.Hq / pl.Hkv;
-  uint32_t c = 0;  // chunk counter (incl. END markers)
+  uint32_t c = 0, dk = 0;  // chunks (incl. END), data chunks
   uint32_t qe_phase = 0;
   bool first_tile = true;
-  // pending V load (the previous chunk)
-  bool vpend = false;
-  uint32_t vp_c = 0, dv = 0;  // pending chunk, data-chunk counter (V slots)
-  int vp_gkv = 0;
 
   auto kacquire = [&]() {
     mbar_wait(smem_u32(&sm.kempty[c % kKSt]), ((c / kKSt) & 1) ^ 1);
   };
-  auto flush_v = [&]() {
-    if (!vpend) return;
-    vpend = false;
-    const uint32_t vs = dv % kVSt, ks = vp_c % kKSt;
-    mbar_wait(smem_u32(&sm.vempty[vs]), ((dv / kVSt) & 1) ^ 1);
-    ++dv;
-    const ChunkMeta& m = sm.meta[ks];
-    const uint32_t vb = smem_u32(&sm.vfull[vs]);
-    if (m.kind == kBlk) {
-      if (lane == 0) {
-        mbar_expect_tx(vb, kTileKV);
-        for (int cc = 0; cc < 2; ++cc)
-          for (int x = 0; x < 2; ++x)
-            tma_load_3d(smem_u32(sm.v[vs] + cc * 16384 + x * 8192), tmv, vb, cc * 64, vp_gkv,
-                        (x ? m.lb1 : m.lb0) * 64);
-      }
-    } else if (m.kind == kBar) {
-      const uint32_t vbase = smem_u32(sm.v[vs]);
-      for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
-        const int row = pidx >> 4, c16 = pidx & 15;
-        const size_t goff = ((size_t)m.rows[row] * pl.Hkv + vp_gkv) * 128 + c16 * 8;
-        cp_async_16(vbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.v + goff);
-      }
-      asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(vb) : "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(vb);
-    }
-    __syncwarp();
+  auto vmacquire = [&]() -> VMeta& {
+    mbar_wait(smem_u32(&sm.vmfree[dk % kVM]), ((dk / kVM) & 1) ^ 1);
+    return sm.vmeta[dk % kVM];
   };
-  auto push = [&](int gkv, bool data) {  // chunk c's K is issued; its V becomes pending
-    flush_v();
-    vpend = data;
-    vp_c = c;
-    vp_gkv = gkv;
-    ++c;
+  auto vmrelease = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&sm.vmfull[dk % kVM]));
+    ++dk;
   };
 
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
@@ -201,14 +183,17 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         if (o1 >= 0) flags |= 1u;
         if (o0 == 0) flags |= 2u;
         if (o1 == 0) flags |= 4u;
+        VMeta& vm = vmacquire();
         kacquire();
         if (lane == 0) {
+          vm.kind = kBlk;
+          vm.lb0 = lb0;
+          vm.lb1 = lb1;
+          vm.gkv = gkv;
           const uint32_t ks = c % kKSt;
           ChunkMeta& m = sm.meta[ks];
           m.kind = kBlk;
           m.flags = flags;
-          m.lb0 = lb0;
-          m.lb1 = lb1;
           const uint32_t kb = smem_u32(&sm.kfull[ks]);
           mbar_expect_tx(kb, kTileKV);
           for (int cc = 0; cc < 2; ++cc)
@@ -216,8 +201,8 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
               tma_load_3d(smem_u32(sm.k[ks] + cc * 16384 + x * 8192), tmk, kb, cc * 64, gkv,
                           (x ? lb1 : lb0) * 64);
         }
-        __syncwarp();
-        push(gkv, true);
+        vmrelease();
+        ++c;
       }
     }
     // ---- bars of origin s: block < g, offset not a selected slash; 128 per chunk
@@ -227,26 +212,30 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       const int ve = pl.vptr[h * (W + 1) + P.s + 1];
       int nst = 0;
       auto emit = [&](int n) {
+        VMeta& vm = vmacquire();
         kacquire();
         const uint32_t ks = c % kKSt;
-        ChunkMeta& m = sm.meta[ks];
-        for (int x = lane; x < 128; x += 32) m.rows[x] = sm.stage_rows[x < n ? x : 0];
+        for (int x = lane; x < 128; x += 32) vm.rows[x] = sm.stage_rows[x < n ? x : 0];
         if (lane == 0) {
-          m.kind = kBar;
-          m.n = n;
+          vm.kind = kBar;
+          vm.n = n;
+          vm.gkv = gkv;
+          sm.meta[ks].kind = kBar;
+          sm.meta[ks].n = n;
         }
         __syncwarp();
         const uint32_t kbase = smem_u32(sm.k[ks]);
         for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
           const int row = pidx >> 4, c16 = pidx & 15;
-          const size_t goff = ((size_t)m.rows[row] * pl.Hkv + gkv) * 128 + c16 * 8;
+          const size_t goff = ((size_t)vm.rows[row] * pl.Hkv + gkv) * 128 + c16 * 8;
           cp_async_16(kbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.k + goff);
         }
         const uint32_t kb = smem_u32(&sm.kfull[ks]);
         asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(kb) : "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(kb);
-        push(gkv, true);
+        vmrelease();
+        ++c;
         const int rem = nst - n;  // shift the remaining staged columns down
         int t0 = 0;
         if (lane < rem) t0 = sm.stage_rows[n + lane];
@@ -277,7 +266,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       }
       if (nst > 0) emit(nst);
     }
-    // ---- END
+    // ---- END (K slot + meta only)
     kacquire();
     if (lane == 0) {
       const uint32_t ks = c % kKSt;
@@ -285,15 +274,55 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       mbar_arrive(smem_u32(&sm.kfull[ks]));
     }
     __syncwarp();
-    push(gkv, false);  // flushes the tile's last V
+    ++c;
   }
-  flush_v();
+  // tell the V producer there is nothing more
+  VMeta& vm = vmacquire();
+  if (lane == 0) vm.kind = kEnd;
+  vmrelease();
+}
+
+__device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
+  const int lane = lane_id();
+  const VSPlan& pl = P.plan;
+  for (uint32_t dv = 0;; ++dv) {
+    mbar_wait(smem_u32(&sm.vmfull[dv % kVM]), (dv / kVM) & 1);
+    const VMeta& vm = sm.vmeta[dv % kVM];
+    const int kind = vm.kind;
+    if (kind == kEnd) break;
+    const uint32_t vs = dv % kVSt;
+    mbar_wait(smem_u32(&sm.vempty[vs]), ((dv / kVSt) & 1) ^ 1);
+    const uint32_t vb = smem_u32(&sm.vfull[vs]);
+    if (kind == kBlk) {
+      if (lane == 0) {
+        mbar_expect_tx(vb, kTileKV);
+        for (int cc = 0; cc < 2; ++cc)
+          for (int x = 0; x < 2; ++x)
+            tma_load_3d(smem_u32(sm.v[vs] + cc * 16384 + x * 8192), tmv, vb, cc * 64, vm.gkv,
+                        (x ? vm.lb1 : vm.lb0) * 64);
+      }
+    } else {
+      const uint32_t vbase = smem_u32(sm.v[vs]);
+      for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
+        const int row = pidx >> 4, c16 = pidx & 15;
+        const size_t goff = ((size_t)vm.rows[row] * pl.Hkv + vm.gkv) * 128 + c16 * 8;
+        cp_async_16(vbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.v + goff);
+      }
+      asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(vb) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(vb);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&sm.vmfree[dv % kVM]));
+  }
 }
 
 // ------------------------------------------------------------------ MMA issuer
 // Chunk k of a tile goes to S^T / P^T buffer k & 1, i.e. to softmax warpgroup
 // k & 1: the two warpgroups alternate chunks so one computes while the tensor
-// core works for the other.  END is published to both warpgroups.
+// core works for the other.  O^T for a chunk is issued two chunks later (after
+// S^T(k + 2)), so a warpgroup's next S^T never waits for its own P^T.  END is
+// published to both warpgroups after the tile's last O^T.
 __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const bool leader = elect_one();
   const uint32_t id_s = make_idesc_bf16(128, 64, false, false);
@@ -303,76 +332,85 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dk0 = make_sdesc(smem_u32(sm.k[0]), 16, 1024);
   const uint64_t dv0 = make_sdesc(smem_u32(sm.v[0]), 16384, 1024);
   const uint64_t dp0 = make_sdesc(smem_u32(sm.p[0]), 8192, 1024);
-  uint32_t c = 0, dc = 0, qf_phase = 0;
-  uint32_t su0 = 0, su1 = 0, pu0 = 0, pu1 = 0;  // per-buffer use counts (S events, P data)
+  uint32_t c = 0, dc = 0, oc = 0, qf_phase = 0;  // chunks, data chunks S-issued, O^T-issued
+  uint32_t su0 = 0, su1 = 0, pu0 = 0, pu1 = 0;   // per-buffer use counts (S events, P data)
+  bool o_started = false;
+  int kind_ring[4];
+  uint32_t buf_ring[4];  // S^T / P^T buffer of each pending data chunk (tile-local parity)
   auto wait_sfree = [&](uint32_t b) {
     if (b == 0) { mbar_wait(smem_u32(&sm.sfree[0]), (su0 & 1) ^ 1); ++su0; }
     else        { mbar_wait(smem_u32(&sm.sfree[1]), (su1 & 1) ^ 1); ++su1; }
+  };
+  // O^T += V^T P^T for the oldest data chunk not yet accumulated (oc)
+  auto issue_o = [&]() {
+    const uint32_t b = buf_ring[oc & 3], vs = oc % kVSt;
+    mbar_wait(smem_u32(&sm.vfull[vs]), (oc / kVSt) & 1);
+    if (kind_ring[oc & 3] == kBar) fence_proxy_async_smem();
+    if (b == 0) { mbar_wait(smem_u32(&sm.pfull[0]), pu0 & 1); ++pu0; }
+    else        { mbar_wait(smem_u32(&sm.pfull[1]), pu1 & 1); ++pu1; }
+    tc_fence_after();
+    const uint64_t dv = sdesc_add(dv0, vs * kTileKV), dp = sdesc_add(dp0, b * kTileP);
+    if (leader) {
+#pragma unroll
+      for (int kk = 0; kk < 128; kk += 16)
+        mma_ss(tmem + kColO, sdesc_add(dv, kk * 128), sdesc_add(dp, kk * 128), id_o,
+               (o_started || kk > 0) ? 1u : 0u);
+      mma_commit(smem_u32(&sm.obar[b]));
+      mma_commit(smem_u32(&sm.vempty[vs]));
+    }
+    o_started = true;
+    ++oc;
   };
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
     mbar_wait(smem_u32(&sm.qfull), qf_phase);
     qf_phase ^= 1;
     tc_fence_after();
-    bool have_prev = false, o_started = false;
-    uint32_t prev_vs = 0, prev_b = 0, k = 0;
-    int prev_kind = kBlk;
+    o_started = false;
+    uint32_t k = 0;  // chunk index inside the tile (data chunks)
     for (;;) {
       const uint32_t ks = c % kKSt;
       mbar_wait(smem_u32(&sm.kfull[ks]), (c / kKSt) & 1);
       const int kind = sm.meta[ks].kind;
       if (kind == kBar) fence_proxy_async_smem();
       tc_fence_after();
-      if (kind != kEnd) {
-        const uint32_t b = k & 1;
-        wait_sfree(b);
-        if (leader) sm.smeta[b].kind = kind;
-        if (leader) sm.smeta[b].n = sm.meta[ks].n;
-        if (leader) sm.smeta[b].flags = sm.meta[ks].flags;
-        if (leader) mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
+      ++c;
+      if (kind == kEnd) {
+        if (leader) {
+          mma_commit(smem_u32(&sm.qempty));  // every S^T of the tile issued before
+          mbar_arrive(smem_u32(&sm.kempty[ks]));
+        }
+        while (oc < dc) issue_o();
+        for (uint32_t b = 0; b < 2; ++b) {
+          wait_sfree(b);
+          if (leader) {
+            sm.smeta[b].kind = kEnd;
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+          }
+        }
+        break;
+      }
+      const uint32_t b = k & 1;
+      wait_sfree(b);
+      if (leader) {
+        sm.smeta[b].kind = kind;
+        sm.smeta[b].n = sm.meta[ks].n;
+        sm.smeta[b].flags = sm.meta[ks].flags;
+        mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
         const uint64_t dk = sdesc_add(dk0, ks * kTileKV);
         const uint32_t ts = tmem + kColS + 64 * b;
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16)
-          if (leader) mma_ss(ts, sdesc_add(dk, (kk >> 6) * 16384 + (kk & 63) * 2),
+          mma_ss(ts, sdesc_add(dk, (kk >> 6) * 16384 + (kk & 63) * 2),
                  sdesc_add(dq0, (kk >> 6) * 8192 + (kk & 63) * 2), id_s, kk > 0);
-        if (leader) mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T ready
-        if (leader) mma_commit(smem_u32(&sm.kempty[ks]));
-      } else {
-        if (leader) mma_commit(smem_u32(&sm.qempty));  // every S^T of the tile issued before
-        if (leader) mbar_arrive(smem_u32(&sm.kempty[ks]));
+        mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T ready
+        mma_commit(smem_u32(&sm.kempty[ks]));
       }
-      if (have_prev) {  // O^T += V^T P^T of the previous data chunk
-        mbar_wait(smem_u32(&sm.vfull[prev_vs]), ((dc - 1) / kVSt) & 1);
-        if (prev_kind == kBar) fence_proxy_async_smem();
-        if (prev_b == 0) { mbar_wait(smem_u32(&sm.pfull[0]), pu0 & 1); ++pu0; }
-        else             { mbar_wait(smem_u32(&sm.pfull[1]), pu1 & 1); ++pu1; }
-        tc_fence_after();
-        const uint64_t dv = sdesc_add(dv0, prev_vs * kTileKV);
-        const uint64_t dp = sdesc_add(dp0, prev_b * kTileP);
-#pragma unroll
-        for (int kk = 0; kk < 128; kk += 16)
-          if (leader) mma_ss(tmem + kColO, sdesc_add(dv, kk * 128), sdesc_add(dp, kk * 128), id_o,
-                 (o_started || kk > 0) ? 1u : 0u);
-        o_started = true;
-        if (leader) mma_commit(smem_u32(&sm.obar[prev_b]));
-        if (leader) mma_commit(smem_u32(&sm.vempty[prev_vs]));
-      }
-      ++c;
-      if (kind == kEnd) {
-        for (uint32_t b = 0; b < 2; ++b) {
-          wait_sfree(b);
-          if (leader) sm.smeta[b].kind = kEnd;
-          if (leader) mbar_arrive(smem_u32(&sm.sfull[b]));
-          if (leader) mbar_arrive(smem_u32(&sm.sfull[b]));
-        }
-        break;
-      }
-      have_prev = true;
-      prev_b = k & 1;
-      prev_vs = dc % kVSt;
-      prev_kind = kind;
+      kind_ring[dc & 3] = kind;
+      buf_ring[dc & 3] = b;
       ++dc;
       ++k;
+      if (dc - oc > 2) issue_o();  // O^T lags S^T by two data chunks
     }
   }
 }
@@ -626,6 +664,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&sm.qfull), 1);
     mbar_init(smem_u32(&sm.qempty), 1);
     mbar_init(smem_u32(&sm.mready), 128);
+    for (int i = 0; i < kVM; ++i) {
+      mbar_init(smem_u32(&sm.vmfull[i]), 1);
+      mbar_init(smem_u32(&sm.vmfree[i]), 1);
+    }
     sm.ovf = 0;
     fence_barrier_init();
   }
@@ -642,7 +684,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
     if (warp == 0) {
-      producer(sm, P, &tmq, &tmk, &tmv);
+      producer_k(sm, P, &tmq, &tmk);
+    } else if (warp == 2) {
+      producer_v(sm, P, &tmv);
     } else if (warp == 1) {
       mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
     }
