@@ -32,8 +32,8 @@ namespace mt {
 
 namespace bwd {
 
-constexpr int kStages = 3;
-constexpr int kThreads = 192;
+constexpr int kStages = 2;      // Q / dO / LSE / D stages
+constexpr int kThreads = 384;   // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
 constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
@@ -41,16 +41,17 @@ constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
 enum : int { kModeBlock = 0, kModeBar = 1 };
 enum : int { kChunk = 0, kEnd = 1 };
 
-// TMEM columns
+// TMEM columns: dK, dV accumulators; one S^T / dP^T pair shared by the two
+// softmax warpgroups (each loads it to registers at once); dQ^T per warpgroup.
 constexpr uint32_t kColDK = 0, kColDV = 128, kColS = 256, kColDP = 320, kColDQ = 384;
 
-struct ChunkMeta {
+struct alignas(16) ChunkMeta {
   int kind;
-  int h;        // q head
-  int j;        // local query block
+  int h;           // q head
+  int j;           // local query block
   uint32_t flags;  // BLOCK: bit0/1 slot0/1 live, bit2/3 slot0/1 diagonal
-  int stage;    // smem stage holding the chunk's Q / dO / LSE / D
-  int pad;
+  int stage;       // smem stage holding the chunk's Q / dO / LSE / D
+  int pad[3];
 };
 
 struct Smem {
@@ -58,16 +59,17 @@ struct Smem {
   uint8_t v[kTileKV];
   uint8_t q[kStages][kTileQ];
   uint8_t dO[kStages][kTileQ];
-  uint8_t pT[kTileP];
-  uint8_t dsT[kTileP];
-  float lse[kStages][64];
-  float dd[kStages][64];
+  uint8_t pT[2][kTileP];   // per softmax warpgroup
+  uint8_t dsT[2][kTileP];
+  alignas(16) float lse[kStages][64];
+  alignas(16) float dd[kStages][64];
   ChunkMeta meta[kStages];
-  ChunkMeta smeta;          // handed to the softmax (single S buffer)
-  int cols[128];            // BAR: global column of each key row (-1 = padding)
-  int tile_rows;            // BAR: live rows in the tile
+  ChunkMeta smeta[2];      // handed to softmax warpgroup 0 / 1
+  int cols[128];           // BAR: global column of each key row (-1 = padding)
+  int tile_chunks[2];      // chunks each softmax warpgroup saw in the current tile
   uint64_t full[kStages], empty[kStages];
-  uint64_t kvfull, kvempty, sfull, sfree, dsfull, dqfull;
+  uint64_t kvfull, kvempty, tfree;
+  uint64_t sfull[2], sfree, dsfull[2], gdone[2], dqfree[2];
   uint32_t tmem_base;
 };
 
@@ -109,7 +111,6 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
     T.lb0 = 2 * (tile / pl.Hkv);  // early key blocks (most work) first
     return T;
   }
-  // BAR: walk heads, ceil(len/128) tiles each
   int base = 0;
   for (int h = 0; h < pl.Hq; ++h) {
     const int b = pl.vptr[h * (W + 1) + P.s], e = pl.vptr[h * (W + 1) + P.s + 1];
@@ -136,25 +137,23 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
   const int W = pl.W;
   const int grp = pl.Hq / pl.Hkv;
   const int64_t S_loc = (int64_t)P.nloc * 64;
-  int stage = 0;
-  uint32_t ephase = 0, kve_phase = 0;
-  bool first_tile = true;
-  auto next_stage = [&]() {
-    if (++stage == kStages) { stage = 0; ephase ^= 1; }
-  };
+  uint32_t c = 0;  // chunk events (incl. END)
+  uint32_t ntile = 0;
   auto emit = [&](int h, int j, uint32_t flags) {
-    mbar_wait(smem_u32(&sm.empty[stage]), ephase ^ 1);
+    const uint32_t stage = c % kStages;
+    mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
     if (lane == 0) {
       ChunkMeta& m = sm.meta[stage];
       m.kind = kChunk;
       m.h = h;
       m.j = j;
       m.flags = flags;
+      m.stage = (int)stage;
       const uint32_t bar = smem_u32(&sm.full[stage]);
       mbar_expect_tx(bar, 2 * kTileQ + 512);
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d(smem_u32(sm.q[stage] + c * 8192), tmq, bar, c * 64, h, j * 64);
-        tma_load_3d(smem_u32(sm.dO[stage] + c * 8192), tmdo, bar, c * 64, h, j * 64);
+      for (int cc = 0; cc < 2; ++cc) {
+        tma_load_3d(smem_u32(sm.q[stage] + cc * 8192), tmq, bar, cc * 64, h, j * 64);
+        tma_load_3d(smem_u32(sm.dO[stage] + cc * 8192), tmdo, bar, cc * 64, h, j * 64);
       }
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
@@ -168,18 +167,19 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
           : "memory");
     }
     __syncwarp();
-    next_stage();
+    ++c;
   };
 
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
     const Tile T = decode_tile(P, tile);
     if (!T.ok) break;
-    // ---- K/V tile (held until every chunk of the tile finished)
-    if (!first_tile) {
-      mbar_wait(smem_u32(&sm.kvempty), kve_phase);
-      kve_phase ^= 1;
+    // ---- K/V tile: wait until every MMA of the previous tile finished and its
+    // epilogue (which reads cols[]) is done
+    if (ntile > 0) {
+      mbar_wait(smem_u32(&sm.kvempty), (ntile - 1) & 1);
+      mbar_wait(smem_u32(&sm.tfree), (ntile - 1) & 1);
     }
-    first_tile = false;
+    ++ntile;
     const uint32_t kvbar = smem_u32(&sm.kvfull);
     if (P.mode == kModeBlock) {
       const bool v1 = T.lb0 + 1 < P.nloc;
@@ -188,22 +188,18 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         // because dQ^T = K^T dS^T contracts over all 128 rows (masked rows have dS = 0)
         mbar_expect_tx(kvbar, 2 * kTileKV);
         for (int sl = 0; sl < 2; ++sl)
-          for (int c = 0; c < 2; ++c) {
-            const uint32_t off = c * 16384 + sl * 8192;
+          for (int cc = 0; cc < 2; ++cc) {
+            const uint32_t off = cc * 16384 + sl * 8192;
             const int blk = v1 ? T.lb0 + sl : T.lb0;
-            tma_load_3d(smem_u32(sm.k + off), tmk, kvbar, c * 64, T.g, blk * 64);
-            tma_load_3d(smem_u32(sm.v + off), tmv, kvbar, c * 64, T.g, blk * 64);
+            tma_load_3d(smem_u32(sm.k + off), tmk, kvbar, cc * 64, T.g, blk * 64);
+            tma_load_3d(smem_u32(sm.v + off), tmv, kvbar, cc * 64, T.g, blk * 64);
           }
       }
       __syncwarp();
     } else {
       const int n = T.e1 - T.e0;
       const int32_t* vc = pl.vcol + (int64_t)T.h * pl.S;
-      for (int rr = lane; rr < 128; rr += 32) {
-        int m = rr < n ? vc[T.e0 + rr] : -1;
-        sm.cols[rr] = m;
-      }
-      if (lane == 0) sm.tile_rows = n;
+      for (int rr = lane; rr < 128; rr += 32) sm.cols[rr] = rr < n ? vc[T.e0 + rr] : -1;
       __syncwarp();
       const uint32_t kb = smem_u32(sm.k), vb = smem_u32(sm.v);
       const int m0 = sm.cols[0];
@@ -233,7 +229,6 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         const int ns = pl.s_cnt[h];
         const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
         // query blocks gq = kb + o for o = t (mod W), merged over the two key slots
-        int ia = 0, ib = 0;
         auto next_valid = [&](int i, int kb) {
           if (kb < 0) return ns;
           while (i < ns) {
@@ -244,8 +239,8 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
           }
           return i;
         };
-        ia = next_valid(0, kb0);
-        ib = next_valid(0, kb1);
+        int ia = next_valid(0, kb0);
+        int ib = next_valid(0, kb1);
         while (ia < ns || ib < ns) {
           const int qa = ia < ns ? kb0 + offs[ia] : INT32_MAX;
           const int qb = ib < ns ? kb1 + offs[ib] : INT32_MAX;
@@ -257,25 +252,30 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         }
       }
     } else {
-      const int mfirst = sm.cols[0];
-      const int bfirst = mfirst >> 6;
+      const int bfirst = sm.cols[0] >> 6;
       // first rank-local query block with global block > bfirst
       int j = (bfirst + 1 - P.r + W - 1) / W;
       if (bfirst + 1 - P.r <= 0) j = 0;
       for (; j < P.nloc; ++j) emit(T.h, j, 0u);
     }
     // ---- END
-    mbar_wait(smem_u32(&sm.empty[stage]), ephase ^ 1);
-    if (lane == 0) {
-      sm.meta[stage].kind = kEnd;
-      mbar_arrive(smem_u32(&sm.full[stage]));
+    {
+      const uint32_t stage = c % kStages;
+      mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
+      if (lane == 0) {
+        sm.meta[stage].kind = kEnd;
+        mbar_arrive(smem_u32(&sm.full[stage]));
+      }
+      __syncwarp();
+      ++c;
     }
-    __syncwarp();
-    next_stage();
   }
 }
 
 // ------------------------------------------------------------------ MMA issuer
+// Chunk k of a tile goes to softmax warpgroup k & 1.  Per chunk: S^T, dP^T into
+// the shared TMEM pair, then the gradient MMAs of the previous chunk (dV, dK
+// accumulate; dQ^T into that warpgroup's buffer).
 __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const bool leader = elect_one();
   const uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // S^T, dP^T
@@ -289,70 +289,103 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dO0 = make_sdesc(smem_u32(sm.dO[0]), 16, 1024);
   const uint64_t dQmn0 = make_sdesc(smem_u32(sm.q[0]), 8192, 1024);
   const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
-  const uint64_t dPT = make_sdesc(smem_u32(sm.pT), 16, 1024);
-  const uint64_t dDST = make_sdesc(smem_u32(sm.dsT), 16, 1024);
-  const uint64_t dDSTmn = make_sdesc(smem_u32(sm.dsT), 8192, 1024);
-  int stage = 0;
-  uint32_t fphase = 0, kvf_phase = 0, sfree_phase = 0, dsf_phase = 0;
+  const uint64_t dPT0 = make_sdesc(smem_u32(sm.pT[0]), 16, 1024);
+  const uint64_t dDST0 = make_sdesc(smem_u32(sm.dsT[0]), 16, 1024);
+  const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.dsT[0]), 8192, 1024);
+  uint32_t c = 0, ntile = 0;
+  uint32_t s_issued = 0, s_waited = 0;          // S^T/dP^T fills vs releases waited
+  uint32_t ds0 = 0, ds1 = 0, gq0 = 0, gq1 = 0;  // per buffer: dsfull waits, grads issued
+  auto wait_s_released = [&]() {
+    while (s_waited < s_issued) {
+      mbar_wait(smem_u32(&sm.sfree), s_waited & 1);
+      ++s_waited;
+    }
+  };
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
     const Tile T = decode_tile(P, tile);
     if (!T.ok) break;
-    mbar_wait(smem_u32(&sm.kvfull), kvf_phase);
-    kvf_phase ^= 1;
+    mbar_wait(smem_u32(&sm.kvfull), ntile & 1);
+    ++ntile;
     if (P.mode == kModeBar) fence_proxy_async_smem();
     tc_fence_after();
     bool have_prev = false, acc_started = false;
-    int prev_stage = 0;
+    uint32_t prev_stage = 0, prev_b = 0, k = 0;
+    auto grads = [&]() {  // gradient MMAs of the previous chunk (buffer prev_b)
+      if (prev_b == 0) {
+        mbar_wait(smem_u32(&sm.dsfull[0]), ds0 & 1);
+        ++ds0;
+        if (gq0 > 0) mbar_wait(smem_u32(&sm.dqfree[0]), (gq0 - 1) & 1);
+        ++gq0;
+      } else {
+        mbar_wait(smem_u32(&sm.dsfull[1]), ds1 & 1);
+        ++ds1;
+        if (gq1 > 0) mbar_wait(smem_u32(&sm.dqfree[1]), (gq1 - 1) & 1);
+        ++gq1;
+      }
+      tc_fence_after();
+      const uint64_t dqm = sdesc_add(dQmn0, prev_stage * kTileQ);
+      const uint64_t dom = sdesc_add(dOmn0, prev_stage * kTileQ);
+      const uint64_t dpt = sdesc_add(dPT0, prev_b * kTileP);
+      const uint64_t dst = sdesc_add(dDST0, prev_b * kTileP);
+      const uint64_t dstm = sdesc_add(dDSTmn0, prev_b * kTileP);
+      if (leader) {
+#pragma unroll
+        for (int kq = 0; kq < 64; kq += 16) {
+          const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
+          mma_ss(tmem + kColDV, sdesc_add(dpt, kq * 2), sdesc_add(dom, kq * 128), id_kv, acc);
+          mma_ss(tmem + kColDK, sdesc_add(dst, kq * 2), sdesc_add(dqm, kq * 128), id_kv, acc);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 128; kk += 16)
+          mma_ss(tmem + kColDQ + 64 * prev_b, sdesc_add(dKmn, kk * 128),
+                 sdesc_add(dstm, kk * 128), id_q, kk > 0);
+        mma_commit(smem_u32(&sm.gdone[prev_b]));
+        mma_commit(smem_u32(&sm.empty[prev_stage]));
+      }
+      acc_started = true;
+    };
     for (;;) {
-      mbar_wait(smem_u32(&sm.full[stage]), fphase);
+      const uint32_t stage = c % kStages;
+      mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
       const int kind = sm.meta[stage].kind;
       tc_fence_after();
-      mbar_wait(smem_u32(&sm.sfree), sfree_phase ^ 1);
-      sfree_phase ^= 1;
-      if (leader) sm.smeta = sm.meta[stage];
-      if (leader) sm.smeta.stage = stage;
-      if (leader) mbar_arrive(smem_u32(&sm.sfull));  // 1st arrival publishes smeta
-      if (kind == kChunk) {
+      ++c;
+      if (kind == kEnd) {
+        if (have_prev) grads();
+        if (leader) {
+          mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
+          mbar_arrive(smem_u32(&sm.empty[stage]));
+        }
+        wait_s_released();
+        for (uint32_t b = 0; b < 2; ++b)
+          if (leader) {
+            sm.smeta[b].kind = kEnd;
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+          }
+        break;
+      }
+      const uint32_t b = k & 1;
+      wait_s_released();
+      if (leader) {
+        sm.smeta[b] = sm.meta[stage];
+        mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
         const uint64_t dq = sdesc_add(dQ0, stage * kTileQ), ddo = sdesc_add(dO0, stage * kTileQ);
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16) {
           const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
           const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
-          if (leader) mma_ss(tmem + kColS, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
-          if (leader) mma_ss(tmem + kColDP, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
+          mma_ss(tmem + kColS, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
+          mma_ss(tmem + kColDP, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
         }
-        if (leader) mma_commit(smem_u32(&sm.sfull));  // 2nd arrival: S^T, dP^T ready
-      } else {
-        if (leader) mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
+        mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
       }
-      if (have_prev) {
-        mbar_wait(smem_u32(&sm.dsfull), dsf_phase);
-        dsf_phase ^= 1;
-        tc_fence_after();
-        const uint64_t dqm = sdesc_add(dQmn0, prev_stage * kTileQ);
-        const uint64_t dom = sdesc_add(dOmn0, prev_stage * kTileQ);
-#pragma unroll
-        for (int kq = 0; kq < 64; kq += 16) {
-          const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
-          if (leader) mma_ss(tmem + kColDV, sdesc_add(dPT, kq * 2), sdesc_add(dom, kq * 128), id_kv, acc);
-          if (leader) mma_ss(tmem + kColDK, sdesc_add(dDST, kq * 2), sdesc_add(dqm, kq * 128), id_kv, acc);
-        }
-        acc_started = true;
-#pragma unroll
-        for (int kk = 0; kk < 128; kk += 16)
-          if (leader) mma_ss(tmem + kColDQ, sdesc_add(dKmn, kk * 128), sdesc_add(dDSTmn, kk * 128), id_q,
-                 kk > 0);
-        if (leader) mma_commit(smem_u32(&sm.dqfull));
-        if (leader) mma_commit(smem_u32(&sm.empty[prev_stage]));
-      }
-      if (kind == kEnd) {
-        if (leader) mbar_arrive(smem_u32(&sm.empty[stage]));
-        if (leader) mbar_arrive(smem_u32(&sm.sfull));
-      }
-      have_prev = (kind == kChunk);
+      ++s_issued;
+      if (have_prev) grads();
+      have_prev = true;
       prev_stage = stage;
-      if (++stage == kStages) { stage = 0; fphase ^= 1; }
-      if (kind == kEnd) break;
+      prev_b = b;
+      ++k;
     }
   }
 }
@@ -362,26 +395,40 @@ __device__ __forceinline__ void red_add_f32(float* addr, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
-  const int wq = warp_id() & 3;
-  const int row = wq * 32 + lane_id();   // key row of the tile == TMEM lane; d index for dQ^T
+  const int w = warp_id();
+  const int quad = w & 3, wg = (w - 4) >> 2;
+  const int lane = lane_id();
+  const int row = quad * 32 + lane;  // key row of the tile == TMEM lane; d index for dQ^T
   const int slot = row >> 6, kk = row & 63;
-  const uint32_t lb = (uint32_t)(wq * 32) << 16;
+  const uint32_t lb = (uint32_t)(quad * 32) << 16;
   const VSPlan& pl = P.plan;
   const int Hq = pl.Hq, W = pl.W;
   const size_t qstride = (size_t)Hq * 128;
-  uint32_t sfull_phase = 0, dq_phase = 0;
-  const uint32_t prow = smem_u32(sm.pT) + row * 128, drow = smem_u32(sm.dsT) + row * 128;
+  const uint32_t sfull = smem_u32(&sm.sfull[wg]), sfree = smem_u32(&sm.sfree);
+  const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
+  const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
+  const uint32_t prow = smem_u32(sm.pT[wg]) + row * 128, drow = smem_u32(sm.dsT[wg]) + row * 128;
+  uint32_t su = 0, gw = 0;  // sfull events, gdone waits
+  uint32_t ntile = 0;
 
-  // dQ^T row `row` (= d index) of the last chunk -> dQ[q][h][row] for its 64 queries
+  // dQ^T of this warpgroup's previous chunk (h, j) -> dQ[q][h][d = row]
   auto drain_dq = [&](int h, int j) {
-    mbar_wait(smem_u32(&sm.dqfull), dq_phase);
-    dq_phase ^= 1;
+    mbar_wait(gdone, gw & 1);
+    ++gw;
     tc_fence_after();
     uint32_t r0[32], r1[32];
-    tmem_ld32(tmem + lb + kColDQ, r0);
-    tmem_ld32(tmem + lb + kColDQ + 32, r1);
+    tmem_ld32(tmem + lb + kColDQ + 64 * wg, r0);
+    tmem_ld32(tmem + lb + kColDQ + 64 * wg + 32, r1);
     tmem_ld_wait();
+    tc_fence_before();
+    mbar_arrive(dqfree);
     float* base = P.dq + (size_t)j * 64 * qstride + (size_t)h * 128 + row;
 #pragma unroll
     for (int c = 0; c < 32; ++c) red_add_f32(base + c * qstride, __uint_as_float(r0[c]));
@@ -392,16 +439,13 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
   for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
     const Tile T = decode_tile(P, tile);
     if (!T.ok) break;
-    int my_col = -2;  // BAR: resolved after the first chunk (cols[] published via kvfull->MMA)
+    int my_col = -2;  // BAR: this row's column, read at the first chunk
     int prev_h = -1, prev_j = -1;
     for (;;) {
-      mbar_wait(smem_u32(&sm.sfull), sfull_phase);
-      sfull_phase ^= 1;
-      const ChunkMeta cm = sm.smeta;
-      if (cm.kind == kEnd) {
-        mbar_arrive(smem_u32(&sm.sfree));
-        break;
-      }
+      mbar_wait(sfull, su & 1);
+      ++su;
+      const ChunkMeta cm = sm.smeta[wg];
+      if (cm.kind == kEnd) break;
       if (P.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
       tc_fence_after();
       uint32_t sv[64], dpv[64];
@@ -411,13 +455,13 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
       tmem_ld32(tmem + lb + kColDP + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(smem_u32(&sm.sfree));
+      mbar_arrive(sfree);
       // which of the 64 queries see this key row
       uint64_t vis;
       if (P.mode == kModeBlock) {
         const bool live = (cm.flags >> slot) & 1u;
         const bool diag = (cm.flags >> (2 + slot)) & 1u;
-        vis = live ? (diag ? (~0ull << kk) : ~0ull) : 0ull;   // causal: query i >= key kk
+        vis = live ? (diag ? (~0ull << kk) : ~0ull) : 0ull;  // causal: query i >= key kk
         if (slot == 1 && T.lb0 + 1 >= P.nloc) vis = 0ull;
       } else {
         bool live = my_col >= 0;
@@ -443,7 +487,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
           const int q = c + u;
           const bool on = (vis >> q) & 1ull;
           const float x = __uint_as_float(sv[q]) * P.scale_log2 - la[u] * 1.4426950408889634f;
-          p[u] = on ? exp2f(x) : 0.f;
+          p[u] = on ? ex2(x) : 0.f;
           ds[u] = on ? p[u] * (__uint_as_float(dpv[q]) - da[u]) * P.inv_sqrt_d : 0.f;
         }
         pk[c >> 1] = pack_bf16x2(p[0], p[1]);
@@ -451,7 +495,8 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
         dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
         dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
       }
-      // previous chunk's dV/dK/dQ MMAs must be done (P^T/dS^T smem + dQ^T TMEM free)
+      // this warpgroup's previous chunk: its gradient MMAs are done (P^T/dS^T free),
+      // and its dQ^T is drained into the dQ accumulator
       if (prev_h >= 0) drain_dq(prev_h, prev_j);
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) {
@@ -465,58 +510,55 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(smem_u32(&sm.dsfull));
+      mbar_arrive(dsfull);
       prev_h = cm.h;
       prev_j = cm.j;
     }
-    if (prev_h >= 0) drain_dq(prev_h, prev_j);  // also: every MMA of the tile is complete
+    if (prev_h >= 0) drain_dq(prev_h, prev_j);  // also: this warpgroup's MMAs are complete
+    tc_fence_after();
+    if (row == 0) sm.tile_chunks[wg] = prev_h >= 0 ? 1 : 0;
+    named_bar_sync(3, 256);  // both warpgroups: every MMA of the tile complete
+    const bool any_chunk = (sm.tile_chunks[0] | sm.tile_chunks[1]) != 0;  // else TMEM is stale
 
-    // ---- dK / dV epilogue (tile rows): fp32 accumulate into the held chunk's dK/dV
+    // ---- dK (warpgroup 0) / dV (warpgroup 1) epilogue: the tile's key rows
     bool live_row;
     int64_t lrow;
     if (P.mode == kModeBlock) {
-      live_row = prev_h >= 0 && !(slot == 1 && T.lb0 + 1 >= P.nloc);
+      live_row = any_chunk && !(slot == 1 && T.lb0 + 1 >= P.nloc);
       lrow = (int64_t)(T.lb0 + slot) * 64 + kk;
     } else {
-      const int m = my_col;  // cached: the producer may already be refilling cols[]
-      live_row = prev_h >= 0 && m >= 0;
+      const int m = sm.cols[row];
+      live_row = any_chunk && m >= 0;
       lrow = live_row ? (int64_t)(((m >> 6) - P.s) / W) * 64 + (m & 63) : 0;
     }
-    float* dkp = P.dk + ((size_t)lrow * pl.Hkv + T.g) * 128;
-    float* dvp = P.dv + ((size_t)lrow * pl.Hkv + T.g) * 128;
+    float* dst = (wg == 0 ? P.dk : P.dv) + ((size_t)lrow * pl.Hkv + T.g) * 128;
+    const uint32_t col = wg == 0 ? kColDK : kColDV;
 #pragma unroll 1
     for (int c0 = 0; c0 < 128; c0 += 32) {
-      uint32_t a[32], b[32];
-      tmem_ld32(tmem + lb + kColDK + c0, a);
-      tmem_ld32(tmem + lb + kColDV + c0, b);
+      uint32_t a[32];
+      tmem_ld32(tmem + lb + col + c0, a);
       tmem_ld_wait();
       if (!live_row) continue;
       if (P.mode == kModeBlock) {
-        float4* k4 = reinterpret_cast<float4*>(dkp + c0);
-        float4* v4 = reinterpret_cast<float4*>(dvp + c0);
+        float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          float4 x = k4[c], y = v4[c];
+          float4 x = d4[c];
           x.x += __uint_as_float(a[4 * c]);
           x.y += __uint_as_float(a[4 * c + 1]);
           x.z += __uint_as_float(a[4 * c + 2]);
           x.w += __uint_as_float(a[4 * c + 3]);
-          y.x += __uint_as_float(b[4 * c]);
-          y.y += __uint_as_float(b[4 * c + 1]);
-          y.z += __uint_as_float(b[4 * c + 2]);
-          y.w += __uint_as_float(b[4 * c + 3]);
-          k4[c] = x;
-          v4[c] = y;
+          d4[c] = x;
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          red_add_f32(dkp + c0 + c, __uint_as_float(a[c]));
-          red_add_f32(dvp + c0 + c, __uint_as_float(b[c]));
-        }
+        for (int c = 0; c < 32; ++c) red_add_f32(dst + c0 + c, __uint_as_float(a[c]));
       }
     }
     tc_fence_before();
+    named_bar_sync(3, 256);  // TMEM dK/dV and cols[] free for the next tile
+    if (threadIdx.x == 128) mbar_arrive(smem_u32(&sm.tfree));
+    ++ntile;
   }
 }
 
@@ -526,8 +568,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // dynamic shared memory starts 1024-aligned (no static __shared__ in this kernel);
-  // using it directly keeps LDS/STS (not generic) addressing for every Smem field
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = warp_id();
@@ -538,10 +578,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(smem_u32(&sm.kvfull), 1);
     mbar_init(smem_u32(&sm.kvempty), 1);
-    mbar_init(smem_u32(&sm.sfull), 2);
+    mbar_init(smem_u32(&sm.tfree), 1);
     mbar_init(smem_u32(&sm.sfree), 128);
-    mbar_init(smem_u32(&sm.dsfull), 128);
-    mbar_init(smem_u32(&sm.dqfull), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&sm.sfull[b]), 2);
+      mbar_init(smem_u32(&sm.dsfull[b]), 128);
+      mbar_init(smem_u32(&sm.gdone[b]), 1);
+      mbar_init(smem_u32(&sm.dqfree[b]), 128);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(smem_u32(&sm.tmem_base), 512);
@@ -557,11 +601,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  if (warp == 0) {
-    producer(sm, P, &tmq, &tmdo, &tmk, &tmv);
-  } else if (warp == 1) {
-    mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+    if (warp == 0) {
+      producer(sm, P, &tmq, &tmdo, &tmk, &tmv);
+    } else if (warp == 1) {
+      mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
+    }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
     softmax_bwd(sm, P, tmem);
   }
   tc_fence_before();
