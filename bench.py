@@ -27,6 +27,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep rank 0's stdout to the one JSON line
 
 METRIC = "sparse attn fwd+bwd tokens/s at 512K, 1/2/4/8 B200; % of bf16 tensor peak"
 UNIT = "tokens/s"

@@ -45,7 +45,7 @@ def main():
     idx1 = ops.build_vs_index(t(q), t(k), a.p, a.p)
     iv, is_ = idx.to_lists()
     iv1, is1 = idx1.to_lists()
-    ok["index_w_invariant"] = all(np.array_equal(x, y) for x, y in zip(iv + is_, iv1 + is1))
+    ok["index_w_invariant"] = bool(all(np.array_equal(x, y) for x, y in zip(iv + is_, iv1 + is1)))
     # ring forward / backward
     o, lse = ops.ring_attn_fwd(comm, S, ql, kl, vl, idx)
     dq, dk, dv = ops.ring_attn_bwd(comm, S, ql, kl, vl, o, lse, dl, idx)
@@ -79,8 +79,8 @@ def main():
                 "dq": nerr(unstripe(gq, ref[0].shape), ref[0]),
                 "dk": nerr(unstripe(gk, ref[1].shape), ref[1]),
                 "dv": nerr(unstripe(gv, ref[2].shape), ref[2])}
-        ok["fwd"] = errs["o"] <= 2e-2 and errs["lse"] <= 1e-3
-        ok["bwd"] = max(errs["dq"], errs["dk"], errs["dv"]) <= 2e-2
+        ok["fwd"] = bool(errs["o"] <= 2e-2 and errs["lse"] <= 1e-3)
+        ok["bwd"] = bool(max(errs["dq"], errs["dk"], errs["dv"]) <= 2e-2)
         print(json.dumps({"world": W, "inner": a.inner or W, "ok": ok,
                           "errs": {k_: float(v_) for k_, v_ in errs.items()}}), flush=True)
     flag = torch.tensor([1 if all(ok.values()) else 0], device=dev)
