@@ -41,13 +41,13 @@ constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB
 constexpr float kOverflow = 64.f;            // log2 headroom before the stabiliser moves
 
-enum : int { kBlk = 0, kBar = 1, kEnd = 2 };
+enum : int { kBlk = 0, kBar = 1, kEnd = 2, kDone = 3 };
 
 struct alignas(16) ChunkMeta {  // per K slot: what the MMA / softmax need
   int kind;
   int n;           // kBar: live rows
   uint32_t flags;  // kBlk: bit0 rows 64..127 live, bit1 rows 0..63 diagonal, bit2 rows 64..127 diagonal
-  int pad;
+  int tile;        // kEnd: the tile it closes
 };
 
 struct alignas(16) VMeta {  // per data chunk: what the producers need to stage K/V
@@ -64,7 +64,7 @@ constexpr int kVM = 4;  // V-metadata ring depth
 struct SMeta {
   int kind, n;
   uint32_t flags;
-  int pad;
+  int tile;
 };
 
 struct Smem {
@@ -103,6 +103,7 @@ struct Params {
   float* lse;
   int* fix_count;  // tiles flagged for the exact fix-up pass (stabiliser overflow)
   int* fix_list;
+  int* tile_counter;  // dynamic tile scheduler (zeroed before the launch)
 };
 
 constexpr uint32_t kColO = 0, kColS = 64;  // TMEM: O^T [0,64), S^T buffers [64,128) [128,192)
@@ -142,7 +143,11 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     ++dk;
   };
 
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+  for (;;) {
+    int tile = 0;
+    if (lane == 0) tile = atomicAdd(P.tile_counter, 1);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= P.n_tiles) break;
     int h, j;
     tile_coords(P, tile, h, j);
     const int g = j * W + P.r;
@@ -271,11 +276,20 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     if (lane == 0) {
       const uint32_t ks = c % kKSt;
       sm.meta[ks].kind = kEnd;
+      sm.meta[ks].tile = tile;
       mbar_arrive(smem_u32(&sm.kfull[ks]));
     }
     __syncwarp();
     ++c;
   }
+  // ---- DONE: no more tiles for this CTA
+  kacquire();
+  if (lane == 0) {
+    const uint32_t ks = c % kKSt;
+    sm.meta[ks].kind = kDone;
+    mbar_arrive(smem_u32(&sm.kfull[ks]));
+  }
+  __syncwarp();
   // tell the V producer there is nothing more
   VMeta& vm = vmacquire();
   if (lane == 0) vm.kind = kEnd;
@@ -361,7 +375,22 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     o_started = true;
     ++oc;
   };
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+  for (;;) {
+    {  // the next chunk tells whether another tile follows
+      const uint32_t ks = c % kKSt;
+      mbar_wait(smem_u32(&sm.kfull[ks]), (c / kKSt) & 1);
+      if (sm.meta[ks].kind == kDone) {
+        for (uint32_t b = 0; b < 2; ++b) {
+          wait_sfree(b);
+          if (leader) {
+            sm.smeta[b].kind = kDone;
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+          }
+        }
+        break;
+      }
+    }
     mbar_wait(smem_u32(&sm.qfull), qf_phase);
     qf_phase ^= 1;
     tc_fence_after();
@@ -371,6 +400,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint32_t ks = c % kKSt;
       mbar_wait(smem_u32(&sm.kfull[ks]), (c / kKSt) & 1);
       const int kind = sm.meta[ks].kind;
+      const int end_tile = sm.meta[ks].tile;  // read before the slot is released
       if (kind == kBar) fence_proxy_async_smem();
       tc_fence_after();
       ++c;
@@ -384,6 +414,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
           wait_sfree(b);
           if (leader) {
             sm.smeta[b].kind = kEnd;
+            sm.smeta[b].tile = end_tile;
             mbar_arrive(smem_u32(&sm.sfull[b]));
             mbar_arrive(smem_u32(&sm.sfull[b]));
           }
@@ -468,20 +499,20 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
   const uint32_t prow = smem_u32(sm.p[wg]) + row * 128;
   uint32_t su = 0, pc = 0, pw = 0, mr_phase = 0;
 
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-    int h, j;
-    tile_coords(P, tile, h, j);
+  for (;;) {
     float l[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) l[i] = 0.f;
     bool m_synced = false;
     bool ovf = false;
+    int tile = -1;
     for (;;) {
       mbar_wait(sfull, su & 1);
       ++su;
       const SMeta cm = sm.smeta[wg];
-      if (cm.kind == kEnd) {
+      if (cm.kind == kEnd || cm.kind == kDone) {
         mbar_arrive(sfree);
+        tile = cm.kind == kEnd ? cm.tile : -1;
         break;
       }
       tc_fence_after();
@@ -560,6 +591,9 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
       mbar_arrive(pfull);
       ++pc;
     }
+    if (tile < 0) break;  // DONE
+    int h, j;
+    tile_coords(P, tile, h, j);
     // keep the once-per-tile mready phase aligned even without data chunks
     if (!m_synced) {
       if (wg == 0) mbar_arrive(mready);
@@ -816,6 +850,7 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.o_acc = o_acc;
   P.lse = lse;
   P.fix_count = plan.scratch;
+  P.tile_counter = plan.scratch + 1;
   P.fix_list = plan.scratch + 16;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmk, tmv;
@@ -832,7 +867,7 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
     attr_done = true;
   }
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
-  cudaMemsetAsync(P.fix_count, 0, sizeof(int), st);
+  cudaMemsetAsync(P.fix_count, 0, 2 * sizeof(int), st);  // fix-up count, tile counter
   if (grid > 0) attn_fwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv);
   MT_TRY(check_launch("attn_fwd_kernel"));
   attn_fwd_fixup<<<num_sms, 256, 0, st>>>(P, static_cast<const __nv_bfloat16*>(q));
