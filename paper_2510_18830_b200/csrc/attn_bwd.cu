@@ -32,7 +32,7 @@ namespace mt {
 
 namespace bwd {
 
-constexpr int kStages = 2;      // Q / dO / LSE / D stages
+constexpr int kStages = 3;      // Q / dO / LSE / D stages
 constexpr int kThreads = 384;   // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
 constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
@@ -658,7 +658,7 @@ __global__ void f32_to_bf16_kernel(const float* x, __nv_bfloat16* y, int64_t n) 
 
 }  // namespace bwd
 
-size_t bwd_smem_bytes() { return sizeof(bwd::Smem) + 1024; }
+size_t bwd_smem_bytes() { return sizeof(bwd::Smem); }  // the dynamic base is 1024-aligned
 
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
                               cudaStream_t st) {
