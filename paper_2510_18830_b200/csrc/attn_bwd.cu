@@ -23,6 +23,8 @@
 //   dQ^T = K^T dS^T                          (TMEM, M = d) -> red.add to dQ
 // Warp roles: warp 0 producer (TMA / cp.async), warp 1 MMA issuer,
 // warps 2..5 softmax-backward + dQ drain + dK/dV epilogue.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "plan.cuh"
 #include "sm100.cuh"
@@ -39,7 +41,7 @@ constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
 
 enum : int { kModeBlock = 0, kModeBar = 1 };
-enum : int { kChunk = 0, kEnd = 1 };
+enum : int { kChunk = 0, kEnd = 1, kDone = 2 };
 
 // TMEM columns: dK, dV accumulators; one S^T / dP^T pair shared by the two
 // softmax warpgroups (each loads it to registers at once); dQ^T per warpgroup.
@@ -51,7 +53,8 @@ struct alignas(16) ChunkMeta {
   int j;           // local query block
   uint32_t flags;  // BLOCK: bit0/1 slot0/1 live, bit2/3 slot0/1 diagonal
   int stage;       // smem stage holding the chunk's Q / dO / LSE / D
-  int pad[3];
+  int tile;        // kEnd: the tile it closes
+  int pad[2];
 };
 
 struct Smem {
@@ -88,6 +91,8 @@ struct Params {
   float* dq;                // [S_loc][Hq][128] fp32 accumulator (reduce-add)
   float* dk;                // [S_loc][Hkv][128] fp32 accumulator of the held chunk
   float* dv;
+  int* tile_counter;        // dynamic tile scheduler (zeroed before the launch)
+  int static_tiles;         // 1: round-robin tiles instead (A/B switch, MT_BWD_STATIC=1)
 };
 
 // ---- tile decoding
@@ -170,7 +175,14 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     ++c;
   };
 
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+  for (int it = 0;; ++it) {
+    int tile = 0;
+    if (P.static_tiles) {
+      tile = blockIdx.x + it * gridDim.x;
+    } else {
+      if (lane == 0) tile = atomicAdd(P.tile_counter, 1);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+    }
     const Tile T = decode_tile(P, tile);
     if (!T.ok) break;
     // ---- K/V tile: wait until every MMA of the previous tile finished and its
@@ -264,12 +276,21 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
       if (lane == 0) {
         sm.meta[stage].kind = kEnd;
+        sm.meta[stage].tile = tile;
         mbar_arrive(smem_u32(&sm.full[stage]));
       }
       __syncwarp();
       ++c;
     }
   }
+  // ---- DONE
+  const uint32_t stage = c % kStages;
+  mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
+  if (lane == 0) {
+    sm.meta[stage].kind = kDone;
+    mbar_arrive(smem_u32(&sm.full[stage]));
+  }
+  __syncwarp();
 }
 
 // ------------------------------------------------------------------ MMA issuer
@@ -301,9 +322,21 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       ++s_waited;
     }
   };
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-    const Tile T = decode_tile(P, tile);
-    if (!T.ok) break;
+  for (;;) {
+    {  // the next chunk tells whether another tile follows
+      const uint32_t stage = c % kStages;
+      mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
+      if (sm.meta[stage].kind == kDone) {
+        wait_s_released();
+        for (uint32_t b = 0; b < 2; ++b)
+          if (leader) {
+            sm.smeta[b].kind = kDone;
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+            mbar_arrive(smem_u32(&sm.sfull[b]));
+          }
+        break;
+      }
+    }
     mbar_wait(smem_u32(&sm.kvfull), ntile & 1);
     ++ntile;
     if (P.mode == kModeBar) fence_proxy_async_smem();
@@ -348,6 +381,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint32_t stage = c % kStages;
       mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
       const int kind = sm.meta[stage].kind;
+      const int end_tile = sm.meta[stage].tile;  // read before the stage is released
       tc_fence_after();
       ++c;
       if (kind == kEnd) {
@@ -360,6 +394,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         for (uint32_t b = 0; b < 2; ++b)
           if (leader) {
             sm.smeta[b].kind = kEnd;
+            sm.smeta[b].tile = end_tile;
             mbar_arrive(smem_u32(&sm.sfull[b]));
             mbar_arrive(smem_u32(&sm.sfull[b]));
           }
@@ -436,16 +471,18 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
     for (int c = 0; c < 32; ++c) red_add_f32(base + (c + 32) * qstride, __uint_as_float(r1[c]));
   };
 
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
-    const Tile T = decode_tile(P, tile);
-    if (!T.ok) break;
+  for (;;) {
     int my_col = -2;  // BAR: this row's column, read at the first chunk
     int prev_h = -1, prev_j = -1;
+    int tile = -1;
     for (;;) {
       mbar_wait(sfull, su & 1);
       ++su;
       const ChunkMeta cm = sm.smeta[wg];
-      if (cm.kind == kEnd) break;
+      if (cm.kind == kEnd || cm.kind == kDone) {
+        tile = cm.kind == kEnd ? cm.tile : -1;
+        break;
+      }
       if (P.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
       tc_fence_after();
       uint32_t sv[64], dpv[64];
@@ -462,7 +499,6 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
         const bool live = (cm.flags >> slot) & 1u;
         const bool diag = (cm.flags >> (2 + slot)) & 1u;
         vis = live ? (diag ? (~0ull << kk) : ~0ull) : 0ull;  // causal: query i >= key kk
-        if (slot == 1 && T.lb0 + 1 >= P.nloc) vis = 0ull;
       } else {
         bool live = my_col >= 0;
         if (live) {
@@ -514,6 +550,8 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
       prev_h = cm.h;
       prev_j = cm.j;
     }
+    if (tile < 0) break;  // DONE
+    const Tile T = decode_tile(P, tile);
     if (prev_h >= 0) drain_dq(prev_h, prev_j);  // also: this warpgroup's MMAs are complete
     tc_fence_after();
     if (row == 0) sm.tile_chunks[wg] = prev_h >= 0 ? 1 : 0;
@@ -700,6 +738,9 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.dq = dq;
   P.dk = dk;
   P.dv = dv;
+  P.tile_counter = plan.scratch + 2;
+  static const int static_tiles = getenv("MT_BWD_STATIC") ? atoi(getenv("MT_BWD_STATIC")) : 0;
+  P.static_tiles = static_tiles;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmdo, tmk, tmv;
   if (make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
@@ -716,12 +757,14 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
     attr_done = true;
   }
   // block (slash) part
+  cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);  // one counter per launch
   P.mode = kModeBlock;
   P.n_tiles = plan.Hkv * ((nloc + 1) / 2);
   int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   if (grid > 0) attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv);
   MT_TRY(check_launch("attn_bwd_kernel(block)"));
   // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
+  P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;
   P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128);
   grid = num_sms;
