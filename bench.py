@@ -102,7 +102,7 @@ def bits_to_torch(bits: np.ndarray, dev):
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def oracle_sample(q, k, v, dO, p: float, S: int, Hq: int, Hkv: int, n_blocks: int = 24):
+def oracle_sample(q, k, v, dO, p: float, S: int, Hq: int, Hkv: int, n_blocks: int = 384):
     """Time the CPU oracle on a bounded sample of the workload; returns a dict.
 
     Sample: the full Alg. 1 index of q head 0 (VS-IDX v1, C fast path) and the
@@ -302,7 +302,7 @@ def run_reference(args):
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        r = oracle_sample(q, k, v, dO, p, S, Hq, Hkv, n_blocks=8)
+        r = oracle_sample(q, k, v, dO, p, S, Hq, Hkv, n_blocks=48)
         if i >= args.warmup:
             vals.append(r["value"])
         last = r

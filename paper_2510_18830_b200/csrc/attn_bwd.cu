@@ -62,8 +62,9 @@ struct Smem {
   uint8_t v[kTileKV];
   uint8_t q[kStages][kTileQ];
   uint8_t dO[kStages][kTileQ];
-  uint8_t pT[2][kTileP];   // per softmax warpgroup
-  uint8_t dsT[2][kTileP];
+  // per softmax warpgroup: P^T (16 KB) then dS^T (16 KB); the same 32 KB also
+  // stages that warpgroup's dQ tile [64 q][128 d] fp32 for the bulk reduce-add
+  uint8_t pd[2][2 * kTileP];
   alignas(16) float lse[kStages][64];
   alignas(16) float dd[kStages][64];
   ChunkMeta meta[kStages];
@@ -93,6 +94,7 @@ struct Params {
   float* dv;
   int* tile_counter;        // dynamic tile scheduler (zeroed before the launch)
   int static_tiles;         // 1: round-robin tiles instead (A/B switch, MT_BWD_STATIC=1)
+  int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
 };
 
 // ---- tile decoding
@@ -310,9 +312,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dO0 = make_sdesc(smem_u32(sm.dO[0]), 16, 1024);
   const uint64_t dQmn0 = make_sdesc(smem_u32(sm.q[0]), 8192, 1024);
   const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
-  const uint64_t dPT0 = make_sdesc(smem_u32(sm.pT[0]), 16, 1024);
-  const uint64_t dDST0 = make_sdesc(smem_u32(sm.dsT[0]), 16, 1024);
-  const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.dsT[0]), 8192, 1024);
+  const uint64_t dPT0 = make_sdesc(smem_u32(sm.pd[0]), 16, 1024);
+  const uint64_t dDST0 = make_sdesc(smem_u32(sm.pd[0] + kTileP), 16, 1024);
+  const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.pd[0] + kTileP), 8192, 1024);
   uint32_t c = 0, ntile = 0;
   uint32_t s_issued = 0, s_waited = 0;          // S^T/dP^T fills vs releases waited
   uint32_t ds0 = 0, ds1 = 0, gq0 = 0, gq1 = 0;  // per buffer: dsfull waits, grads issued
@@ -358,9 +360,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       tc_fence_after();
       const uint64_t dqm = sdesc_add(dQmn0, prev_stage * kTileQ);
       const uint64_t dom = sdesc_add(dOmn0, prev_stage * kTileQ);
-      const uint64_t dpt = sdesc_add(dPT0, prev_b * kTileP);
-      const uint64_t dst = sdesc_add(dDST0, prev_b * kTileP);
-      const uint64_t dstm = sdesc_add(dDSTmn0, prev_b * kTileP);
+      const uint64_t dpt = sdesc_add(dPT0, prev_b * 2 * kTileP);
+      const uint64_t dst = sdesc_add(dDST0, prev_b * 2 * kTileP);
+      const uint64_t dstm = sdesc_add(dDSTmn0, prev_b * 2 * kTileP);
       if (leader) {
 #pragma unroll
         for (int kq = 0; kq < 64; kq += 16) {
@@ -436,7 +438,8 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
+__device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
+                            const CUtensorMap* tmdq) {
   const int w = warp_id();
   const int quad = w & 3, wg = (w - 4) >> 2;
   const int lane = lane_id();
@@ -449,7 +452,9 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
   const uint32_t sfull = smem_u32(&sm.sfull[wg]), sfree = smem_u32(&sm.sfree);
   const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
   const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
-  const uint32_t prow = smem_u32(sm.pT[wg]) + row * 128, drow = smem_u32(sm.dsT[wg]) + row * 128;
+  const uint32_t pdbuf = smem_u32(sm.pd[wg]);
+  const uint32_t prow = pdbuf + row * 128, drow = pdbuf + kTileP + row * 128;
+  const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
   uint32_t su = 0, gw = 0;  // sfull events, gdone waits
   uint32_t ntile = 0;
 
@@ -464,11 +469,31 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem) {
     tmem_ld_wait();
     tc_fence_before();
     mbar_arrive(dqfree);
-    float* base = P.dq + (size_t)j * 64 * qstride + (size_t)h * 128 + row;
+    if (P.dbg & 1) return;
+    // stage dQ[q][d] (fp32, [64][128]) in this warpgroup's P/dS buffer, then one
+    // bulk tensor reduce-add into the fp32 dQ accumulator
 #pragma unroll
-    for (int c = 0; c < 32; ++c) red_add_f32(base + c * qstride, __uint_as_float(r0[c]));
+    for (int c = 0; c < 32; ++c)
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)(c * 128 + row) * 4),
+                   "f"(__uint_as_float(r0[c]))
+                   : "memory");
 #pragma unroll
-    for (int c = 0; c < 32; ++c) red_add_f32(base + (c + 32) * qstride, __uint_as_float(r1[c]));
+    for (int c = 0; c < 32; ++c)
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)((c + 32) * 128 + row) * 4),
+                   "f"(__uint_as_float(r1[c]))
+                   : "memory");
+    fence_proxy_async_smem();
+    named_bar_sync(wg_bar, 128);
+    if (row == 0) {
+      asm volatile(
+          "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+          " [%0, {%1, %2, %3}], [%4];" ::"l"(tmdq),
+          "r"(0), "r"(h), "r"(j * 64), "r"(pdbuf)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    named_bar_sync(wg_bar, 128);  // the staging buffer may be overwritten
   };
 
   for (;;) {
@@ -604,7 +629,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmdo,
                     const __grid_constant__ CUtensorMap tmk,
-                    const __grid_constant__ CUtensorMap tmv) {
+                    const __grid_constant__ CUtensorMap tmv,
+                    const __grid_constant__ CUtensorMap tmdq) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -648,7 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
-    softmax_bwd(sm, P, tmem);
+    softmax_bwd(sm, P, tmem, &tmdq);
+    if (threadIdx.x % 128 == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -741,9 +768,12 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.tile_counter = plan.scratch + 2;
   static const int static_tiles = getenv("MT_BWD_STATIC") ? atoi(getenv("MT_BWD_STATIC")) : 0;
   P.static_tiles = static_tiles;
+  static const int dbg = getenv("MT_BWD_DBG") ? atoi(getenv("MT_BWD_DBG")) : 0;
+  P.dbg = dbg;
   const uint64_t S_loc = (uint64_t)nloc * 64;
-  CUtensorMap tmq, tmdo, tmk, tmv;
-  if (make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
+  CUtensorMap tmq, tmdo, tmk, tmv, tmdq;
+  if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 64) ||
+      make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmdo, dO, 128, plan.Hq, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmk, k, 128, plan.Hkv, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmv, v, 128, plan.Hkv, S_loc, 64, 1, 64))
@@ -761,14 +791,14 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.mode = kModeBlock;
   P.n_tiles = plan.Hkv * ((nloc + 1) / 2);
   int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
-  if (grid > 0) attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv);
+  if (grid > 0) attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq);
   MT_TRY(check_launch("attn_bwd_kernel(block)"));
   // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
   P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;
   P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128);
   grid = num_sms;
-  attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv);
+  attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq);
   return check_launch("attn_bwd_kernel(bar)");
 }
 

@@ -33,6 +33,20 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t 
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
 }
 
+int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1, uint64_t n2,
+                     uint32_t b0, uint32_t b1, uint32_t b2) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[3] = {n0, n1, n2};
+  cuuint64_t strides[2] = {n0 * 4, n0 * n1 * 4};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
+}
+
 int make_tmap_bf16_2d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1,
                       uint64_t pitch_bytes, uint32_t b0, uint32_t b1) {
   auto enc = get_encode();
