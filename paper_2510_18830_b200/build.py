@@ -40,6 +40,7 @@ def _flags() -> list[str]:
     nccl = _nccl_dirs()
     if nccl:
         f += ["-I", str(nccl[0]), "-DMT_HAVE_NCCL=1"]
+    f += os.environ.get("MT_NVCC_EXTRA", "").split()  # e.g. a shorter spin timeout for debugging
     return f
 
 

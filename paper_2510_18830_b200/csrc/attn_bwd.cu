@@ -7,10 +7,11 @@
 // Key-major ("column-parallel") tiles: the 128 key rows of a tile stay in smem
 // and their dK/dV accumulate in TMEM over every (q head, query block) chunk
 // that attends them; dQ of each chunk is reduce-added to an fp32 accumulator.
-//   mode BLOCK: tile = kv head g x local key blocks (lb0, lb0+1) of the held
-//               chunk; chunks = (q head h of the group, local query block j)
-//               with g_q - kb = o for a selected slash o (o = t mod W).  dK/dV
-//               rows are owned by the tile -> plain read-add-write.
+//   mode BLOCK: tile = q head h x local key blocks (lb0, lb0+1) of the held
+//               chunk; chunks = local query blocks j of head h with
+//               g_q - kb = o for a selected slash o (o = t mod W).  The 8 q heads
+//               of a kv group add into the same dK/dV rows -> bulk tensor
+//               reduce-add.  Tiles run in synchronised waves (below).
 //   mode BAR  : tile = q head h x 128 consecutive entries of the origin's
 //               vertical list; chunks = every later local query block; a
 //               (column, block) pair is live iff the column is not covered by a
@@ -21,8 +22,18 @@
 //   P^T, dS^T (bf16, dS pre-scaled by 1/sqrt d) in registers -> smem
 //   dV += P^T dO, dK += dS^T Q              (TMEM accumulators, N = 128)
 //   dQ^T = K^T dS^T                          (TMEM, M = d) -> red.add to dQ
-// Warp roles: warp 0 producer (TMA / cp.async), warp 1 MMA issuer,
-// warps 2..5 softmax-backward + dQ drain + dK/dV epilogue.
+// Warp roles: warp 0 producer (TMA / cp.async), warp 1 MMA issuer, warps 4..11
+// two softmax-backward warpgroups (alternate chunks) + dQ drain + epilogue.
+//
+// L2 locality (BLOCK): the streamed operands (Q, dO: 32 KB, dQ reduce: 32 KB per
+// chunk) dominate DRAM traffic.  A query block (h, g_q) is needed by the tiles
+// kb = g_q - o, o in i_s[h].  Tiles are numbered head-major with key pairs
+// ascending and handed out by an atomic counter, so the ~148 resident tiles are
+// consecutive key pairs of one head walking the same offset list at the same
+// pace: each query block they touch is reused by ~(2 x 148 x |i_s| / nb) tiles
+// while L2-resident (measured: DRAM traffic 1.84 TB -> 0.20 TB per 512K launch,
+// L2 hit 19% -> 70%).  MT_BWD_WAVE=1 additionally starts each wave of 148 tiles
+// together behind a soft grid barrier (bounded spin); measured slower.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -94,6 +105,10 @@ struct Params {
   float* dv;
   int* tile_counter;        // dynamic tile scheduler (zeroed before the launch)
   int static_tiles;         // 1: round-robin tiles instead (A/B switch, MT_BWD_STATIC=1)
+  int wave;                 // BLOCK: 1 = synchronised waves (MT_BWD_WAVE=1; default dynamic)
+  int wave_pairs;           // key-block pairs per wave (<= gridDim.x)
+  int waves_per_head;
+  int* wave_counter;        // soft grid barrier (zeroed before the launch)
   int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
 };
 
@@ -112,10 +127,11 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
   const int W = pl.W;
   if (P.mode == kModeBlock) {
     const int npairs = (P.nloc + 1) / 2;
-    if (tile >= pl.Hkv * npairs) return T;
+    if (tile < 0 || tile >= pl.Hq * npairs) return T;
     T.ok = true;
-    T.g = tile % pl.Hkv;
-    T.lb0 = 2 * (tile / pl.Hkv);  // early key blocks (most work) first
+    T.h = tile / npairs;
+    T.g = T.h / (pl.Hq / pl.Hkv);
+    T.lb0 = 2 * (tile % npairs);  // early key blocks (most work) first
     return T;
   }
   int base = 0;
@@ -142,12 +158,12 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
   const int lane = lane_id();
   const VSPlan& pl = P.plan;
   const int W = pl.W;
-  const int grp = pl.Hq / pl.Hkv;
   const int64_t S_loc = (int64_t)P.nloc * 64;
   uint32_t c = 0;  // chunk events (incl. END)
   uint32_t ntile = 0;
   auto emit = [&](int h, int j, uint32_t flags) {
     const uint32_t stage = c % kStages;
+    MT_CRUMB(2, 1000000 + (int)c);
     mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
     if (lane == 0) {
       ChunkMeta& m = sm.meta[stage];
@@ -177,9 +193,31 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     ++c;
   };
 
+  const bool waves = P.mode == kModeBlock && P.wave;
+  const int npairs = (P.nloc + 1) / 2;
   for (int it = 0;; ++it) {
     int tile = 0;
-    if (P.static_tiles) {
+    if (waves) {
+      if (it >= pl.Hq * P.waves_per_head) break;
+      if (it > 0) {  // soft barrier: wave it starts when every CTA has emitted wave it-1
+        if (lane == 0) {
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.wave_counter) : "memory");
+          const int target = (int)gridDim.x * it;
+          const long long t0 = clock64();
+          for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.wave_counter) : "memory");
+            if (v >= target || clock64() - t0 > (1ll << 16)) break;
+            __nanosleep(128);
+          }
+        }
+        __syncwarp();
+      }
+      const int h = it / P.waves_per_head, w = it % P.waves_per_head;
+      const int pair = w * P.wave_pairs + (int)blockIdx.x;
+      if ((int)blockIdx.x >= P.wave_pairs || pair >= npairs) continue;  // idle in this wave
+      tile = h * npairs + pair;
+    } else if (P.static_tiles) {
       tile = blockIdx.x + it * gridDim.x;
     } else {
       if (lane == 0) tile = atomicAdd(P.tile_counter, 1);
@@ -190,7 +228,9 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     // ---- K/V tile: wait until every MMA of the previous tile finished and its
     // epilogue (which reads cols[]) is done
     if (ntile > 0) {
+      MT_CRUMB(2, 2000000 + (int)ntile);
       mbar_wait(smem_u32(&sm.kvempty), (ntile - 1) & 1);
+      MT_CRUMB(2, 3000000 + (int)ntile);
       mbar_wait(smem_u32(&sm.tfree), (ntile - 1) & 1);
     }
     ++ntile;
@@ -238,8 +278,8 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       const bool v1 = T.lb0 + 1 < P.nloc;
       const int kb0 = T.lb0 * W + P.s;
       const int kb1 = v1 ? kb0 + W : -1;
-      for (int hh = 0; hh < grp; ++hh) {
-        const int h = T.g * grp + hh;
+      {
+        const int h = T.h;
         const int ns = pl.s_cnt[h];
         const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
         // query blocks gq = kb + o for o = t (mod W), merged over the two key slots
@@ -285,7 +325,10 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       ++c;
     }
   }
-  // ---- DONE
+  // ---- DONE, only once the last tile's epilogue is over: both softmax warpgroups
+  // have then consumed that tile's END, so sfull never runs two phases ahead of a
+  // warpgroup still draining its last chunk (parity aliasing)
+  if (ntile > 0) mbar_wait(smem_u32(&sm.tfree), (ntile - 1) & 1);
   const uint32_t stage = c % kStages;
   mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
   if (lane == 0) {
@@ -319,6 +362,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   uint32_t s_issued = 0, s_waited = 0;          // S^T/dP^T fills vs releases waited
   uint32_t ds0 = 0, ds1 = 0, gq0 = 0, gq1 = 0;  // per buffer: dsfull waits, grads issued
   auto wait_s_released = [&]() {
+    MT_CRUMB(0, 3);
+    MT_CRUMB(5, (int)s_issued);
+    MT_CRUMB(6, (int)s_waited);
     while (s_waited < s_issued) {
       mbar_wait(smem_u32(&sm.sfree), s_waited & 1);
       ++s_waited;
@@ -339,6 +385,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         break;
       }
     }
+    MT_CRUMB(0, 2);
     mbar_wait(smem_u32(&sm.kvfull), ntile & 1);
     ++ntile;
     if (P.mode == kModeBar) fence_proxy_async_smem();
@@ -346,6 +393,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     bool have_prev = false, acc_started = false;
     uint32_t prev_stage = 0, prev_b = 0, k = 0;
     auto grads = [&]() {  // gradient MMAs of the previous chunk (buffer prev_b)
+      MT_CRUMB(0, 4 + 10 * (int)prev_b);
       if (prev_b == 0) {
         mbar_wait(smem_u32(&sm.dsfull[0]), ds0 & 1);
         ++ds0;
@@ -357,6 +405,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         if (gq1 > 0) mbar_wait(smem_u32(&sm.dqfree[1]), (gq1 - 1) & 1);
         ++gq1;
       }
+      MT_CRUMB(0, 6);
       tc_fence_after();
       const uint64_t dqm = sdesc_add(dQmn0, prev_stage * kTileQ);
       const uint64_t dom = sdesc_add(dOmn0, prev_stage * kTileQ);
@@ -381,6 +430,8 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     };
     for (;;) {
       const uint32_t stage = c % kStages;
+      MT_CRUMB(0, 1);
+      MT_CRUMB(1, (int)c);
       mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
       const int kind = sm.meta[stage].kind;
       const int end_tile = sm.meta[stage].tile;  // read before the stage is released
@@ -438,8 +489,8 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
-                            const CUtensorMap* tmdq) {
+__device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUtensorMap* tmdq,
+                            const CUtensorMap* tmdk, const CUtensorMap* tmdv) {
   const int w = warp_id();
   const int quad = w & 3, wg = (w - 4) >> 2;
   const int lane = lane_id();
@@ -448,7 +499,6 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
   const uint32_t lb = (uint32_t)(quad * 32) << 16;
   const VSPlan& pl = P.plan;
   const int Hq = pl.Hq, W = pl.W;
-  const size_t qstride = (size_t)Hq * 128;
   const uint32_t sfull = smem_u32(&sm.sfull[wg]), sfree = smem_u32(&sm.sfree);
   const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
   const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
@@ -457,10 +507,22 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
   uint32_t su = 0, gw = 0;  // sfull events, gdone waits
   uint32_t ntile = 0;
+  bool staging_busy = false;  // a bulk reduce may still be reading this warpgroup's buffer
 
-  // dQ^T of this warpgroup's previous chunk (h, j) -> dQ[q][h][d = row]
+  auto wait_staging = [&]() {  // warpgroup-uniform
+    if (!staging_busy) return;
+    if (row == 0) MT_CRUMB(3 + wg, 3000000);
+    if (row == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    named_bar_sync(wg_bar, 128);
+    staging_busy = false;
+  };
+  // dQ^T of this warpgroup's chunk (h, j) -> dQ[q][h][d = row].  Runs right after the
+  // chunk's P/dS^T is published, so it overlaps the next S^T instead of delaying the
+  // gradient MMAs; the reduce's smem read is only waited for before the buffer is
+  // rewritten (next P/dS^T or the epilogue).
   auto drain_dq = [&](int h, int j) {
-    mbar_wait(gdone, gw & 1);
+    if (row == 0) MT_CRUMB(3 + wg, 2000000 + (int)gw);
+    mbar_wait(gdone, gw & 1);  // gradient MMAs done: P/dS^T free, dQ^T complete
     ++gw;
     tc_fence_after();
     uint32_t r0[32], r1[32];
@@ -483,6 +545,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
                    "f"(__uint_as_float(r1[c]))
                    : "memory");
     fence_proxy_async_smem();
+    if (row == 0) MT_CRUMB(3 + wg, 4000000);
     named_bar_sync(wg_bar, 128);
     if (row == 0) {
       asm volatile(
@@ -491,16 +554,16 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
           "r"(0), "r"(h), "r"(j * 64), "r"(pdbuf)
           : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
-    named_bar_sync(wg_bar, 128);  // the staging buffer may be overwritten
+    staging_busy = true;
   };
 
   for (;;) {
     int my_col = -2;  // BAR: this row's column, read at the first chunk
-    int prev_h = -1, prev_j = -1;
+    bool had_chunk = false;
     int tile = -1;
     for (;;) {
+      if (row == 0) MT_CRUMB(3 + wg, 1000000 + (int)su);
       mbar_wait(sfull, su & 1);
       ++su;
       const ChunkMeta cm = sm.smeta[wg];
@@ -556,9 +619,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
         dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
         dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
       }
-      // this warpgroup's previous chunk: its gradient MMAs are done (P^T/dS^T free),
-      // and its dQ^T is drained into the dQ accumulator
-      if (prev_h >= 0) drain_dq(prev_h, prev_j);
+      wait_staging();  // the previous chunk's dQ reduce has read the buffer
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) {
         const uint32_t sw = (uint32_t)((c16 ^ (row & 7)) << 4);
@@ -572,14 +633,15 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(dsfull);
-      prev_h = cm.h;
-      prev_j = cm.j;
+      drain_dq(cm.h, cm.j);
+      had_chunk = true;
     }
     if (tile < 0) break;  // DONE
     const Tile T = decode_tile(P, tile);
-    if (prev_h >= 0) drain_dq(prev_h, prev_j);  // also: this warpgroup's MMAs are complete
+    wait_staging();  // the epilogue stages dK/dV in the same buffer
     tc_fence_after();
-    if (row == 0) sm.tile_chunks[wg] = prev_h >= 0 ? 1 : 0;
+    if (row == 0) sm.tile_chunks[wg] = had_chunk ? 1 : 0;
+    if (row == 0) MT_CRUMB(3 + wg, 5000000 + (int)ntile);
     named_bar_sync(3, 256);  // both warpgroups: every MMA of the tile complete
     const bool any_chunk = (sm.tile_chunks[0] | sm.tile_chunks[1]) != 0;  // else TMEM is stale
 
@@ -594,31 +656,56 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem,
       live_row = any_chunk && m >= 0;
       lrow = live_row ? (int64_t)(((m >> 6) - P.s) / W) * 64 + (m & 63) : 0;
     }
-    float* dst = (wg == 0 ? P.dk : P.dv) + ((size_t)lrow * pl.Hkv + T.g) * 128;
     const uint32_t col = wg == 0 ? kColDK : kColDV;
+    if (P.mode == kModeBlock) {
+      // rows lb0*64 .. +127 are contiguous: stage [128 rows][32 d] fp32 (SW128) in this
+      // warpgroup's P/dS buffer, two column groups per round, and bulk reduce-add them
+      // (rows past the chunk end are clipped by the tensor map; they hold zeros anyway)
+      const CUtensorMap* tm = wg == 0 ? tmdk : tmdv;
 #pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      uint32_t a[32];
-      tmem_ld32(tmem + lb + col + c0, a);
-      tmem_ld_wait();
-      if (!live_row) continue;
-      if (P.mode == kModeBlock) {
-        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+      for (int rd = 0; rd < 2; ++rd) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float4 x = d4[c];
-          x.x += __uint_as_float(a[4 * c]);
-          x.y += __uint_as_float(a[4 * c + 1]);
-          x.z += __uint_as_float(a[4 * c + 2]);
-          x.w += __uint_as_float(a[4 * c + 3]);
-          d4[c] = x;
+        for (int g2 = 0; g2 < 2; ++g2) {
+          uint32_t a[32];
+          tmem_ld32(tmem + lb + col + (rd * 2 + g2) * 32, a);
+          tmem_ld_wait();
+          const uint32_t base = pdbuf + g2 * 16384 + row * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             base + ((uint32_t)(c ^ (row & 7)) << 4)),
+                         "r"(a[4 * c]), "r"(a[4 * c + 1]), "r"(a[4 * c + 2]), "r"(a[4 * c + 3])
+                         : "memory");
         }
-      } else {
+        fence_proxy_async_smem();
+        named_bar_sync(wg_bar, 128);
+        if (row == 0 && any_chunk) {
+#pragma unroll
+          for (int g2 = 0; g2 < 2; ++g2)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+                " [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+                "r"((rd * 2 + g2) * 32), "r"(T.g), "r"(T.lb0 * 64), "r"(pdbuf + g2 * 16384)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        named_bar_sync(wg_bar, 128);
+      }
+    } else {
+      float* dst = (wg == 0 ? P.dk : P.dv) + ((size_t)lrow * pl.Hkv + T.g) * 128;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t a[32];
+        tmem_ld32(tmem + lb + col + c0, a);
+        tmem_ld_wait();
+        if (!live_row) continue;
 #pragma unroll
         for (int c = 0; c < 32; ++c) red_add_f32(dst + c0 + c, __uint_as_float(a[c]));
       }
     }
     tc_fence_before();
+    if (row == 0) MT_CRUMB(3 + wg, 7000000 + (int)ntile);
     named_bar_sync(3, 256);  // TMEM dK/dV and cols[] free for the next tile
     if (threadIdx.x == 128) mbar_arrive(smem_u32(&sm.tfree));
     ++ntile;
@@ -630,7 +717,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tmdo,
                     const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv,
-                    const __grid_constant__ CUtensorMap tmdq) {
+                    const __grid_constant__ CUtensorMap tmdq,
+                    const __grid_constant__ CUtensorMap tmdk,
+                    const __grid_constant__ CUtensorMap tmdv) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -674,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
-    softmax_bwd(sm, P, tmem, &tmdq);
+    softmax_bwd(sm, P, tmem, &tmdq, &tmdk, &tmdv);
     if (threadIdx.x % 128 == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
@@ -770,9 +859,13 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.static_tiles = static_tiles;
   static const int dbg = getenv("MT_BWD_DBG") ? atoi(getenv("MT_BWD_DBG")) : 0;
   P.dbg = dbg;
+  static const int wave = getenv("MT_BWD_WAVE") ? atoi(getenv("MT_BWD_WAVE")) : 0;
+  P.wave = wave;
   const uint64_t S_loc = (uint64_t)nloc * 64;
-  CUtensorMap tmq, tmdo, tmk, tmv, tmdq;
+  CUtensorMap tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv;
   if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 64) ||
+      make_tmap_f32_3d(&tmdk, dk, 128, plan.Hkv, S_loc, 32, 1, 128, true) ||
+      make_tmap_f32_3d(&tmdv, dv, 128, plan.Hkv, S_loc, 32, 1, 128, true) ||
       make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmdo, dO, 128, plan.Hq, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmk, k, 128, plan.Hkv, S_loc, 64, 1, 64) ||
@@ -787,18 +880,23 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
     attr_done = true;
   }
   // block (slash) part
-  cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);  // one counter per launch
+  cudaMemsetAsync(P.tile_counter, 0, 3 * sizeof(int), st);  // 2 tile counters + wave barrier
   P.mode = kModeBlock;
-  P.n_tiles = plan.Hkv * ((nloc + 1) / 2);
-  int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
-  if (grid > 0) attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq);
+  const int npairs = (nloc + 1) / 2;
+  P.n_tiles = plan.Hq * npairs;
+  P.wave_counter = plan.scratch + 4;
+  P.waves_per_head = (npairs + num_sms - 1) / num_sms;
+  P.wave_pairs = P.waves_per_head > 0 ? (npairs + P.waves_per_head - 1) / P.waves_per_head : 0;
+  int grid = P.wave ? P.wave_pairs : (P.n_tiles < num_sms ? P.n_tiles : num_sms);
+  if (grid > 0)
+    attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
   MT_TRY(check_launch("attn_bwd_kernel(block)"));
   // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
   P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;
   P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128);
   grid = num_sms;
-  attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq);
+  attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
   return check_launch("attn_bwd_kernel(bar)");
 }
 

@@ -26,7 +26,8 @@ struct VSPlan {
   const uint32_t* s_bits;
   const int32_t* vptr;  // [Hq][W + 1]
   const int32_t* vcol;  // [Hq][S] (global column ids, grouped by origin)
-  int32_t* scratch;     // [16 + Hq * nb] ints: kernel scratch (fix-up tile list)
+  int32_t* scratch;     // [16 + Hq * nb] ints: [0] fwd fix-up count, [1] fwd tile counter,
+                        // [2], [3] bwd tile counters, [4] bwd wave barrier, [16..] fix-up list
 };
 
 __device__ __forceinline__ bool plan_has_slash(const VSPlan& p, int h, int o) {

@@ -67,7 +67,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 }
 // Debug breadcrumbs (per block, 4 words): roles may record progress here; the
 // timeout message prints them.
-__device__ volatile int g_mt_dbg[1024][4];
+__device__ volatile int g_mt_dbg[1024][8];
+#ifdef MT_BREADCRUMBS
+#define MT_CRUMB(i, v) (g_mt_dbg[blockIdx.x & 1023][(i)] = (v))
+#else
+#define MT_CRUMB(i, v) ((void)0)
+#endif
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
@@ -75,9 +80,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
     if (clock64() - t0 > MT_SPIN_TIMEOUT_CYCLES) {
       const int b = blockIdx.x & 1023;
-      printf("mt: mbarrier timeout smem=0x%x parity=%u block=%d thread=%d dbg=%d,%d,%d,%d\n",
+      printf("mt: mbarrier timeout smem=0x%x parity=%u block=%d thread=%d dbg=%d,%d,%d,%d,%d,%d,%d,%d\n",
              bar, parity, (int)blockIdx.x, (int)threadIdx.x, g_mt_dbg[b][0], g_mt_dbg[b][1],
-             g_mt_dbg[b][2], g_mt_dbg[b][3]);
+             g_mt_dbg[b][2], g_mt_dbg[b][3], g_mt_dbg[b][4], g_mt_dbg[b][5], g_mt_dbg[b][6],
+             g_mt_dbg[b][7]);
       __trap();
     }
   }

@@ -34,7 +34,7 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t 
 }
 
 int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1, uint64_t n2,
-                     uint32_t b0, uint32_t b1, uint32_t b2) {
+                     uint32_t b0, uint32_t b1, uint32_t b2, bool swizzle128) {
   auto enc = get_encode();
   if (!enc) return -1;
   cuuint64_t dims[3] = {n0, n1, n2};
@@ -42,7 +42,8 @@ int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n
   cuuint32_t box[3] = {b0, b1, b2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
 }
