@@ -239,12 +239,34 @@ mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* shape, const void* q_l
  * node (inner == world: flat).  out must hold world * world ints. */
 mt_status mt_ring_schedule(int world, int inner, int32_t* out);
 
+/* ------------------------------------------------------------------ layout */
+/* Block-striped context-parallel layout (SURVEY §8 a1,
+ * reading Q12): global 64-token block b lives on rank b mod W as local block
+ * floor(b / W), i.e. local row j of rank r <-> global token
+ * (floor(j / 64) * W + r) * 64 + j mod 64.  Tensors are token-major with
+ * `row_bytes` bytes per token (e.g. Hq * 128 * 2 for bf16 Q); both pointers are
+ * device pointers owned by the caller; row_bytes must be a multiple of 16.
+ *   mt_stripe:   local[S/W rows]  <- global[S rows]   (rank r's share)
+ *   mt_unstripe: global[S rows]   <- local[S/W rows]  (writes only rank r's rows)
+ * Errors: MT_ESHAPE (NULL, row_bytes % 16, bad rank/world), MT_EWINDOW,
+ * MT_ELAYOUT (S % (64 W)), MT_ECUDA. */
+mt_status mt_stripe(int64_t seq_len, int64_t row_bytes, int world, int rank,
+                    const void* global, void* local, mt_stream_t stream);
+mt_status mt_unstripe(int64_t seq_len, int64_t row_bytes, int world, int rank,
+                      const void* local, void* global, mt_stream_t stream);
+
 /* ------------------------------------------------------------------ tests */
 /* Hardware self-test hook (not part of the attention API): one 128-row tcgen05
  * MMA configuration on one CTA, see csrc/selftest.cu for the variants.
  * A, B: bf16 device buffers, D: float32 device buffer [128][N]. */
 mt_status mt_selftest_mma(int variant, const void* A, const void* B, float* D,
                           mt_stream_t stream);
+
+/* Profiling hook (not part of the attention API): copies the backward kernel's
+ * timeline probe — int64 clock64 stamps [8 events][4096 chunk events] of CTA 0 of
+ * the most recent launch — to host memory `out` (8 * 4096 int64).  All zeros
+ * unless the library was built with -DMT_TIMELINE (MT_NVCC_EXTRA). */
+mt_status mt_debug_bwd_timeline(int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,7 @@ SZ = ctypes.c_size_t
 
 _SIGS: dict[str, list] = {
     "mt_selftest_mma": [I, P, P, P, P],
+    "mt_debug_bwd_timeline": [P],
     "mt_sparse_attn_fwd_workspace_bytes": [P, I],
     "mt_sparse_attn_fwd": [P, P, P, P, P, P, P, P, SZ, P],
     "mt_attn_fwd_step": [P, I, I, I, I, I, P, P, P, P, P, P, P, P, SZ, P],
@@ -83,6 +84,8 @@ _SIGS: dict[str, list] = {
     "mt_ring_attn_fwd": [P, P, P, P, P, P, P, P, P, SZ, P],
     "mt_ring_attn_bwd": [P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "mt_ring_schedule": [I, I, P],
+    "mt_stripe": [I64, I64, I, I, P, P, P],
+    "mt_unstripe": [I64, I64, I, I, P, P, P],
 }
 _RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
             "mt_build_vs_index_workspace_bytes": ctypes.c_size_t,

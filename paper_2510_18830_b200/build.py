@@ -62,6 +62,12 @@ def _compile(src: Path, verbose: bool) -> Path:
 
 def build(verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
+    stamp = BUILD / "flags.txt"  # objects built with other flags are stale
+    flags = " ".join(_flags())
+    if not stamp.exists() or stamp.read_text() != flags:
+        for o in BUILD.glob("*.o"):
+            o.unlink()
+        stamp.write_text(flags)
     srcs = sorted(CSRC.glob("*.cu"))
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))

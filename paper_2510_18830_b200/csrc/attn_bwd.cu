@@ -38,6 +38,7 @@
 
 #include "common.cuh"
 #include "plan.cuh"
+#define MT_TL_ON (P.mode == 0)  // timeline probe: the block (slash) launch only
 #include "sm100.cuh"
 #include "tmap.cuh"
 
@@ -65,7 +66,8 @@ struct alignas(16) ChunkMeta {
   uint32_t flags;  // BLOCK: bit0/1 slot0/1 live, bit2/3 slot0/1 diagonal
   int stage;       // smem stage holding the chunk's Q / dO / LSE / D
   int tile;        // kEnd: the tile it closes
-  int pad[2];
+  int seq;         // producer event index (timeline probe)
+  int pad;
 };
 
 struct Smem {
@@ -165,8 +167,10 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     const uint32_t stage = c % kStages;
     MT_CRUMB(2, 1000000 + (int)c);
     mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
+    if (lane == 0) MT_TL(0, c);
     if (lane == 0) {
       ChunkMeta& m = sm.meta[stage];
+      m.seq = (int)c;
       m.kind = kChunk;
       m.h = h;
       m.j = j;
@@ -390,28 +394,40 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     ++ntile;
     if (P.mode == kModeBar) fence_proxy_async_smem();
     tc_fence_after();
-    bool have_prev = false, acc_started = false;
-    uint32_t prev_stage = 0, prev_b = 0, k = 0;
-    auto grads = [&]() {  // gradient MMAs of the previous chunk (buffer prev_b)
-      MT_CRUMB(0, 4 + 10 * (int)prev_b);
-      if (prev_b == 0) {
-        mbar_wait(smem_u32(&sm.dsfull[0]), ds0 & 1);
-        ++ds0;
-        if (gq0 > 0) mbar_wait(smem_u32(&sm.dqfree[0]), (gq0 - 1) & 1);
-        ++gq0;
-      } else {
-        mbar_wait(smem_u32(&sm.dsfull[1]), ds1 & 1);
-        ++ds1;
-        if (gq1 > 0) mbar_wait(smem_u32(&sm.dqfree[1]), (gq1 - 1) & 1);
-        ++gq1;
+    // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and the
+    // S/dP TMEM pair is free; the gradient MMAs of chunk g as soon as its P/dS^T is
+    // published.  (A fixed S(k), G(k-1), S(k+1) order makes G(k) wait for chunk
+    // k+1's load, which holds chunk k's stage ~2x longer: measured.)
+    bool acc_started = false, end_seen = false;
+    uint32_t k = 0, g = 0;  // tile-local: chunks whose S^T issued / gradients issued
+    uint32_t pstage[2] = {0, 0}, end_stage = 0;
+    int pseq[2] = {0, 0}, end_tile = 0;
+    auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
+    auto s_released_now = [&]() {
+      while (s_waited < s_issued) {
+        if (!uni(mbar_test_wait(smem_u32(&sm.sfree), s_waited & 1))) return false;
+        ++s_waited;
       }
-      MT_CRUMB(0, 6);
+      return true;
+    };
+    auto try_grads = [&]() {  // gradient MMAs of chunk g (softmax warpgroup g & 1)
+      const uint32_t bg = g & 1;
+      uint32_t& ds = bg ? ds1 : ds0;
+      uint32_t& gq = bg ? gq1 : gq0;
+      if (!uni(mbar_test_wait(smem_u32(&sm.dsfull[bg]), ds & 1))) return false;
+      if (gq > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[bg]), (gq - 1) & 1))) return false;
+      ++ds;
+      ++gq;
+#ifdef MT_TL_ISSUER
+      if (leader) MT_TL(6, pseq[bg]);
+#endif
       tc_fence_after();
-      const uint64_t dqm = sdesc_add(dQmn0, prev_stage * kTileQ);
-      const uint64_t dom = sdesc_add(dOmn0, prev_stage * kTileQ);
-      const uint64_t dpt = sdesc_add(dPT0, prev_b * 2 * kTileP);
-      const uint64_t dst = sdesc_add(dDST0, prev_b * 2 * kTileP);
-      const uint64_t dstm = sdesc_add(dDSTmn0, prev_b * 2 * kTileP);
+      const uint32_t st = pstage[bg];
+      const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
+      const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
+      const uint64_t dpt = sdesc_add(dPT0, bg * 2 * kTileP);
+      const uint64_t dst = sdesc_add(dDST0, bg * 2 * kTileP);
+      const uint64_t dstm = sdesc_add(dDSTmn0, bg * 2 * kTileP);
       if (leader) {
 #pragma unroll
         for (int kq = 0; kq < 64; kq += 16) {
@@ -421,40 +437,32 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         }
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16)
-          mma_ss(tmem + kColDQ + 64 * prev_b, sdesc_add(dKmn, kk * 128),
-                 sdesc_add(dstm, kk * 128), id_q, kk > 0);
-        mma_commit(smem_u32(&sm.gdone[prev_b]));
-        mma_commit(smem_u32(&sm.empty[prev_stage]));
+          mma_ss(tmem + kColDQ + 64 * bg, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128),
+                 id_q, kk > 0);
+        mma_commit(smem_u32(&sm.gdone[bg]));
+        mma_commit(smem_u32(&sm.empty[st]));
+        MT_TL(3, pseq[bg]);
       }
       acc_started = true;
+      ++g;
+      return true;
     };
-    for (;;) {
+    auto try_s = [&]() {  // S^T/dP^T of the next chunk, or note the tile's END
       const uint32_t stage = c % kStages;
-      MT_CRUMB(0, 1);
-      MT_CRUMB(1, (int)c);
-      mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
-      const int kind = sm.meta[stage].kind;
-      const int end_tile = sm.meta[stage].tile;  // read before the stage is released
-      tc_fence_after();
-      ++c;
-      if (kind == kEnd) {
-        if (have_prev) grads();
-        if (leader) {
-          mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
-          mbar_arrive(smem_u32(&sm.empty[stage]));
-        }
-        wait_s_released();
-        for (uint32_t b = 0; b < 2; ++b)
-          if (leader) {
-            sm.smeta[b].kind = kEnd;
-            sm.smeta[b].tile = end_tile;
-            mbar_arrive(smem_u32(&sm.sfull[b]));
-            mbar_arrive(smem_u32(&sm.sfull[b]));
-          }
-        break;
+      if (!uni(mbar_test_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1))) return false;
+      if (sm.meta[stage].kind == kEnd) {
+        end_seen = true;
+        end_stage = stage;
+        end_tile = sm.meta[stage].tile;  // read before the stage is released
+        ++c;
+        return true;
       }
+      if (!s_released_now()) return false;
+#ifdef MT_TL_ISSUER
+      if (leader) MT_TL(7, sm.meta[stage].seq);
+#endif
+      tc_fence_after();
       const uint32_t b = k & 1;
-      wait_s_released();
       if (leader) {
         sm.smeta[b] = sm.meta[stage];
         mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
@@ -467,14 +475,33 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
           mma_ss(tmem + kColDP, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
         }
         mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
+        MT_TL(2, sm.meta[stage].seq);
       }
+      pstage[b] = stage;
+      pseq[b] = sm.meta[stage].seq;
       ++s_issued;
-      if (have_prev) grads();
-      have_prev = true;
-      prev_stage = stage;
-      prev_b = b;
       ++k;
+      ++c;
+      return true;
+    };
+    MT_CRUMB(0, 1);
+    for (;;) {
+      if (g < k) try_grads();
+      if (!end_seen && k < g + 2) try_s();
+      if (end_seen && g == k) break;
     }
+    if (leader) {
+      mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
+      mbar_arrive(smem_u32(&sm.empty[end_stage]));
+    }
+    wait_s_released();
+    for (uint32_t b = 0; b < 2; ++b)
+      if (leader) {
+        sm.smeta[b].kind = kEnd;
+        sm.smeta[b].tile = end_tile;
+        mbar_arrive(smem_u32(&sm.sfull[b]));
+        mbar_arrive(smem_u32(&sm.sfull[b]));
+      }
   }
 }
 
@@ -520,10 +547,13 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   // chunk's P/dS^T is published, so it overlaps the next S^T instead of delaying the
   // gradient MMAs; the reduce's smem read is only waited for before the buffer is
   // rewritten (next P/dS^T or the epilogue).
-  auto drain_dq = [&](int h, int j) {
+  auto drain_dq = [&](int h, int j, int seq) {
     if (row == 0) MT_CRUMB(3 + wg, 2000000 + (int)gw);
     mbar_wait(gdone, gw & 1);  // gradient MMAs done: P/dS^T free, dQ^T complete
     ++gw;
+#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER)
+    if (row == 0) MT_TL(6, seq);
+#endif
     tc_fence_after();
     uint32_t r0[32], r1[32];
     tmem_ld32(tmem + lb + kColDQ + 64 * wg, r0);
@@ -532,6 +562,15 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
     tc_fence_before();
     mbar_arrive(dqfree);
     if (P.dbg & 1) return;
+    if (P.dbg & 4) {  // A/B: coalesced per-element reduction (thread = d, 64 queries)
+      float* dst = P.dq + ((size_t)j * 64 * pl.Hq + h) * 128 + row;
+      const size_t qs = (size_t)pl.Hq * 128;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) red_add_f32(dst + c * qs, __uint_as_float(r0[c]));
+#pragma unroll
+      for (int c = 0; c < 32; ++c) red_add_f32(dst + (c + 32) * qs, __uint_as_float(r1[c]));
+      return;
+    }
     // stage dQ[q][d] (fp32, [64][128]) in this warpgroup's P/dS buffer, then one
     // bulk tensor reduce-add into the fp32 dQ accumulator
 #pragma unroll
@@ -554,6 +593,9 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
           "r"(0), "r"(h), "r"(j * 64), "r"(pdbuf)
           : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER)
+      MT_TL(7, seq);
+#endif
     }
     staging_busy = true;
   };
@@ -572,6 +614,9 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         break;
       }
       if (P.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
+#ifndef MT_TL_WARPS
+      if (row == 0) MT_TL(4, cm.seq);
+#endif
       tc_fence_after();
       uint32_t sv[64], dpv[64];
       tmem_ld32(tmem + lb + kColS, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
@@ -633,7 +678,12 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(dsfull);
-      drain_dq(cm.h, cm.j);
+#ifdef MT_TL_WARPS
+      if (lane == 0) MT_TL(4 + quad, cm.seq);  // per-warp publish times (quad 0..3)
+#else
+      if (row == 0) MT_TL(5, cm.seq);
+#endif
+      drain_dq(cm.h, cm.j, cm.seq);
       had_chunk = true;
     }
     if (tile < 0) break;  // DONE
@@ -761,6 +811,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
       mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
     }
+#ifdef MT_TIMELINE
+    else if (warp == 3 && blockIdx.x == 0 && P.mode == kModeBlock) {
+      // observer: stamps each stage's "full" completion (load latency = event 1 - event 0)
+      for (uint32_t c = 0;; ++c) {
+        const uint32_t st = c % kStages;
+        mbar_wait(smem_u32(&sm.full[st]), (c / kStages) & 1);
+        if (lane_id() == 0) MT_TL(1, c);
+        if (sm.meta[st].kind == kDone) break;
+      }
+    }
+#endif
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
     softmax_bwd(sm, P, tmem, &tmdq, &tmdk, &tmdv);
@@ -901,3 +962,10 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
 }
 
 }  // namespace mt
+
+extern "C" mt_status mt_debug_bwd_timeline(int64_t* out) {
+  if (!out) return mt::fail(MT_ESHAPE, "NULL output");
+  if (cudaMemcpyFromSymbol(out, mt::g_mt_tl, sizeof(mt::g_mt_tl)) != cudaSuccess)
+    return mt::fail(MT_ECUDA, "cudaMemcpyFromSymbol(timeline) failed");
+  return MT_OK;
+}

@@ -65,9 +65,37 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking probe of a phase (for warps that poll several barriers).
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Debug breadcrumbs (per block, 4 words): roles may record progress here; the
 // timeout message prints them.
 __device__ volatile int g_mt_dbg[1024][8];
+// Timeline probe (compile with -DMT_TIMELINE): CTA 0 stamps clock64 per (event,
+// chunk) for its first kTlChunks chunk events; read back with mt_debug_timeline().
+constexpr int kTlEvents = 8, kTlChunks = 4096;
+__device__ long long g_mt_tl[kTlEvents][kTlChunks];
+#ifdef MT_TIMELINE
+#ifndef MT_TL_ON
+#define MT_TL_ON true
+#endif
+#define MT_TL(e, c)                                                           \
+  do {                                                                        \
+    if (blockIdx.x == 0 && (MT_TL_ON) && (unsigned)(c) < (unsigned)kTlChunks) \
+      g_mt_tl[(e)][(c)] = clock64();                                          \
+  } while (0)
+#else
+#define MT_TL(e, c) ((void)0)
+#endif
 #ifdef MT_BREADCRUMBS
 #define MT_CRUMB(i, v) (g_mt_dbg[blockIdx.x & 1023][(i)] = (v))
 #else

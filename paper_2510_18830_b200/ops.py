@@ -213,6 +213,24 @@ class Comm:
             self.handle = None
 
 
+def stripe(x_global: torch.Tensor, world: int, rank: int) -> torch.Tensor:
+    """Rank `rank`'s block-striped share of a token-major tensor (mt_stripe)."""
+    S = x_global.shape[0]
+    out = torch.empty((S // world,) + tuple(x_global.shape[1:]), dtype=x_global.dtype,
+                      device=x_global.device)
+    row = x_global[0].numel() * x_global.element_size()
+    _lib.check(_lib.lib().mt_stripe(S, row, world, rank, _ptr(x_global), _ptr(out), _stream()))
+    return out
+
+
+def unstripe(x_local: torch.Tensor, world: int, rank: int, out: torch.Tensor) -> torch.Tensor:
+    """Scatter rank `rank`'s local rows back into the global tensor `out` (mt_unstripe)."""
+    S = out.shape[0]
+    row = out[0].numel() * out.element_size()
+    _lib.check(_lib.lib().mt_unstripe(S, row, world, rank, _ptr(x_local), _ptr(out), _stream()))
+    return out
+
+
 def ring_schedule(world: int, inner: int | None = None):
     """Host-side schedule from the library: held[t][x] = origin at rank x, step t."""
     out = (ctypes.c_int32 * (world * world))()

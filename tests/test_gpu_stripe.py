@@ -1,0 +1,37 @@
+"""GPU block-striped layout (mt_stripe / mt_unstripe) vs the oracle's stripe_perm
+(SURVEY §8 a1).  Byte copies: bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.sparseformat import stripe_perm
+from paper_2510_18830_b200 import _lib, ops
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("S,W", [(4096, 1), (4096, 2), (8192, 4), (131072, 8)])
+def test_stripe_roundtrip_matches_oracle_perm(cuda_lib, S, W):
+    g = torch.Generator().manual_seed(S + W)
+    x = torch.randint(-30000, 30000, (S, 3, 128), generator=g, dtype=torch.int16).cuda()
+    perm = stripe_perm(S, W)
+    back = torch.zeros_like(x)
+    for r in range(W):
+        loc = ops.stripe(x, W, r)
+        ref = x.cpu().numpy()[perm[r]]
+        assert np.array_equal(loc.cpu().numpy(), ref)
+        ops.unstripe(loc, W, r, back)
+    torch.cuda.synchronize()
+    assert torch.equal(back, x)
+
+
+def test_stripe_errors(cuda_lib):
+    x = torch.zeros(4096, 1, 8, dtype=torch.int16, device="cuda")  # 16-byte rows
+    lib = _lib.lib()
+    y = torch.zeros(1024, 1, 8, dtype=torch.int16, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.mt_stripe(4096, 16, 4, 0, x.data_ptr(), y.data_ptr(), s) == 0
+    assert lib.mt_stripe(4096, 12, 4, 0, x.data_ptr(), y.data_ptr(), s) == 1   # MT_ESHAPE
+    assert lib.mt_stripe(4096, 16, 4, 4, x.data_ptr(), y.data_ptr(), s) == 1   # rank out of range
+    assert lib.mt_stripe(4000, 16, 1, 0, x.data_ptr(), y.data_ptr(), s) == 2   # MT_EWINDOW
+    assert lib.mt_stripe(4096 + 64, 16, 2, 0, x.data_ptr(), y.data_ptr(), s) == 4  # MT_ELAYOUT
