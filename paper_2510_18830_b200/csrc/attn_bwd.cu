@@ -17,11 +17,16 @@
 //               (column, block) pair is live iff the column is not covered by a
 //               selected slash of that block (I9).  dK/dV -> atomic scatter-add
 //               (the paper's "backward for all vertical lines").
-// Per chunk (M = 128 keys, N = 64 queries):
-//   S^T = K Q^T, dP^T = V dO^T              (tcgen05 -> TMEM)
-//   P^T, dS^T (bf16, dS pre-scaled by 1/sqrt d) in registers -> smem
-//   dV += P^T dO, dK += dS^T Q              (TMEM accumulators, N = 128)
-//   dQ^T = K^T dS^T                          (TMEM, M = d) -> red.add to dQ
+// Per chunk (M = 128 keys, N = 64 queries), in the TMEM region of the softmax
+// warpgroup that owns the chunk:
+//   S^T = K Q^T, dP^T = V dO^T              (tcgen05, SMEM x SMEM -> TMEM)
+//   P^T, dS^T (bf16, dS pre-scaled by 1/sqrt d) in registers -> tcgen05.st back
+//     over S^T (A operands of the next two MMAs); dS^T also -> SMEM
+//   dV += P^T dO, dK += dS^T Q              (A from TMEM, N = 128)
+//   dQ^T = K^T dS^T                          (TMEM over dP^T, M = d) -> bulk reduce-add
+// Keeping P^T/dS^T in TMEM saves 48 KB of shared-memory traffic per chunk: the
+// SMEM x SMEM N = 64 MMAs are shared-memory-bandwidth bound (51 instead of 32
+// cycles per MMA, tools/mma_bench.cu), so SMEM bytes are this kernel's currency.
 // Warp roles: warp 0 producer (TMA / cp.async), warp 1 MMA issuer, warps 4..11
 // two softmax-backward warpgroups (alternate chunks) + dQ drain + epilogue.
 //
@@ -55,9 +60,11 @@ constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
 enum : int { kModeBlock = 0, kModeBar = 1 };
 enum : int { kChunk = 0, kEnd = 1, kDone = 2 };
 
-// TMEM columns: dK, dV accumulators; one S^T / dP^T pair shared by the two
-// softmax warpgroups (each loads it to registers at once); dQ^T per warpgroup.
-constexpr uint32_t kColDK = 0, kColDV = 128, kColS = 256, kColDP = 320, kColDQ = 384;
+// TMEM columns: dK, dV accumulators, then one 128-column region per softmax
+// warpgroup b at kColR + 128 b:
+//   [0, 64)   S^T (fp32)  -> P^T (bf16 pairs, cols 0-31) + dS^T (bf16 pairs, 32-63)
+//   [64, 128) dP^T (fp32) -> dQ^T (fp32, lanes = d)
+constexpr uint32_t kColDK = 0, kColDV = 128, kColR = 256;
 
 struct alignas(16) ChunkMeta {
   int kind;
@@ -86,7 +93,7 @@ struct Smem {
   int tile_chunks[2];      // chunks each softmax warpgroup saw in the current tile
   uint64_t full[kStages], empty[kStages];
   uint64_t kvfull, kvempty, tfree;
-  uint64_t sfull[2], sfree, dsfull[2], gdone[2], dqfree[2];
+  uint64_t sfull[2], dsfull[2], gdone[2], dqfree[2];  // dqfree: region drained
   uint32_t tmem_base;
 };
 
@@ -359,27 +366,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dO0 = make_sdesc(smem_u32(sm.dO[0]), 16, 1024);
   const uint64_t dQmn0 = make_sdesc(smem_u32(sm.q[0]), 8192, 1024);
   const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
-  const uint64_t dPT0 = make_sdesc(smem_u32(sm.pd[0]), 16, 1024);
-  const uint64_t dDST0 = make_sdesc(smem_u32(sm.pd[0] + kTileP), 16, 1024);
   const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.pd[0] + kTileP), 8192, 1024);
   uint32_t c = 0, ntile = 0;
-  uint32_t s_issued = 0, s_waited = 0;          // S^T/dP^T fills vs releases waited
-  uint32_t ds0 = 0, ds1 = 0, gq0 = 0, gq1 = 0;  // per buffer: dsfull waits, grads issued
-  auto wait_s_released = [&]() {
-    MT_CRUMB(0, 3);
-    MT_CRUMB(5, (int)s_issued);
-    MT_CRUMB(6, (int)s_waited);
-    while (s_waited < s_issued) {
-      mbar_wait(smem_u32(&sm.sfree), s_waited & 1);
-      ++s_waited;
-    }
-  };
+  uint32_t sq[2] = {0, 0};                      // S^T/dP^T issued into region b
+  uint32_t ds0 = 0, ds1 = 0;  // per buffer: dsfull waits
   for (;;) {
     {  // the next chunk tells whether another tile follows
       const uint32_t stage = c % kStages;
       mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
       if (sm.meta[stage].kind == kDone) {
-        wait_s_released();
         for (uint32_t b = 0; b < 2; ++b)
           if (leader) {
             sm.smeta[b].kind = kDone;
@@ -394,30 +389,20 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     ++ntile;
     if (P.mode == kModeBar) fence_proxy_async_smem();
     tc_fence_after();
-    // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and the
-    // S/dP TMEM pair is free; the gradient MMAs of chunk g as soon as its P/dS^T is
-    // published.  (A fixed S(k), G(k-1), S(k+1) order makes G(k) wait for chunk
+    // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and its
+    // warpgroup's TMEM region is drained; the gradient MMAs of chunk g as soon as its
+    // P/dS^T is published.  (A fixed S(k), G(k-1), S(k+1) order makes G(k) wait for chunk
     // k+1's load, which holds chunk k's stage ~2x longer: measured.)
     bool acc_started = false, end_seen = false;
     uint32_t k = 0, g = 0;  // tile-local: chunks whose S^T issued / gradients issued
     uint32_t pstage[2] = {0, 0}, end_stage = 0;
     int pseq[2] = {0, 0}, end_tile = 0;
     auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
-    auto s_released_now = [&]() {
-      while (s_waited < s_issued) {
-        if (!uni(mbar_test_wait(smem_u32(&sm.sfree), s_waited & 1))) return false;
-        ++s_waited;
-      }
-      return true;
-    };
     auto try_grads = [&]() {  // gradient MMAs of chunk g (softmax warpgroup g & 1)
       const uint32_t bg = g & 1;
       uint32_t& ds = bg ? ds1 : ds0;
-      uint32_t& gq = bg ? gq1 : gq0;
       if (!uni(mbar_test_wait(smem_u32(&sm.dsfull[bg]), ds & 1))) return false;
-      if (gq > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[bg]), (gq - 1) & 1))) return false;
       ++ds;
-      ++gq;
 #ifdef MT_TL_ISSUER
       if (leader) MT_TL(6, pseq[bg]);
 #endif
@@ -425,20 +410,18 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint32_t st = pstage[bg];
       const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
       const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
-      const uint64_t dpt = sdesc_add(dPT0, bg * 2 * kTileP);
-      const uint64_t dst = sdesc_add(dDST0, bg * 2 * kTileP);
       const uint64_t dstm = sdesc_add(dDSTmn0, bg * 2 * kTileP);
+      const uint32_t R = tmem + kColR + 128 * bg;
       if (leader) {
 #pragma unroll
-        for (int kq = 0; kq < 64; kq += 16) {
+        for (int kq = 0; kq < 64; kq += 16) {  // A = P^T / dS^T from TMEM (2 bf16 per column)
           const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
-          mma_ss(tmem + kColDV, sdesc_add(dpt, kq * 2), sdesc_add(dom, kq * 128), id_kv, acc);
-          mma_ss(tmem + kColDK, sdesc_add(dst, kq * 2), sdesc_add(dqm, kq * 128), id_kv, acc);
+          mma_ts(tmem + kColDV, R + kq / 2, sdesc_add(dom, kq * 128), id_kv, acc);
+          mma_ts(tmem + kColDK, R + 32 + kq / 2, sdesc_add(dqm, kq * 128), id_kv, acc);
         }
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16)
-          mma_ss(tmem + kColDQ + 64 * bg, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128),
-                 id_q, kk > 0);
+          mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
         mma_commit(smem_u32(&sm.gdone[bg]));
         mma_commit(smem_u32(&sm.empty[st]));
         MT_TL(3, pseq[bg]);
@@ -457,12 +440,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         ++c;
         return true;
       }
-      if (!s_released_now()) return false;
+      const uint32_t b = k & 1;
+      // region b is free once the chunk it held two chunks ago was drained
+      if (sq[b] > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[b]), (sq[b] - 1) & 1)))
+        return false;
 #ifdef MT_TL_ISSUER
       if (leader) MT_TL(7, sm.meta[stage].seq);
 #endif
       tc_fence_after();
-      const uint32_t b = k & 1;
+      const uint32_t R = tmem + kColR + 128 * b;
       if (leader) {
         sm.smeta[b] = sm.meta[stage];
         mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
@@ -471,15 +457,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         for (int kk = 0; kk < 128; kk += 16) {
           const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
           const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
-          mma_ss(tmem + kColS, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
-          mma_ss(tmem + kColDP, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
+          mma_ss(R, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
+          mma_ss(R + 64, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
         }
         mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
         MT_TL(2, sm.meta[stage].seq);
       }
       pstage[b] = stage;
       pseq[b] = sm.meta[stage].seq;
-      ++s_issued;
+      ++sq[b];
       ++k;
       ++c;
       return true;
@@ -487,14 +473,14 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     MT_CRUMB(0, 1);
     for (;;) {
       if (g < k) try_grads();
-      if (!end_seen && k < g + 2) try_s();
+      if (!end_seen) try_s();
       if (end_seen && g == k) break;
     }
     if (leader) {
       mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
       mbar_arrive(smem_u32(&sm.empty[end_stage]));
     }
-    wait_s_released();
+    // every chunk's gradients are issued, so each warpgroup consumed its last sfull
     for (uint32_t b = 0; b < 2; ++b)
       if (leader) {
         sm.smeta[b].kind = kEnd;
@@ -525,12 +511,13 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   const int slot = row >> 6, kk = row & 63;
   const uint32_t lb = (uint32_t)(quad * 32) << 16;
   const VSPlan& pl = P.plan;
-  const int Hq = pl.Hq, W = pl.W;
-  const uint32_t sfull = smem_u32(&sm.sfull[wg]), sfree = smem_u32(&sm.sfree);
+  const int W = pl.W;
+  const uint32_t sfull = smem_u32(&sm.sfull[wg]);
+  const uint32_t R = tmem + lb + kColR + 128 * wg;  // this warpgroup's TMEM region (own lanes)
   const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
   const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
   const uint32_t pdbuf = smem_u32(sm.pd[wg]);
-  const uint32_t prow = pdbuf + row * 128, drow = pdbuf + kTileP + row * 128;
+  const uint32_t drow = pdbuf + kTileP + row * 128;  // dS^T row in SMEM (B of dQ^T)
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
   uint32_t su = 0, gw = 0;  // sfull events, gdone waits
   uint32_t ntile = 0;
@@ -556,8 +543,8 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
 #endif
     tc_fence_after();
     uint32_t r0[32], r1[32];
-    tmem_ld32(tmem + lb + kColDQ + 64 * wg, r0);
-    tmem_ld32(tmem + lb + kColDQ + 64 * wg + 32, r1);
+    tmem_ld32(R + 64, r0);
+    tmem_ld32(R + 96, r1);
     tmem_ld_wait();
     tc_fence_before();
     mbar_arrive(dqfree);
@@ -619,13 +606,11 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
 #endif
       tc_fence_after();
       uint32_t sv[64], dpv[64];
-      tmem_ld32(tmem + lb + kColS, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-      tmem_ld32(tmem + lb + kColS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-      tmem_ld32(tmem + lb + kColDP, *reinterpret_cast<uint32_t(*)[32]>(&dpv[0]));
-      tmem_ld32(tmem + lb + kColDP + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
+      tmem_ld32(R, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+      tmem_ld32(R + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+      tmem_ld32(R + 64, *reinterpret_cast<uint32_t(*)[32]>(&dpv[0]));
+      tmem_ld32(R + 96, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
       tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(sfree);
       // which of the 64 queries see this key row
       uint64_t vis;
       if (P.mode == kModeBlock) {
@@ -664,17 +649,18 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
         dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
       }
+      // P^T, dS^T over S^T in this warpgroup's TMEM region (A of dV, dK)
+      tmem_st32(R, pk);
+      tmem_st32(R + 32, dk);
       wait_staging();  // the previous chunk's dQ reduce has read the buffer
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) {
         const uint32_t sw = (uint32_t)((c16 ^ (row & 7)) << 4);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + sw), "r"(pk[4 * c16]),
-                     "r"(pk[4 * c16 + 1]), "r"(pk[4 * c16 + 2]), "r"(pk[4 * c16 + 3])
-                     : "memory");
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + sw), "r"(dk[4 * c16]),
                      "r"(dk[4 * c16 + 1]), "r"(dk[4 * c16 + 2]), "r"(dk[4 * c16 + 3])
                      : "memory");
       }
+      tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(dsfull);
@@ -782,7 +768,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&sm.kvfull), 1);
     mbar_init(smem_u32(&sm.kvempty), 1);
     mbar_init(smem_u32(&sm.tfree), 1);
-    mbar_init(smem_u32(&sm.sfree), 128);
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.sfull[b]), 2);
       mbar_init(smem_u32(&sm.dsfull[b]), 128);
