@@ -368,7 +368,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
   const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.pd[0] + kTileP), 8192, 1024);
   uint32_t c = 0, ntile = 0;
-  uint32_t sq[2] = {0, 0};                      // S^T/dP^T issued into region b
+  uint32_t sq0 = 0, sq1 = 0;                    // S^T/dP^T issued into region 0 / 1
   uint32_t ds0 = 0, ds1 = 0;  // per buffer: dsfull waits
   for (;;) {
     {  // the next chunk tells whether another tile follows
@@ -395,8 +395,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     // k+1's load, which holds chunk k's stage ~2x longer: measured.)
     bool acc_started = false, end_seen = false;
     uint32_t k = 0, g = 0;  // tile-local: chunks whose S^T issued / gradients issued
-    uint32_t pstage[2] = {0, 0}, end_stage = 0;
-    int pseq[2] = {0, 0}, end_tile = 0;
+    // per region: stage / producer seq of its pending chunk (scalars: no local memory)
+    uint32_t pst0 = 0, pst1 = 0, end_stage = 0;
+    int pseq0 = 0, pseq1 = 0, end_tile = 0;
     auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
     auto try_grads = [&]() {  // gradient MMAs of chunk g (softmax warpgroup g & 1)
       const uint32_t bg = g & 1;
@@ -404,10 +405,10 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       if (!uni(mbar_test_wait(smem_u32(&sm.dsfull[bg]), ds & 1))) return false;
       ++ds;
 #ifdef MT_TL_ISSUER
-      if (leader) MT_TL(6, pseq[bg]);
+      if (leader) MT_TL(6, bg ? pseq1 : pseq0);
 #endif
       tc_fence_after();
-      const uint32_t st = pstage[bg];
+      const uint32_t st = bg ? pst1 : pst0;
       const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
       const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
       const uint64_t dstm = sdesc_add(dDSTmn0, bg * 2 * kTileP);
@@ -424,7 +425,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
           mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
         mma_commit(smem_u32(&sm.gdone[bg]));
         mma_commit(smem_u32(&sm.empty[st]));
-        MT_TL(3, pseq[bg]);
+        MT_TL(3, bg ? pseq1 : pseq0);
       }
       acc_started = true;
       ++g;
@@ -442,7 +443,8 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       }
       const uint32_t b = k & 1;
       // region b is free once the chunk it held two chunks ago was drained
-      if (sq[b] > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[b]), (sq[b] - 1) & 1)))
+      const uint32_t nsq = b ? sq1 : sq0;
+      if (nsq > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[b]), (nsq - 1) & 1)))
         return false;
 #ifdef MT_TL_ISSUER
       if (leader) MT_TL(7, sm.meta[stage].seq);
@@ -463,9 +465,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
         MT_TL(2, sm.meta[stage].seq);
       }
-      pstage[b] = stage;
-      pseq[b] = sm.meta[stage].seq;
-      ++sq[b];
+      if (b) {
+        pst1 = stage;
+        pseq1 = sm.meta[stage].seq;
+        ++sq1;
+      } else {
+        pst0 = stage;
+        pseq0 = sm.meta[stage].seq;
+        ++sq0;
+      }
       ++k;
       ++c;
       return true;
@@ -496,10 +504,44 @@ __device__ __forceinline__ void red_add_f32(float* addr, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
 }
 
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 32 queries of one key row: P = exp2(S log2e/sqrt d - LSE log2e), dS = P (dP - D)/sqrt d,
+// packed to bf16 pairs.  nl[q] = -LSE_q log2e, nd[q] = -D_q/sqrt d (pre-scaled per
+// chunk).  kMasked: queries whose bit in `vis` is clear get P = dS = 0.
+template <bool kMasked>
+__device__ __forceinline__ void softmax_half(const uint32_t (&sv)[32], const uint32_t (&dpv)[32],
+                                             const float* nl, const float* nd, float scale_log2,
+                                             float inv_sqrt_d, uint32_t vis, uint32_t* pk,
+                                             uint32_t* dk) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 4) {
+    const float4 l4 = *reinterpret_cast<const float4*>(nl + c);
+    const float4 d4 = *reinterpret_cast<const float4*>(nd + c);
+    const float la[4] = {l4.x, l4.y, l4.z, l4.w};
+    const float da[4] = {d4.x, d4.y, d4.z, d4.w};
+    float p[4], ds[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = c + u;
+      p[u] = ex2(fmaf(__uint_as_float(sv[q]), scale_log2, la[u]));
+      ds[u] = p[u] * fmaf(__uint_as_float(dpv[q]), inv_sqrt_d, da[u]);
+      if (kMasked) {
+        const bool on = (vis >> q) & 1u;
+        p[u] = on ? p[u] : 0.f;
+        ds[u] = on ? ds[u] : 0.f;
+      }
+    }
+    pk[c >> 1] = pack_bf16x2(p[0], p[1]);
+    pk[(c >> 1) + 1] = pack_bf16x2(p[2], p[3]);
+    dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
+    dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
+  }
 }
 
 __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUtensorMap* tmdq,
@@ -605,12 +647,6 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       if (row == 0) MT_TL(4, cm.seq);
 #endif
       tc_fence_after();
-      uint32_t sv[64], dpv[64];
-      tmem_ld32(R, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-      tmem_ld32(R + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-      tmem_ld32(R + 64, *reinterpret_cast<uint32_t(*)[32]>(&dpv[0]));
-      tmem_ld32(R + 96, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
-      tmem_ld_wait();
       // which of the 64 queries see this key row
       uint64_t vis;
       if (P.mode == kModeBlock) {
@@ -626,28 +662,28 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         }
         vis = live ? ~0ull : 0ull;
       }
-      const float* lse_s = sm.lse[cm.stage];
-      const float* d_s = sm.dd[cm.stage];
+      // per-query constants of the chunk, once: -LSE log2(e) and -D / sqrt(d)
+      float* nl = sm.lse[cm.stage];
+      float* nd = sm.dd[cm.stage];
+      if (row < 64)
+        nl[row] = -nl[row] * 1.4426950408889634f;
+      else
+        nd[row - 64] = -nd[row - 64] * P.inv_sqrt_d;
+      named_bar_sync(wg_bar, 128);
       uint32_t pk[32], dk[32];
 #pragma unroll
-      for (int c = 0; c < 64; c += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c);
-        const float4 d4 = *reinterpret_cast<const float4*>(d_s + c);
-        const float la[4] = {l4.x, l4.y, l4.z, l4.w};
-        const float da[4] = {d4.x, d4.y, d4.z, d4.w};
-        float p[4], ds[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int q = c + u;
-          const bool on = (vis >> q) & 1ull;
-          const float x = __uint_as_float(sv[q]) * P.scale_log2 - la[u] * 1.4426950408889634f;
-          p[u] = on ? ex2(x) : 0.f;
-          ds[u] = on ? p[u] * (__uint_as_float(dpv[q]) - da[u]) * P.inv_sqrt_d : 0.f;
-        }
-        pk[c >> 1] = pack_bf16x2(p[0], p[1]);
-        pk[(c >> 1) + 1] = pack_bf16x2(p[2], p[3]);
-        dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
-        dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
+      for (int hf = 0; hf < 2; ++hf) {  // 32 queries at a time (register budget)
+        uint32_t sv[32], dpv[32];
+        tmem_ld32(R + 32 * hf, sv);
+        tmem_ld32(R + 64 + 32 * hf, dpv);
+        tmem_ld_wait();
+        const uint32_t vh = (uint32_t)(vis >> (32 * hf));
+        if (vh == 0xffffffffu)
+          softmax_half<false>(sv, dpv, nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
+                              pk + 16 * hf, dk + 16 * hf);
+        else
+          softmax_half<true>(sv, dpv, nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
+                             pk + 16 * hf, dk + 16 * hf);
       }
       // P^T, dS^T over S^T in this warpgroup's TMEM region (A of dV, dK)
       tmem_st32(R, pk);
