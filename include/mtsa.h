@@ -267,6 +267,8 @@ mt_status mt_selftest_mma(int variant, const void* A, const void* B, float* D,
  * the most recent launch — to host memory `out` (8 * 4096 int64).  All zeros
  * unless the library was built with -DMT_TIMELINE (MT_NVCC_EXTRA). */
 mt_status mt_debug_bwd_timeline(int64_t* out);
+/* Same for the forward kernel (CTA 0 of the most recent launch). */
+mt_status mt_debug_fwd_timeline(int64_t* out);
 
 #ifdef __cplusplus
 }

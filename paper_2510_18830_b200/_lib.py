@@ -66,6 +66,7 @@ SZ = ctypes.c_size_t
 _SIGS: dict[str, list] = {
     "mt_selftest_mma": [I, P, P, P, P],
     "mt_debug_bwd_timeline": [P],
+    "mt_debug_fwd_timeline": [P],
     "mt_sparse_attn_fwd_workspace_bytes": [P, I],
     "mt_sparse_attn_fwd": [P, P, P, P, P, P, P, P, SZ, P],
     "mt_attn_fwd_step": [P, I, I, I, I, I, P, P, P, P, P, P, P, P, SZ, P],

@@ -24,6 +24,8 @@
 //   warp 3       idle
 //   warps 4..11  two softmax warpgroups; warpgroup g takes the tile's chunks
 //                k = g (mod 2); warp w covers TMEM lanes 32*(w%4)..
+#include <cstdlib>
+
 #include "common.cuh"
 #include "plan.cuh"
 #include "sm100.cuh"
@@ -33,7 +35,7 @@ namespace mt {
 
 namespace fwd {
 
-constexpr int kKSt = 3, kVSt = 2;
+constexpr int kKSt = 2, kVSt = 3;  // V lives ~2 chunks longer than K (O^T lags S^T)
 constexpr int kThreads = 384;  // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr int kSoftmax = 256;
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB
@@ -65,6 +67,7 @@ struct SMeta {
   int kind, n;
   uint32_t flags;
   int tile;
+  int seq;  // data chunk index (timeline probe)
 };
 
 struct Smem {
@@ -201,6 +204,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
           m.flags = flags;
           const uint32_t kb = smem_u32(&sm.kfull[ks]);
           mbar_expect_tx(kb, kTileKV);
+          MT_TL(0, dk);
           for (int cc = 0; cc < 2; ++cc)
             for (int x = 0; x < 2; ++x)
               tma_load_3d(smem_u32(sm.k[ks] + cc * 16384 + x * 8192), tmk, kb, cc * 64, gkv,
@@ -306,6 +310,7 @@ __device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
     if (kind == kEnd) break;
     const uint32_t vs = dv % kVSt;
     mbar_wait(smem_u32(&sm.vempty[vs]), ((dv / kVSt) & 1) ^ 1);
+    if (lane == 0) MT_TL(1, dv);
     const uint32_t vb = smem_u32(&sm.vfull[vs]);
     if (kind == kBlk) {
       if (lane == 0) {
@@ -359,6 +364,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   auto issue_o = [&]() {
     const uint32_t b = buf_ring[oc & 3], vs = oc % kVSt;
     mbar_wait(smem_u32(&sm.vfull[vs]), (oc / kVSt) & 1);
+    if (leader) MT_TL(7, oc);
     if (kind_ring[oc & 3] == kBar) fence_proxy_async_smem();
     if (b == 0) { mbar_wait(smem_u32(&sm.pfull[0]), pu0 & 1); ++pu0; }
     else        { mbar_wait(smem_u32(&sm.pfull[1]), pu1 & 1); ++pu1; }
@@ -371,6 +377,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
                (o_started || kk > 0) ? 1u : 0u);
       mma_commit(smem_u32(&sm.obar[b]));
       mma_commit(smem_u32(&sm.vempty[vs]));
+      MT_TL(3, oc);
     }
     o_started = true;
     ++oc;
@@ -421,9 +428,11 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         }
         break;
       }
+      if (leader) MT_TL(6, dc);
       const uint32_t b = k & 1;
       wait_sfree(b);
       if (leader) {
+        sm.smeta[b].seq = (int)dc;
         sm.smeta[b].kind = kind;
         sm.smeta[b].n = sm.meta[ks].n;
         sm.smeta[b].flags = sm.meta[ks].flags;
@@ -436,6 +445,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
                  sdesc_add(dq0, (kk >> 6) * 8192 + (kk & 63) * 2), id_s, kk > 0);
         mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T ready
         mma_commit(smem_u32(&sm.kempty[ks]));
+        MT_TL(2, dc);
       }
       kind_ring[dc & 3] = kind;
       buf_ring[dc & 3] = b;
@@ -515,6 +525,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
         tile = cm.kind == kEnd ? cm.tile : -1;
         break;
       }
+      if (row == 0) MT_TL(4, cm.seq);
       tc_fence_after();
       uint32_t sr[64];
       tmem_ld32(tmem + lb + kColS + 64 * wg, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -589,6 +600,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(pfull);
+      if (row == 0) MT_TL(5, cm.seq);
       ++pc;
     }
     if (tile < 0) break;  // DONE
@@ -875,3 +887,10 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
 }
 
 }  // namespace mt
+
+extern "C" mt_status mt_debug_fwd_timeline(int64_t* out) {
+  if (!out) return mt::fail(MT_ESHAPE, "NULL output");
+  if (cudaMemcpyFromSymbol(out, mt::g_mt_tl, sizeof(mt::g_mt_tl)) != cudaSuccess)
+    return mt::fail(MT_ECUDA, "cudaMemcpyFromSymbol(timeline) failed");
+  return MT_OK;
+}

@@ -1,0 +1,36 @@
+"""Forward pipeline timeline (needs a -DMT_TIMELINE build): per data chunk of CTA 0,
+0 K load issued, 1 V load issued, 6 MMA warp saw K, 2 S^T issued, 4 softmax saw S^T,
+5 P^T published, 7 MMA warp saw V, 3 O^T issued."""
+import ctypes
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2510_18830_b200 import _lib, ops  # noqa: E402
+from synth.generator import make_qkv  # noqa: E402
+
+S = int(sys.argv[1]) if len(sys.argv) > 1 else 524288
+q, k, v = make_qkv(S, 16, 2, seed=0)
+t = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).cuda()
+qd, kd, vd = t(q), t(k), t(v)
+for _ in range(2):
+    idx = ops.build_vs_index(qd, kd, 0.9, 0.9)
+    o, lse = ops.sparse_attn_fwd(qd, kd, vd, idx)
+torch.cuda.synchronize()
+buf = np.zeros((8, 4096), dtype=np.int64)
+_lib.check(_lib.lib().mt_debug_fwd_timeline(buf.ctypes.data_as(ctypes.c_void_p)))
+print("stamped per event:", (buf > 0).sum(axis=1).tolist())
+c = np.nonzero((buf > 0).all(axis=0))[0]
+c = c[c > 16]
+E = buf[:, c].astype(np.float64)
+for n, (a, b) in {"K load -> MMA saw K": (0, 6), "MMA saw K -> S issued": (6, 2),
+                  "S issued -> WG saw S": (2, 4), "WG saw S -> P published": (4, 5),
+                  "V load -> MMA saw V": (1, 7), "P published -> O issued": (5, 3),
+                  "MMA saw V -> O issued": (7, 3), "S issued -> O issued": (2, 3)}.items():
+    d = E[b] - E[a]
+    print(f"{n:26s} p10 {np.percentile(d, 10):7.0f} p50 {np.percentile(d, 50):7.0f} p90 {np.percentile(d, 90):7.0f}")
+per = np.diff(E[2])
+print(f"S-issue period: p50 {np.percentile(per, 50):.0f} mean {per.mean():.0f} clk")
