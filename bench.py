@@ -27,7 +27,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep rank 0's stdout to the one JSON line
+os.environ["NCCL_DEBUG"] = os.environ.get("MT_NCCL_DEBUG", "WARN")  # stdout = the one JSON line
 
 METRIC = "sparse attn fwd+bwd tokens/s at 512K, 1/2/4/8 B200; % of bf16 tensor peak"
 UNIT = "tokens/s"
@@ -265,7 +265,9 @@ def run_ours(args):
     tr = ROOT / "profiles" / "traffic.json"
     if tr.exists():
         try:
-            roof["traffic"] = json.loads(tr.read_text()).get("attn_bwd_bytes_per_launch")
+            t = json.loads(tr.read_text())
+            if t.get("seq_len") == S and t.get("world") == W:  # measured on this config only
+                roof["traffic"] = t.get("attn_bwd_bytes_per_launch")
         except Exception:
             pass
 

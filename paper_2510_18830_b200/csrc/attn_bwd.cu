@@ -319,9 +319,11 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     } else {
       const int bfirst = sm.cols[0] >> 6;
       // first rank-local query block with global block > bfirst
-      int j = (bfirst + 1 - P.r + W - 1) / W;
-      if (bfirst + 1 - P.r <= 0) j = 0;
-      for (; j < P.nloc; ++j) emit(T.h, j, 0u);
+      int j0 = (bfirst + 1 - P.r + W - 1) / W;
+      if (bfirst + 1 - P.r <= 0) j0 = 0;
+      // walk from the last query block down: the resident bar tiles of a head start
+      // together at j = nloc - 1 and share each Q/dO/dQ block while it is in L2
+      for (int j = P.nloc - 1; j >= j0; --j) emit(T.h, j, 0u);
     }
     // ---- END
     {
