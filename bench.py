@@ -27,7 +27,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-os.environ["NCCL_DEBUG"] = os.environ.get("MT_NCCL_DEBUG", "WARN")  # stdout = the one JSON line
+# stdout carries exactly one JSON line: NCCL's log (its version banner is printed at
+# WARN level too) goes to stderr
+os.environ["NCCL_DEBUG"] = os.environ.get("MT_NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "sparse attn fwd+bwd tokens/s at 512K, 1/2/4/8 B200; % of bf16 tensor peak"
 UNIT = "tokens/s"
@@ -250,6 +253,40 @@ def run_ours(args):
         e2e = {"value": S * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # ---- ring step profile: one extra, untimed step with CUDA events
+    # around each step's kernels and transfers (rank 0's view)
+    ring = None
+    if comm is not None:
+        comm.profile(True)
+        barrier()
+        step(qd, kd, vd, dOd)
+        torch.cuda.synchronize()
+        ring = {"profiled": "one untimed step after the timed region, rank 0", "passes": {}}
+        for name, bwd in (("fwd", False), ("bwd", True)):
+            tt = np.array(comm.step_times(bwd))  # [steps][compute, inner, outer, dkv]
+            kv = np.where(tt[:, 1] >= 0, tt[:, 1], tt[:, 2])
+            kvb = 2 * (S // W) * Hkv * 128 * 2
+            d = {"compute_ms_median": round(float(np.median(tt[:, 0])), 3),
+                 "compute_ms_per_step": [round(float(x), 3) for x in tt[:, 0]],
+                 "kv_bytes_per_step": kvb}
+            # transfer events include waiting for the peer to post its receive: the
+            # fastest step is the closest to wire time
+            kvs = kv[kv > 0]
+            if len(kvs):
+                d["kv_ms_median"] = round(float(np.median(kvs)), 3)
+                d["kv_ms_min"] = round(float(kvs.min()), 3)
+                d["kv_gbps_best"] = round(kvb / (float(kvs.min()) / 1e3) / 1e9, 1)
+            if bwd:
+                dk = tt[:, 3][tt[:, 3] > 0]
+                if len(dk):
+                    dkb = 2 * (S // W) * Hkv * 128 * 4
+                    d["dkv_bytes_per_step"] = dkb
+                    d["dkv_ms_median"] = round(float(np.median(dk)), 3)
+                    d["dkv_ms_min"] = round(float(dk.min()), 3)
+                    d["dkv_gbps_best"] = round(dkb / (float(dk.min()) / 1e3) / 1e9, 1)
+            ring["passes"][name] = d
+        comm.profile(False)
+
     pk, pk_src = peaks()
     fl_bwd = 10 * 128 * pairs / W
     fl_fwd = 4 * 128 * pairs / W
@@ -281,6 +318,7 @@ def run_ours(args):
                        "density": round(dens, 4), "activated_pairs": pairs,
                        "l2": "inputs larger than L2 (Q alone 2 GiB)"},
             "roofline": roof, "e2e": e2e, "clocks": clk,
+            **({"ring": ring} if ring else {}),
             "gpu_launches": args.steps * (17 if W == 1 else 17 + 6 * W)}
     if rank == 0 and W == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {kk: vv for kk, vv in oracle_sample(q, k, v, dO, p, S, Hq, Hkv).items()

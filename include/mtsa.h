@@ -108,6 +108,20 @@ mt_status mt_comm_unique_id(uint8_t id[128]);
 mt_status mt_comm_create(const uint8_t id[128], int world, int rank, int inner, mt_comm** out);
 mt_status mt_comm_destroy(mt_comm* comm);
 
+/* Ring step profiling (per-step compute vs communication, ring
+ * GB/s).  mt_comm_profile(comm, 1) makes later ring calls on `comm` record CUDA
+ * events around each step's kernels (compute stream) and each transfer (comm
+ * streams); 0 disables and frees them.  Recording adds a few microseconds per
+ * step: keep it out of timed regions.
+ * mt_comm_step_times: after a profiled mt_ring_attn_fwd (backward = 0) or _bwd
+ * (1), waits for its events and writes out[t * 4 + {0,1,2,3}] = milliseconds
+ * of step t's {compute, inner-ring KV transfer, outer-ring KV transfer, dK/dV
+ * partial transfer} (-1 where the step had none); *n_steps = steps written
+ * (<= max_steps).  Errors: MT_ESHAPE, MT_ECONFIG (not profiling), MT_ECUDA. */
+mt_status mt_comm_profile(mt_comm* comm, int enable);
+mt_status mt_comm_step_times(mt_comm* comm, int backward, int max_steps, float* out,
+                             int* n_steps);
+
 /* ------------------------------------------------------------- VS index */
 /* Workspace (bytes) for mt_build_vs_index on a `world`-rank layout. */
 size_t mt_build_vs_index_workspace_bytes(const mt_shape* shape, int world);

@@ -76,6 +76,8 @@ _SIGS: dict[str, list] = {
     "mt_comm_unique_id": [P],
     "mt_comm_create": [P, I, I, I, P],
     "mt_comm_destroy": [P],
+    "mt_comm_profile": [P, I],
+    "mt_comm_step_times": [P, I, I, P, P],
     "mt_sparse_attn_bwd_workspace_bytes": [P],
     "mt_sparse_attn_bwd": [P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "mt_attn_step_workspace_bytes": [P, I],

@@ -100,8 +100,60 @@ extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, 
 #endif
 }
 
+static void prof_free(mt_comm* c) {
+  if (!c->prof) return;
+  for (auto& p : c->prof->ev)
+    for (auto& st : p)
+      for (auto& e : st)
+        if (e) cudaEventDestroy(e);
+  delete c->prof;
+  c->prof = nullptr;
+}
+
+extern "C" mt_status mt_comm_profile(mt_comm* c, int enable) {
+  if (!c) return mt::fail(MT_ESHAPE, "comm is NULL");
+  if (!enable) {
+    prof_free(c);
+    return MT_OK;
+  }
+  if (c->prof) return MT_OK;
+  c->prof = new RingProfile();
+  for (auto& p : c->prof->ev)
+    for (auto& st : p)
+      for (auto& e : st)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+          prof_free(c);
+          return mt::fail(MT_ECUDA, "cudaEventCreate(profile) failed");
+        }
+  return MT_OK;
+}
+
+extern "C" mt_status mt_comm_step_times(mt_comm* c, int backward, int max_steps, float* out,
+                                        int* n_steps) {
+  if (!c || !out || !n_steps || max_steps < 0) return mt::fail(MT_ESHAPE, "NULL argument");
+  if (!c->prof) return mt::fail(MT_ECONFIG, "profiling not enabled (mt_comm_profile)");
+  const int pass = backward ? 1 : 0;
+  const int n = c->prof->steps[pass] < max_steps ? c->prof->steps[pass] : max_steps;
+  for (int t = 0; t < n; ++t)
+    for (int k = 0; k < 4; ++k) {
+      const int b = 2 * k, e = 2 * k + 1;
+      float ms = -1.f;
+      if (c->prof->rec[pass][t][b] && c->prof->rec[pass][t][e]) {
+        if (cudaEventSynchronize(c->prof->ev[pass][t][e]) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, c->prof->ev[pass][t][b], c->prof->ev[pass][t][e]) != cudaSuccess)
+          return mt::fail(MT_ECUDA, "profile event query failed");
+      }
+      out[t * 4 + k] = ms;
+    }
+  for (auto& st : c->prof->rec[pass])
+    for (auto& r : st) r = false;
+  *n_steps = n;
+  return MT_OK;
+}
+
 extern "C" mt_status mt_comm_destroy(mt_comm* c) {
   if (!c) return MT_OK;
+  prof_free(c);
 #ifdef MT_HAVE_NCCL
   if (c->nccl3) ncclCommDestroy(c->nccl3);
   if (c->nccl2) ncclCommDestroy(c->nccl2);

@@ -7,6 +7,17 @@
 #include <nccl.h>
 #endif
 
+// Optional per-step timeline of the ring calls (mt_comm_profile): CUDA events on
+// the compute stream around each step's kernels and on the comm streams around
+// each transfer.  [pass 0 fwd / 1 bwd][step][event]
+struct RingProfile {
+  static constexpr int kMaxSteps = 64, kEv = 8;
+  enum { kCompB, kCompE, kInnerB, kInnerE, kOuterB, kOuterE, kDkvB, kDkvE };
+  cudaEvent_t ev[2][kMaxSteps][kEv] = {};
+  bool rec[2][kMaxSteps][kEv] = {};
+  int steps[2] = {0, 0};
+};
+
 struct mt_comm {
 #ifdef MT_HAVE_NCCL
   ncclComm_t nccl = nullptr;   // inner (node) ring KV exchange, index collectives
@@ -19,7 +30,18 @@ struct mt_comm {
   cudaStream_t comm_stream3 = nullptr;  // dK/dV partial P2P
   cudaEvent_t ev_ready = nullptr;      // compute -> comm ordering
   cudaEvent_t ev_done = nullptr;       // comm -> compute ordering
+  RingProfile* prof = nullptr;         // non-null while profiling is enabled
 };
+
+namespace mt {
+// Record profiling event e of (pass, step) on stream st (no-op when not profiling).
+inline void prof_mark(mt_comm* c, int pass, int step, int e, cudaStream_t st) {
+  if (!c || !c->prof || step >= RingProfile::kMaxSteps) return;
+  cudaEventRecord(c->prof->ev[pass][step][e], st);
+  c->prof->rec[pass][step][e] = true;
+  if (step + 1 > c->prof->steps[pass]) c->prof->steps[pass] = step + 1;
+}
+}  // namespace mt
 
 namespace mt {
 #ifdef MT_HAVE_NCCL

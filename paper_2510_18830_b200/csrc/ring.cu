@@ -157,6 +157,7 @@ struct KVRing {
   const __nv_bfloat16* curK;
   const __nv_bfloat16* curV;
   int inner_sel = 0, outer_sel = 0;
+  int pass = 0;  // profiling: 0 forward, 1 backward
   cudaEvent_t ev_c, ev_i, ev_o;
   bool inner_pending = false, outer_pending = false;
 
@@ -193,15 +194,19 @@ struct KVRing {
     if (j == 0 && i < nout - 1) {  // outer: send the chunk held now (start of outer step)
       cudaStreamWaitEvent(c->comm_stream2, ev_c, 0);
       __nv_bfloat16* dst = (__nv_bfloat16*)ob[outer_sel];
+      prof_mark(c, pass, t, RingProfile::kOuterB, c->comm_stream2);
       MT_TRY(xchg(c->nccl2, c->comm_stream2, curK, curV, (r + G) % W, dst, (r - G + W) % W));
+      prof_mark(c, pass, t, RingProfile::kOuterE, c->comm_stream2);
       cudaEventRecord(ev_o, c->comm_stream2);
       outer_pending = true;
     }
     if (j < G - 1) {
       cudaStreamWaitEvent(c->comm_stream, ev_c, 0);
       __nv_bfloat16* dst = (__nv_bfloat16*)ib[inner_sel];
+      prof_mark(c, pass, t, RingProfile::kInnerB, c->comm_stream);
       MT_TRY(xchg(c->nccl, c->comm_stream, curK, curV, n * G + (l + 1) % G, dst,
                   n * G + (l + G - 1) % G));
+      prof_mark(c, pass, t, RingProfile::kInnerE, c->comm_stream);
       cudaEventRecord(ev_i, c->comm_stream);
       inner_pending = true;
     }
@@ -250,10 +255,13 @@ extern "C" mt_status mt_ring_attn_fwd(mt_comm* comm, const mt_shape* sh, const v
                        w.plan, stream));
   const auto sched = ring_schedule(W, comm->inner);
   KVRing ring(comm, S_loc, sh->n_kv_heads, k_loc, v_loc, w.kv);
+  if (comm->prof) comm->prof->steps[0] = 0;
   for (int t = 0; t < W; ++t) {
     MT_TRY(ring.post(t, stream));
+    prof_mark(comm, 0, t, RingProfile::kCompB, stream);
     MT_TRY(attn_fwd_step(plan, r, sched[t][r], nloc, q_loc, ring.curK, ring.curV, o_loc, w.o_acc,
                          lse_loc, t == 0, t == W - 1, device_num_sms(), stream));
+    prof_mark(comm, 0, t, RingProfile::kCompE, stream);
     ring.advance(t, stream);
   }
   return check_launch("mt_ring_attn_fwd");
@@ -292,6 +300,8 @@ extern "C" mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* sh, const v
   cudaMemsetAsync(w.dkv_acc, 0, (size_t)nkv * 2 * 4, stream);
   const auto sched = ring_schedule(W, comm->inner);
   KVRing ring(comm, S_loc, Hkv, k_loc, v_loc, w.kv);
+  ring.pass = 1;
+  if (comm->prof) comm->prof->steps[1] = 0;
   cudaEvent_t ev_done, ev_p[2];
   cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ev_p[i], cudaEventDisableTiming);
@@ -315,17 +325,21 @@ extern "C" mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* sh, const v
       cudaMemsetAsync(w.part[b], 0, (size_t)nkv * 2 * 4, stream);
       dk = w.part[b];
     }
+    prof_mark(comm, 1, t, RingProfile::kCompB, stream);
     MT_TRY(attn_bwd_step(plan, r, s, nloc, q_loc, ring.curK, ring.curV, dO_loc, lse_loc, w.D,
                          w.dq, dk, dk + nkv, device_num_sms(), stream));
+    prof_mark(comm, 1, t, RingProfile::kCompE, stream);
     // partial of the held chunk -> its owner; my own chunk's partial <- its holder
     if (s != r || holder != r) {
       cudaEventRecord(ev_done, stream);
       cudaStreamWaitEvent(comm->comm_stream3, ev_done, 0);
+      prof_mark(comm, 1, t, RingProfile::kDkvB, comm->comm_stream3);
       ncclGroupStart();
       if (s != r) ncclSend(w.part[b], 2 * nkv, ncclFloat32, s, comm->nccl3, comm->comm_stream3);
       if (holder != r)
         ncclRecv(w.recv[b], 2 * nkv, ncclFloat32, holder, comm->nccl3, comm->comm_stream3);
       if (ncclGroupEnd() != ncclSuccess) st = fail(MT_ENCCL, "dKV partial exchange failed");
+      prof_mark(comm, 1, t, RingProfile::kDkvE, comm->comm_stream3);
       cudaEventRecord(ev_p[b], comm->comm_stream3);
       p_pending[b] = (s != r);
       r_pending[b] = (holder != r);

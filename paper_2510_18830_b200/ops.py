@@ -212,6 +212,19 @@ class Comm:
             _lib.check(_lib.lib().mt_comm_destroy(self.handle))
             self.handle = None
 
+    def profile(self, enable: bool = True):
+        """Record per-step CUDA events in later ring calls (mt_comm_profile)."""
+        _lib.check(_lib.lib().mt_comm_profile(self.handle, int(enable)))
+
+    def step_times(self, backward: bool):
+        """[(compute, inner KV, outer KV, dK/dV partial) ms per step] of the last
+        profiled ring call (-1 where a step had no such transfer)."""
+        n = ctypes.c_int()
+        out = (ctypes.c_float * (4 * 64))()
+        _lib.check(_lib.lib().mt_comm_step_times(self.handle, int(backward), 64, out,
+                                                 ctypes.byref(n)))
+        return [tuple(out[4 * t + k] for k in range(4)) for t in range(n.value)]
+
 
 def stripe(x_global: torch.Tensor, world: int, rank: int) -> torch.Tensor:
     """Rank `rank`'s block-striped share of a token-major tensor (mt_stripe)."""

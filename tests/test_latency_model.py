@@ -1,0 +1,34 @@
+"""Appendix C latency model pinned to Table 4's printed totals."""
+import json
+from pathlib import Path
+
+import pytest
+
+from paper_2510_18830_b200 import latency_model as lm
+
+G = json.loads((Path(__file__).parent / "golden" / "paper_latency_table4.json").read_text())
+
+
+@pytest.mark.parametrize("pass_", ["forward", "backward"])
+def test_table4_totals(pass_):
+    g = G[pass_]
+    W = G["world"]
+    flat = lm.flat_ring_total(g["pre"], g["cpu"], g["comp"], g["intra"], g["inter"], W)
+    hier = lm.hier_ring_total(g["pre"], g["cpu"], g["comp"], g["intra"], W)
+    assert flat == pytest.approx(g["naive_total"], abs=5e-3)
+    assert hier == pytest.approx(g["hier_total"], abs=5e-3)
+    assert hier < flat  # the paper's 42.7% (fwd) cut
+
+
+def test_hierarchical_gain_vanishes_on_a_uniform_fabric():
+    """On one NVSwitch box every hop has the same bandwidth: when comm hides under
+    compute both schedules cost W steps of T_comp."""
+    f = lm.flat_ring_total(0, 0, 1.0, 0.2, 0.2, 8)
+    h = lm.hier_ring_total(0, 0, 1.0, 0.2, 8)
+    assert f == pytest.approx(h)
+
+
+def test_step_bytes_matches_survey():
+    # C4 (512K, W=8, 2 kv heads): 64 MiB KV per step; bwd adds 128 MiB fp32 dKV
+    assert lm.step_bytes(524288, 8, 2) == 64 * 2**20
+    assert lm.step_bytes(524288, 8, 2, backward=True) == (64 + 128) * 2**20
