@@ -310,7 +310,9 @@ __device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
     if (kind == kEnd) break;
     const uint32_t vs = dv % kVSt;
     mbar_wait(smem_u32(&sm.vempty[vs]), ((dv / kVSt) & 1) ^ 1);
+#ifndef MT_TL_FWD_WG
     if (lane == 0) MT_TL(1, dv);
+#endif
     const uint32_t vb = smem_u32(&sm.vfull[vs]);
     if (kind == kBlk) {
       if (lane == 0) {
@@ -542,15 +544,16 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
         live = row < cm.n;
         diag = false;
       }
-      float x[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const bool ok = live && (!diag || kk <= i);
-        x[i] = ok ? __uint_as_float(sr[i]) * P.scale_log2 : -INFINITY;
-      }
       if (!m_synced) {
+        // chunk 0 of the tile: exact column max over the 128 rows (4 warps) = the
+        // tile's fixed stabiliser (log2 units)
+        float x[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const bool ok = live && (!diag || kk <= i);
+          x[i] = ok ? __uint_as_float(sr[i]) * P.scale_log2 : -INFINITY;
+        }
         if (wg == 0) {
-          // exact column max of this chunk over the 128 rows (4 warps)
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             float tmp[32];
@@ -572,21 +575,52 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
         }
         m_synced = true;
       }
+      // P = exp2(S log2e/sqrt d - m): one FFMA + one MUFU per element; overflow of the
+      // fixed stabiliser is tracked as the largest exponent (checked once per chunk)
       uint32_t pk[32];
+      float emax = -INFINITY;
+      const float sc = P.scale_log2;
+      if (!live) {
 #pragma unroll
-      for (int i = 0; i < 64; i += 4) {
-        const float4 m4 = lds_f4(&sm.m[i]);
-        ovf |= (x[i] > m4.x + kOverflow) | (x[i + 1] > m4.y + kOverflow) |
-               (x[i + 2] > m4.z + kOverflow) | (x[i + 3] > m4.w + kOverflow);
-        const float p0 = ex2(x[i] - m4.x), p1 = ex2(x[i + 1] - m4.y);
-        const float p2 = ex2(x[i + 2] - m4.z), p3 = ex2(x[i + 3] - m4.w);
-        l[i] += p0;
-        l[i + 1] += p1;
-        l[i + 2] += p2;
-        l[i + 3] += p3;
-        pk[i >> 1] = pack_bf16x2(p0, p1);
-        pk[(i >> 1) + 1] = pack_bf16x2(p2, p3);
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+      } else if (!diag) {
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+          const float4 m4 = lds_f4(&sm.m[i]);
+          const float t0 = fmaf(__uint_as_float(sr[i]), sc, -m4.x);
+          const float t1 = fmaf(__uint_as_float(sr[i + 1]), sc, -m4.y);
+          const float t2 = fmaf(__uint_as_float(sr[i + 2]), sc, -m4.z);
+          const float t3 = fmaf(__uint_as_float(sr[i + 3]), sc, -m4.w);
+          emax = fmaxf(emax, fmaxf(fmaxf(t0, t1), fmaxf(t2, t3)));
+          const float p0 = ex2(t0), p1 = ex2(t1), p2 = ex2(t2), p3 = ex2(t3);
+          l[i] += p0;
+          l[i + 1] += p1;
+          l[i + 2] += p2;
+          l[i + 3] += p3;
+          pk[i >> 1] = pack_bf16x2(p0, p1);
+          pk[(i >> 1) + 1] = pack_bf16x2(p2, p3);
+        }
+      } else {  // diagonal block: causal mask inside (query i sees key kk <= i)
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+          const float4 m4 = lds_f4(&sm.m[i]);
+          const float ma[4] = {m4.x, m4.y, m4.z, m4.w};
+          float p[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float t = kk <= i + u ? fmaf(__uint_as_float(sr[i + u]), sc, -ma[u]) : -INFINITY;
+            emax = fmaxf(emax, t);
+            p[u] = ex2(t);
+            l[i + u] += p[u];
+          }
+          pk[i >> 1] = pack_bf16x2(p[0], p[1]);
+          pk[(i >> 1) + 1] = pack_bf16x2(p[2], p[3]);
+        }
       }
+      ovf |= emax > kOverflow;
+#ifdef MT_TL_FWD_WG
+      if (row == 0) MT_TL(1, cm.seq);  // math done, before waiting for the P^T buffer
+#endif
       while (pw < pc) {  // the O^T that last read this P^T buffer is complete
         mbar_wait(obar, pw & 1);
         ++pw;

@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2510_18830_b200 import _lib, ops  # noqa: E402
 from synth.generator import make_qkv  # noqa: E402
 
-S = int(sys.argv[1]) if len(sys.argv) > 1 else 524288
+S = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 524288
 q, k, v = make_qkv(S, 16, 2, seed=0)
 t = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).cuda()
 qd, kd, vd = t(q), t(k), t(v)
@@ -32,5 +32,9 @@ for n, (a, b) in {"K load -> MMA saw K": (0, 6), "MMA saw K -> S issued": (6, 2)
                   "MMA saw V -> O issued": (7, 3), "S issued -> O issued": (2, 3)}.items():
     d = E[b] - E[a]
     print(f"{n:26s} p10 {np.percentile(d, 10):7.0f} p50 {np.percentile(d, 50):7.0f} p90 {np.percentile(d, 90):7.0f}")
+if "--wg" in sys.argv:  # event 1 = softmax math done (MT_TL_FWD_WG build)
+    for n, (a_, b_) in {"WG saw S -> math done": (4, 1), "math done -> P published (P buffer wait)": (1, 5)}.items():
+        d = E[b_] - E[a_]
+        print(f"{n:42s} p10 {np.percentile(d, 10):7.0f} p50 {np.percentile(d, 50):7.0f} p90 {np.percentile(d, 90):7.0f}")
 per = np.diff(E[2])
 print(f"S-issue period: p50 {np.percentile(per, 50):.0f} mean {per.mean():.0f} clk")
