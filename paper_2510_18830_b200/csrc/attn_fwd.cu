@@ -204,7 +204,9 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
           m.flags = flags;
           const uint32_t kb = smem_u32(&sm.kfull[ks]);
           mbar_expect_tx(kb, kTileKV);
+#ifndef MT_TL_FWD_TILE
           MT_TL(0, dk);
+#endif
           for (int cc = 0; cc < 2; ++cc)
             for (int x = 0; x < 2; ++x)
               tma_load_3d(smem_u32(sm.k[ks] + cc * 16384 + x * 8192), tmk, kb, cc * 64, gkv,
@@ -310,7 +312,7 @@ __device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
     if (kind == kEnd) break;
     const uint32_t vs = dv % kVSt;
     mbar_wait(smem_u32(&sm.vempty[vs]), ((dv / kVSt) & 1) ^ 1);
-#ifndef MT_TL_FWD_WG
+#if !defined(MT_TL_FWD_WG) && !defined(MT_TL_FWD_TILE)
     if (lane == 0) MT_TL(1, dv);
 #endif
     const uint32_t vb = smem_u32(&sm.vfull[vs]);
@@ -401,6 +403,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       }
     }
     mbar_wait(smem_u32(&sm.qfull), qf_phase);
+#ifdef MT_TL_FWD_TILE
+    if (leader) MT_TL(6, dc);  // next tile's Q landed
+#endif
     qf_phase ^= 1;
     tc_fence_after();
     o_started = false;
@@ -414,6 +419,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       tc_fence_after();
       ++c;
       if (kind == kEnd) {
+#ifdef MT_TL_FWD_TILE
+        if (leader) MT_TL(0, dc);  // END seen (dc = next tile's first data chunk)
+#endif
         if (leader) {
           mma_commit(smem_u32(&sm.qempty));  // every S^T of the tile issued before
           mbar_arrive(smem_u32(&sm.kempty[ks]));
@@ -428,9 +436,14 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
             mbar_arrive(smem_u32(&sm.sfull[b]));
           }
         }
+#ifdef MT_TL_FWD_TILE
+        if (leader) MT_TL(1, dc);  // remaining O^T issued, END published
+#endif
         break;
       }
+#ifndef MT_TL_FWD_TILE
       if (leader) MT_TL(6, dc);
+#endif
       const uint32_t b = k & 1;
       wait_sfree(b);
       if (leader) {

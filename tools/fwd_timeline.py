@@ -23,6 +23,21 @@ torch.cuda.synchronize()
 buf = np.zeros((8, 4096), dtype=np.int64)
 _lib.check(_lib.lib().mt_debug_fwd_timeline(buf.ctypes.data_as(ctypes.c_void_p)))
 print("stamped per event:", (buf > 0).sum(axis=1).tolist())
+np.save("gpurun_out/fwd_timeline_raw.npy", buf)
+if "--tile" in sys.argv:  # MT_TL_FWD_TILE build: 0 END seen, 1 END published, 6 next Q landed
+    first = np.nonzero((buf[0] > 0) & (buf[2] > 0))[0]
+    first = first[(first > 0) & (buf[2][first - 1] > 0)]
+    S2 = buf[2].astype(np.float64)
+    gap = S2[first] - S2[first - 1]
+    per = np.diff(S2[(buf[2] > 0)])
+    print(f"tiles seen: {len(first)}; chunks/tile ~ {4096 / max(len(first), 1):.1f}")
+    print(f"boundary gap (last S -> next tile's first S): p50 {np.percentile(gap, 50):.0f} mean {gap.mean():.0f}")
+    print(f"  share of all S-issue time spent in boundary gaps: {gap.sum() / per.sum():.2%}")
+    for n, (a_, b_) in {"last S -> END seen": (None, 0), "END seen -> Os drained+published": (0, 1),
+                        "published -> next Q landed": (1, 6), "next Q landed -> first S": (6, 2)}.items():
+        x = (buf[b_][first] - (S2[first - 1] if a_ is None else buf[a_][first])).astype(np.float64)
+        print(f"  {n:36s} p50 {np.percentile(x, 50):7.0f} mean {x.mean():7.0f}")
+    sys.exit(0)
 c = np.nonzero((buf > 0).all(axis=0))[0]
 c = c[c > 16]
 E = buf[:, c].astype(np.float64)
