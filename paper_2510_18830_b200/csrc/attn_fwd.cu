@@ -62,6 +62,7 @@ struct alignas(16) VMeta {  // per data chunk: what the producers need to stage 
 };
 
 constexpr int kVM = 4;  // V-metadata ring depth
+constexpr int kSbitsWords = 1024;  // SMEM copy of a head's slash bitmap: nb <= 32768 (2M tokens)
 
 struct SMeta {
   int kind, n;
@@ -84,6 +85,7 @@ struct Smem {
   alignas(16) float wa[64];         // rescale factors / epilogue merge weights
   alignas(16) float wb[64];
   int stage_rows[192];
+  uint32_t sbits[kSbitsWords];  // the tile head's slash bitmap (producer warp only)
   int ovf;
   uint64_t kfull[kKSt], kempty[kKSt], vfull[kVSt], vempty[kVSt];
   uint64_t sfull[2], sfree[2], pfull[2], obar[2];
@@ -222,6 +224,16 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
       const int vb = pl.vptr[h * (W + 1) + P.s];
       const int ve = pl.vptr[h * (W + 1) + P.s + 1];
       int nst = 0;
+      // the coverage test reads the head's slash bitmap from SMEM (once per tile)
+      const bool bits_smem = pl.bits_words <= kSbitsWords;
+      if (bits_smem && vb < ve) {
+        const uint32_t* gb = pl.s_bits + (int64_t)h * pl.bits_words;
+        for (int w = lane; w < pl.bits_words; w += 32) sm.sbits[w] = gb[w];
+        __syncwarp();
+      }
+      auto covered = [&](int o) {
+        return bits_smem ? ((sm.sbits[o >> 5] >> (o & 31)) & 1u) != 0u : plan_has_slash(pl, h, o);
+      };
       auto emit = [&](int n) {
         VMeta& vm = vmacquire();
         kacquire();
@@ -255,16 +267,18 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         __syncwarp();
         nst = rem;
       };
+      int m_next = vb + lane < ve ? vc[vb + lane] : 0;  // loads run one batch ahead
       for (int base = vb; base < ve; base += 32) {
         const int i = base + lane;
+        const int m = m_next;
+        if (base + 32 + lane < ve) m_next = vc[base + 32 + lane];
         bool keep = false, more = false;
         int lrow = 0;
         if (i < ve) {
-          const int m = vc[i];
           const int blk = m >> 6;
           if (blk < g) {
             more = true;
-            keep = !plan_has_slash(pl, h, g - blk);
+            keep = !covered(g - blk);
             lrow = ((blk - P.s) / W) * 64 + (m & 63);
           }
         }

@@ -143,6 +143,18 @@ __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads)
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
+// TMA gather: 4 rows (r0..r3) x box-width columns starting at column c0 of a 2-D
+// tensor map, written as 4 consecutive 128-B rows of the map's swizzle layout
+// (verified byte-exact against sw128() staging for 512-B aligned destinations,
+// tools/gather4_check.cu).
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, uint32_t bar, int c0,
+                                            int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int c0,
                                             int c1, int c2) {
   asm volatile(
