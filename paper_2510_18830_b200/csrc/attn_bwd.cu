@@ -582,7 +582,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
     if (row == 0) MT_CRUMB(3 + wg, 2000000 + (int)gw);
     mbar_wait(gdone, gw & 1);  // gradient MMAs done: P/dS^T free, dQ^T complete
     ++gw;
-#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER)
+#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
     if (row == 0) MT_TL(6, seq);
 #endif
     tc_fence_after();
@@ -624,7 +624,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
           "r"(0), "r"(h), "r"(j * 64), "r"(pdbuf)
           : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER)
+#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
       MT_TL(7, seq);
 #endif
     }
@@ -688,9 +688,15 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
                              pk + 16 * hf, dk + 16 * hf);
       }
       // P^T, dS^T over S^T in this warpgroup's TMEM region (A of dV, dK)
+#ifdef MT_TL_WGSPLIT
+      if (row == 0) MT_TL(6, cm.seq);  // math done
+#endif
       tmem_st32(R, pk);
       tmem_st32(R + 32, dk);
       wait_staging();  // the previous chunk's dQ reduce has read the buffer
+#ifdef MT_TL_WGSPLIT
+      if (row == 0) MT_TL(7, cm.seq);  // staging buffer free
+#endif
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) {
         const uint32_t sw = (uint32_t)((c16 ^ (row & 7)) << 4);

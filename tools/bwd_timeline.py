@@ -44,13 +44,18 @@ for (a, b), n in zip(hops, names):
     d = E[b] - E[a]
     print(f"{n:32s} p10 {np.percentile(d, 10):8.0f}  p50 {np.percentile(d, 50):8.0f}  "
           f"p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f} clk")
+if "--wgsplit" in sys.argv:  # MT_TL_WGSPLIT: 6 = math done, 7 = staging buffer free
+    for n, (a_, b_) in {"WG sees S -> math done": (4, 6), "math done -> staging free": (6, 7),
+                        "staging free -> published": (7, 5)}.items():
+        d = E[b_] - E[a_]
+        print(f"{n:34s} p10 {np.percentile(d, 10):7.0f} p50 {np.percentile(d, 50):7.0f} p90 {np.percentile(d, 90):7.0f}")
 if "--issuer" in sys.argv:
     for n, (a, b) in {"publish -> G waits pass": (5, 6), "G waits pass -> G issued": (6, 3),
                       "S waits pass -> S issued": (7, 2), "data in smem -> S waits pass": (1, 7),
                       "S issued(k) -> S waits pass(k+1)": None}.items():
         if (a, b) is None or n.startswith("S issued(k)"):
             d = E[7][1:] - E[2][:-1]
-        else:
+        else:  # noqa
             d = E[b] - E[a]
         print(f"{n:34s} p10 {np.percentile(d, 10):7.0f} p50 {np.percentile(d, 50):7.0f} p90 {np.percentile(d, 90):7.0f}")
 if "--warps" in sys.argv:
