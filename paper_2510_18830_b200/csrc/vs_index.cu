@@ -392,6 +392,14 @@ static size_t cub_sort_bytes(int Hq, int64_t n) {
                                           (const int*)nullptr, 0, vsi::kIdxBits + vsi::kScoreBits);
   return b;
 }
+// One device-wide radix sort of n keys (the column scores of one head): a segmented
+// sort over Hq segments of S keys keeps only ~Hq CTAs busy per pass.
+static size_t cub_sort1_bytes(int64_t n) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)n,
+                                 0, vsi::kIdxBits + vsi::kScoreBits);
+  return b;
+}
 
 static VSIndexWs carve_vsidx(void* base, int64_t S, int Hq, int W) {
   VSIndexWs w{};
@@ -417,7 +425,7 @@ static VSIndexWs carve_vsidx(void* base, int64_t S, int Hq, int W) {
   w.segV = (int*)take((size_t)(Hq + 1) * 4);
   w.segP = (int*)take((size_t)(Hq + 1) * 4);
   w.qwin = (__nv_bfloat16*)take((size_t)64 * Hq * 128 * 2);
-  w.cub_bytes = std::max(cub_sort_bytes(Hq, S), cub_sort_bytes(Hq, nb));
+  w.cub_bytes = std::max(cub_sort1_bytes(S), cub_sort_bytes(Hq, nb));
   w.cub_tmp = take(w.cub_bytes);
   w.total = off;
   return w;
@@ -465,11 +473,14 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   }
   seg_offsets<<<1, 64, 0, st>>>(w.segV, Hq, S);
   seg_offsets<<<1, 64, 0, st>>>(w.segP, Hq, nb);
-  size_t tb = w.cub_bytes;
-  if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysV, w.sortV, (int)(Hq * S), Hq,
-                                              w.segV, w.segV + 1, 0, kIdxBits + kScoreBits,
-                                              st) != cudaSuccess)
-    return fail(MT_ECUDA, "segmented sort (verticals) failed");
+  size_t tb;
+  for (int h = 0; h < Hq; ++h) {  // per head: a device-wide sort (see cub_sort1_bytes)
+    tb = w.cub_bytes;
+    if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysV + (size_t)h * S,
+                                       w.sortV + (size_t)h * S, (int)S, 0, kIdxBits + kScoreBits,
+                                       st) != cudaSuccess)
+      return fail(MT_ECUDA, "radix sort (verticals) failed");
+  }
   tb = w.cub_bytes;
   if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb), Hq,
                                               w.segP, w.segP + 1, 0, kIdxBits + kScoreBits,
