@@ -288,32 +288,31 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     if (P.mode == kModeBlock) {
       const bool v1 = T.lb0 + 1 < P.nloc;
       const int kb0 = T.lb0 * W + P.s;
-      const int kb1 = v1 ? kb0 + W : -1;
       {
+        // query blocks gq = kb0 + x with x on the lattice t + mW (gq = r mod W): slot 0
+        // (key block kb0) is live iff x is a selected offset, slot 1 (kb0 + W) iff x - W
+        // is.  32 lattice points per ballot from the slash bitmap: a scalar walk of the
+        // offset list costs a dependent global load per offset and skips (W-1)/W of them.
         const int h = T.h;
-        const int ns = pl.s_cnt[h];
-        const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
-        // query blocks gq = kb + o for o = t (mod W), merged over the two key slots
-        auto next_valid = [&](int i, int kb) {
-          if (kb < 0) return ns;
-          while (i < ns) {
-            const int o = offs[i];
-            if (kb + o >= pl.nb) return ns;  // ascending offsets: no later match
-            if ((o % W) == P.t) break;
-            ++i;
+        const uint32_t* bits = pl.s_bits + (int64_t)h * pl.bits_words;
+        auto has = [&](int x) { return x >= 0 && ((bits[x >> 5] >> (x & 31)) & 1u) != 0u; };
+        const int xmax = pl.nb - kb0;  // gq < nb
+        for (int m0 = 0; P.t + m0 * W < xmax; m0 += 32) {
+          const int x = P.t + (m0 + lane) * W;
+          const bool in = x < xmax;
+          const bool a = in && has(x);
+          const bool b = in && v1 && has(x - W);
+          const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b);
+          uint32_t bal = ba | bb;
+          while (bal) {
+            const int l = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const int xs = P.t + (m0 + l) * W;
+            uint32_t flags = 0;
+            if ((ba >> l) & 1u) flags |= xs == 0 ? 5u : 1u;      // slot 0 live (+ diagonal)
+            if ((bb >> l) & 1u) flags |= xs == W ? 10u : 2u;     // slot 1 live (+ diagonal)
+            emit(h, (kb0 + xs - P.r) / W, flags);
           }
-          return i;
-        };
-        int ia = next_valid(0, kb0);
-        int ib = next_valid(0, kb1);
-        while (ia < ns || ib < ns) {
-          const int qa = ia < ns ? kb0 + offs[ia] : INT32_MAX;
-          const int qb = ib < ns ? kb1 + offs[ib] : INT32_MAX;
-          const int gq = min(qa, qb);
-          uint32_t flags = 0;
-          if (qa == gq) { flags |= 1u; if (offs[ia] == 0) flags |= 4u; ia = next_valid(ia + 1, kb0); }
-          if (qb == gq) { flags |= 2u; if (offs[ib] == 0) flags |= 8u; ib = next_valid(ib + 1, kb1); }
-          emit(h, (gq - P.r) / W, flags);
         }
       }
     } else {

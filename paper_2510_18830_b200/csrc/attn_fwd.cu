@@ -172,21 +172,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     {
       const int ns = pl.s_cnt[h];
       const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
-      auto next = [&](int from) {
-        while (from < ns) {
-          const int o = offs[from];
-          if (o > g) return ns;
-          if ((o % W) == P.t) return from;
-          ++from;
-        }
-        return ns;
-      };
-      int i = next(0);
-      while (i < ns) {
-        const int o0 = offs[i];
-        const int i1 = next(i + 1);
-        const int o1 = i1 < ns ? offs[i1] : -1;
-        i = i1 < ns ? next(i1 + 1) : ns;
+      auto emit_pair = [&](int o0, int o1) {  // o1 < 0: second slot empty
         const int lb0 = (g - o0 - P.s) / W;
         const int lb1 = o1 >= 0 ? (g - o1 - P.s) / W : lb0;
         uint32_t flags = 0;
@@ -216,7 +202,30 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         }
         vmrelease();
         ++c;
+      };
+      // offsets of residue t (= ring step) with o <= g, ascending, two per chunk.  The
+      // list is read 32 offsets per coalesced load and filtered with a ballot: a scalar
+      // walk costs one dependent global load per offset, and at W > 1 it skips the
+      // (W-1)/W offsets of other steps (measured: 3.2K cycles per chunk at W = 4).
+      int pending = -1;
+      for (int base = 0; base < ns; base += 32) {
+        const int o = base + lane < ns ? offs[base + lane] : INT_MAX;
+        const bool past = o > g;  // ascending: nothing later matches
+        uint32_t bal = __ballot_sync(0xffffffffu, !past && (o % W) == P.t);
+        while (bal) {
+          const int l = __ffs(bal) - 1;
+          bal &= bal - 1;
+          const int ov = __shfl_sync(0xffffffffu, o, l);
+          if (pending < 0) {
+            pending = ov;
+          } else {
+            emit_pair(pending, ov);
+            pending = -1;
+          }
+        }
+        if (__any_sync(0xffffffffu, past)) break;
       }
+      if (pending >= 0) emit_pair(pending, -1);
     }
     // ---- bars of origin s: block < g, offset not a selected slash; 128 per chunk
     {
