@@ -685,6 +685,19 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
     if (ovf) sm.ovf = 1;
 
     // ---- epilogue (both warpgroups): l_q, O = O^T / l, LSE, merge with the running result
+    // Ring steps after the first merge into the running (O, LSE): issue those global
+    // loads now so their latency hides behind the O^T wait and the l reductions.
+    const int64_t tok0 = (int64_t)j * 64;
+    const size_t qstride = (size_t)Hq * 128;
+    const size_t obase = (size_t)tok0 * qstride + (size_t)h * 128 + row;  // O[tok][h][d=row]
+    const int col0 = wg * 32;
+    float oacc_pre[32];
+    float lse_pre = -INFINITY;
+    if (!P.first) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) oacc_pre[i] = P.o_acc[obase + (size_t)(col0 + i) * qstride];
+      if (wg == 0 && quad < 2) lse_pre = P.lse[(int64_t)h * S_loc + tok0 + quad * 32 + lane];
+    }
     while (pw < pc) {
       mbar_wait(obar, pw & 1);
       ++pw;
@@ -695,7 +708,6 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
     sm.lsum[wg][quad][32 + lane] = warp_colreduce<false>(&l[32]);
     const bool tile_ovf = sm.ovf != 0;
     named_bar_sync(3, kSoftmax);
-    const int64_t tok0 = (int64_t)j * 64;
     if (wg == 0 && quad < 2) {
       const int q = quad * 32 + lane;
       float lq = 0.f;
@@ -711,7 +723,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
           inv_l = 1.f / lq;
           lse_new = (sm.m[q] + __log2f(lq)) * 0.69314718055994531f;
         }
-        const float lse_old = P.first ? -INFINITY : *lp;
+        const float lse_old = lse_pre;  // -inf on the first step
         const float mx = fmaxf(lse_old, lse_new);
         float out = -INFINITY;
         if (mx > -INFINITY) {
@@ -729,21 +741,18 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
     }
     named_bar_sync(3, kSoftmax);
     if (!tile_ovf) {  // flagged tiles are written by the exact fix-up pass
-      const int col0 = wg * 32;
       uint32_t o[32];
       tmem_ld32(tmem + lb + kColO + col0, o);
       tmem_ld_wait();
-      const size_t qstride = (size_t)Hq * 128;
-      const size_t base = (size_t)tok0 * qstride + (size_t)h * 128 + row;  // O[tok][h][d=row]
 #pragma unroll 8
       for (int i = 0; i < 32; ++i) {
         const int q = col0 + i;
         float val = __uint_as_float(o[i]) * sm.wb[q];
-        if (!P.first) val += sm.wa[q] * P.o_acc[base + (size_t)q * qstride];
+        if (!P.first) val += sm.wa[q] * oacc_pre[i];
         if (P.last)
-          P.o[base + (size_t)q * qstride] = __float2bfloat16_rn(val);
+          P.o[obase + (size_t)q * qstride] = __float2bfloat16_rn(val);
         else
-          P.o_acc[base + (size_t)q * qstride] = val;
+          P.o_acc[obase + (size_t)q * qstride] = val;
       }
     }
     tc_fence_before();
