@@ -88,10 +88,14 @@ __device__ long long g_mt_tl[kTlEvents][kTlChunks];
 #ifndef MT_TL_ON
 #define MT_TL_ON true
 #endif
-#define MT_TL(e, c)                                                           \
-  do {                                                                        \
-    if (blockIdx.x == 0 && (MT_TL_ON) && (unsigned)(c) < (unsigned)kTlChunks) \
-      g_mt_tl[(e)][(c)] = clock64();                                          \
+#ifndef MT_TL_SKIP
+#define MT_TL_SKIP 0  // sample chunk events [MT_TL_SKIP, MT_TL_SKIP + kTlChunks)
+#endif
+#define MT_TL(e, c)                                                               \
+  do {                                                                            \
+    const unsigned tl_i_ = (unsigned)((c) - (MT_TL_SKIP));                        \
+    if (blockIdx.x == 0 && (MT_TL_ON) && tl_i_ < (unsigned)kTlChunks)             \
+      g_mt_tl[(e)][tl_i_] = clock64();                                            \
   } while (0)
 #else
 #define MT_TL(e, c) ((void)0)
