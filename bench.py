@@ -350,7 +350,10 @@ def run_ours(args):
                                    f"p_v=p_s={p}, {'flat' if not args.inner or args.inner == W else f'{W // args.inner}x{args.inner}'} ring",
                        "seq_len": S, "global_batch": 1, "parallelism": f"cp{W}",
                        "density": round(dens, 4), "activated_pairs": pairs,
-                       "l2": "inputs larger than L2 (Q alone 2 GiB)"},
+                       "l2": "inputs larger than L2 (Q alone 2 GiB)",
+                       **({"emulated_inter_node": {"gbps": float(os.environ["MT_EMU_INTER_GBPS"]),
+                                                   "ranks_per_node": int(os.environ.get("MT_EMU_NODE", args.inner or W))}}
+                          if os.environ.get("MT_EMU_INTER_GBPS") else {})},
             "roofline": roof, "e2e": e2e, "clocks": clk,
             **({"ring": ring} if ring else {}),
             "gpu_launches": args.steps * (17 if W == 1 else 17 + 6 * W)}

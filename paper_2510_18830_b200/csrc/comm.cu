@@ -8,6 +8,10 @@
 // (uint64 fixed-point row sums), all-gather (packed sort keys).  Every rank then
 // runs the same sort/top-p and obtains the same global lists, bit-identical to
 // the single-GPU result.
+#include <chrono>
+#include <cstdlib>
+#include <thread>
+
 #include "comm.cuh"
 #include "vsidx.cuh"
 #include <cuda_bf16.h>
@@ -72,6 +76,9 @@ extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, 
   c->world = world;
   c->rank = rank;
   c->inner = inner;
+  if (const char* e = getenv("MT_EMU_INTER_GBPS")) c->emu_gbps = atof(e);
+  c->emu_node = getenv("MT_EMU_NODE") ? atoi(getenv("MT_EMU_NODE")) : inner;
+  if (c->emu_node <= 0) c->emu_node = world;
   ncclUniqueId u;
   memcpy(&u, id, 128);
   ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
@@ -98,6 +105,19 @@ extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, 
   (void)id; (void)world; (void)rank; (void)inner; (void)out;
   return fail(MT_EUNSUPPORTED, "built without NCCL");
 #endif
+}
+
+namespace {
+void sleep_host(void* p) {
+  const double ms = *static_cast<double*>(p);
+  delete static_cast<double*>(p);
+  std::this_thread::sleep_for(std::chrono::microseconds((long long)(ms * 1e3)));
+}
+}  // namespace
+
+void mt::emu_inbound(mt_comm* c, int from, size_t bytes, cudaStream_t st) {
+  if (!c || c->emu_gbps <= 0.0 || from / c->emu_node == c->rank / c->emu_node) return;
+  cudaLaunchHostFunc(st, sleep_host, new double(bytes / (c->emu_gbps * 1e9) * 1e3));
 }
 
 static void prof_free(mt_comm* c) {

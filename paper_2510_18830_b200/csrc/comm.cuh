@@ -31,9 +31,17 @@ struct mt_comm {
   cudaEvent_t ev_ready = nullptr;      // compute -> comm ordering
   cudaEvent_t ev_done = nullptr;       // comm -> compute ordering
   RingProfile* prof = nullptr;         // non-null while profiling is enabled
+  // Slow inter-node link emulation (env MT_EMU_INTER_GBPS, MT_EMU_NODE):
+  // ring receives from a rank of another emulated node are held back by
+  // bytes / emu_gbps on their comm stream (a host function: no SM is taken).
+  double emu_gbps = 0.0;  // 0 = off
+  int emu_node = 0;       // ranks per emulated node
 };
 
 namespace mt {
+// Emulated wire time of `bytes` arriving at rank c->rank from rank `from` (no-op
+// unless emulation is on and the two ranks sit on different emulated nodes).
+void emu_inbound(mt_comm* c, int from, size_t bytes, cudaStream_t st);
 // Record profiling event e of (pass, step) on stream st (no-op when not profiling).
 inline void prof_mark(mt_comm* c, int pass, int step, int e, cudaStream_t st) {
   if (!c || !c->prof || step >= RingProfile::kMaxSteps) return;

@@ -183,7 +183,9 @@ struct KVRing {
     ncclSend(v, half, ncclBfloat16, to, nc, cs);
     ncclRecv(dst, half, ncclBfloat16, from, nc, cs);
     ncclRecv(dst + half, half, ncclBfloat16, from, nc, cs);
-    return nccl_check(ncclGroupEnd(), "ring exchange");
+    MT_TRY(nccl_check(ncclGroupEnd(), "ring exchange"));
+    emu_inbound(c, from, 2 * half * sizeof(__nv_bfloat16), cs);
+    return MT_OK;
   }
   // Post the transfers of step t (before its compute).  `ready` = the stream
   // whose prior work must finish before receive targets are overwritten.
@@ -339,6 +341,7 @@ extern "C" mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* sh, const v
       if (holder != r)
         ncclRecv(w.recv[b], 2 * nkv, ncclFloat32, holder, comm->nccl3, comm->comm_stream3);
       if (ncclGroupEnd() != ncclSuccess) st = fail(MT_ENCCL, "dKV partial exchange failed");
+      if (holder != r) emu_inbound(comm, holder, (size_t)nkv * 2 * 4, comm->comm_stream3);
       prof_mark(comm, 1, t, RingProfile::kDkvE, comm->comm_stream3);
       cudaEventRecord(ev_p[b], comm->comm_stream3);
       p_pending[b] = (s != r);
