@@ -118,16 +118,20 @@ struct Params {
   int wave_pairs;           // key-block pairs per wave (<= gridDim.x)
   int waves_per_head;
   int* wave_counter;        // soft grid barrier (zeroed before the launch)
+  int bar_parts;            // BAR: query-range parts per column group
+  int bar_part_len;         // BAR: query blocks per part
   int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
 };
 
 // ---- tile decoding
 struct Tile {
   bool ok;
+  bool skip;   // BAR: part holds no query block after the tile's first column
   int g;       // kv head
   int h;       // BAR: q head
   int lb0;     // BLOCK: first local key block
   int e0, e1;  // BAR: entry range in vcol (absolute)
+  int j_lo, j_hi;  // BAR: local query blocks [j_lo, j_hi) of this part
 };
 
 __device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
@@ -143,19 +147,31 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
     T.lb0 = 2 * (tile % npairs);  // early key blocks (most work) first
     return T;
   }
+  // BAR: (head, 128-column group, part of the query range).  Parts of at most
+  // bar_part_len query blocks keep tile lengths comparable (a group of early
+  // columns otherwise walks every later query block); within a head, the parts
+  // nearest the end go first, matching the descending walk.
   int base = 0;
   for (int h = 0; h < pl.Hq; ++h) {
     const int b = pl.vptr[h * (W + 1) + P.s], e = pl.vptr[h * (W + 1) + P.s + 1];
     const int n = (e - b + 127) / 128;
-    if (tile < base + n) {
+    if (tile < base + n * P.bar_parts) {
+      const int t = tile - base;
+      const int part = P.bar_parts - 1 - t / n;
       T.ok = true;
       T.h = h;
       T.g = h / (pl.Hq / pl.Hkv);
-      T.e0 = b + (tile - base) * 128;
+      T.e0 = b + (t % n) * 128;
       T.e1 = min(e, T.e0 + 128);
+      T.j_lo = part * P.bar_part_len;
+      T.j_hi = min(P.nloc, T.j_lo + P.bar_part_len);
+      // first rank-local query block after the group's first (smallest) column
+      const int bfirst = pl.vcol[(int64_t)h * pl.S + T.e0] >> 6;
+      const int j0 = bfirst + 1 - P.r <= 0 ? 0 : (bfirst + 1 - P.r + W - 1) / W;
+      T.skip = max(T.j_lo, j0) >= T.j_hi;
       return T;
     }
-    base += n;
+    base += n * P.bar_parts;
   }
   return T;
 }
@@ -236,6 +252,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     }
     const Tile T = decode_tile(P, tile);
     if (!T.ok) break;
+    if (T.skip) continue;
     // ---- K/V tile: wait until every MMA of the previous tile finished and its
     // epilogue (which reads cols[]) is done
     if (ntile > 0) {
@@ -320,9 +337,9 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       // first rank-local query block with global block > bfirst
       int j0 = (bfirst + 1 - P.r + W - 1) / W;
       if (bfirst + 1 - P.r <= 0) j0 = 0;
-      // walk from the last query block down: the resident bar tiles of a head start
-      // together at j = nloc - 1 and share each Q/dO/dQ block while it is in L2
-      for (int j = P.nloc - 1; j >= j0; --j) emit(T.h, j, 0u);
+      // walk this part's query blocks from the last one down: the resident bar tiles
+      // of a head start together and share each Q/dO/dQ block while it is in L2
+      for (int j = T.j_hi - 1; j >= max(j0, T.j_lo); --j) emit(T.h, j, 0u);
     }
     // ---- END
     {
@@ -983,7 +1000,9 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
   P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;
-  P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128);
+  P.bar_part_len = nloc < 1024 ? (nloc > 0 ? nloc : 1) : 1024;
+  P.bar_parts = (nloc + P.bar_part_len - 1) / P.bar_part_len;
+  P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128) * P.bar_parts;
   grid = num_sms;
   attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
   return check_launch("attn_bwd_kernel(bar)");
