@@ -109,14 +109,20 @@ struct Params {
   int* fix_count;  // tiles flagged for the exact fix-up pass (stabiliser overflow)
   int* fix_list;
   int* tile_counter;  // dynamic tile scheduler (zeroed before the launch)
+  int order;          // tile order (MT_FWD_ORDER): 1 head-major (default; L2 reuse of K/V), 0 query-block-major
 };
 
 constexpr uint32_t kColO = 0, kColS = 64;  // TMEM: O^T [0,64), S^T buffers [64,128) [128,192)
 
 __device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h, int& j) {
   const int Hq = P.plan.Hq;
-  j = P.nloc - 1 - tile / Hq;  // late query blocks (most keys) first
-  h = tile % Hq;
+  if (P.order) {  // head-major: resident tiles = consecutive query blocks of one head
+    h = tile / P.nloc;
+    j = P.nloc - 1 - tile % P.nloc;
+  } else {
+    j = P.nloc - 1 - tile / Hq;  // late query blocks (most keys) first
+    h = tile % Hq;
+  }
 }
 
 // ------------------------------------------------------------------ producers
@@ -942,6 +948,8 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.lse = lse;
   P.fix_count = plan.scratch;
   P.tile_counter = plan.scratch + 1;
+  static const int ord = getenv("MT_FWD_ORDER") ? atoi(getenv("MT_FWD_ORDER")) : 1;
+  P.order = ord;
   P.fix_list = plan.scratch + 16;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmk, tmv;
