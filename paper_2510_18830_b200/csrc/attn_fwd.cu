@@ -85,12 +85,18 @@ struct Smem {
   alignas(16) float wa[64];         // rescale factors / epilogue merge weights
   alignas(16) float wb[64];
   int stage_rows[192];
+  // bar chunks: K-gather requests from the K producer (warp 0) to the gatherer (warp 3)
+  struct alignas(16) GatherReq {
+    int rows[128];
+    int ks, gkv, pad[2];
+  } greq[2];
   uint32_t sbits[kSbitsWords];  // the tile head's slash bitmap (producer warp only)
   int ovf;
   uint64_t kfull[kKSt], kempty[kKSt], vfull[kVSt], vempty[kVSt];
   uint64_t sfull[2], sfree[2], pfull[2], obar[2];
   uint64_t vmfull[kVM], vmfree[kVM];
   uint64_t qfull, qempty, mready;
+  uint64_t gqfull[2], gqempty[2];
   uint32_t tmem_base;
 };
 
@@ -138,6 +144,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
   const int W = pl.W;
   const int grp = pl.Hq / pl.Hkv;
   uint32_t c = 0, dk = 0;  // chunks (incl. END), data chunks
+  uint32_t ng = 0;         // K-gather requests posted to warp 3
   uint32_t qe_phase = 0;
   bool first_tile = true;
 
@@ -262,16 +269,18 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
           sm.meta[ks].n = n;
         }
         __syncwarp();
-        const uint32_t kbase = smem_u32(sm.k[ks]);
-        for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
-          const int row = pidx >> 4, c16 = pidx & 15;
-          const size_t goff = ((size_t)vm.rows[row] * pl.Hkv + gkv) * 128 + c16 * 8;
-          cp_async_16(kbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.k + goff);
+        {  // hand the K gather to warp 3 (it arrives on kfull[ks] when the rows land)
+          const uint32_t gi = ng & 1;
+          mbar_wait(smem_u32(&sm.gqempty[gi]), ((ng >> 1) & 1) ^ 1);
+          for (int x = lane; x < 128; x += 32) sm.greq[gi].rows[x] = vm.rows[x];
+          if (lane == 0) {
+            sm.greq[gi].ks = (int)ks;
+            sm.greq[gi].gkv = gkv;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&sm.gqfull[gi]));
+          ++ng;
         }
-        const uint32_t kb = smem_u32(&sm.kfull[ks]);
-        asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(kb) : "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kb);
         vmrelease();
         ++c;
         const int rem = nst - n;  // shift the remaining staged columns down
@@ -317,7 +326,17 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     __syncwarp();
     ++c;
   }
-  // ---- DONE: no more tiles for this CTA
+  // ---- DONE: no more tiles for this CTA; stop the K gatherer
+  {
+    const uint32_t gi = ng & 1;
+    mbar_wait(smem_u32(&sm.gqempty[gi]), ((ng >> 1) & 1) ^ 1);
+    if (lane == 0) {
+      sm.greq[gi].ks = -1;
+      mbar_arrive(smem_u32(&sm.gqfull[gi]));
+    }
+    __syncwarp();
+    ++ng;
+  }
   kacquire();
   if (lane == 0) {
     const uint32_t ks = c % kKSt;
@@ -329,6 +348,32 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
   VMeta& vm = vmacquire();
   if (lane == 0) vm.kind = kEnd;
   vmrelease();
+}
+
+// Warp 3: K rows of bar chunks, gathered with cp.async into the K stage the K
+// producer acquired (so its column scan runs on while the rows are in flight).
+__device__ void k_gatherer(Smem& sm, const Params& P) {
+  const int lane = lane_id();
+  const int Hkv = P.plan.Hkv;
+  for (uint32_t n = 0;; ++n) {
+    const uint32_t gi = n & 1;
+    mbar_wait(smem_u32(&sm.gqfull[gi]), (n >> 1) & 1);
+    const int ks = sm.greq[gi].ks, gkv = sm.greq[gi].gkv;
+    if (ks < 0) break;
+    const uint32_t kbase = smem_u32(sm.k[ks]);
+    for (int pidx = lane; pidx < 128 * 16; pidx += 32) {
+      const int row = pidx >> 4, c16 = pidx & 15;
+      const size_t goff = ((size_t)sm.greq[gi].rows[row] * Hkv + gkv) * 128 + c16 * 8;
+      cp_async_16(kbase + (c16 >> 3) * 16384 + sw128(row, c16 & 7), P.k + goff);
+    }
+    const uint32_t kb = smem_u32(&sm.kfull[ks]);
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(kb) : "memory");
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(kb);
+      mbar_arrive(smem_u32(&sm.gqempty[gi]));  // rows read: the request slot is free
+    }
+  }
 }
 
 __device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
@@ -795,6 +840,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&sm.qfull), 1);
     mbar_init(smem_u32(&sm.qempty), 1);
     mbar_init(smem_u32(&sm.mready), 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&sm.gqfull[i]), 1);
+      mbar_init(smem_u32(&sm.gqempty[i]), 1);
+    }
     for (int i = 0; i < kVM; ++i) {
       mbar_init(smem_u32(&sm.vmfull[i]), 1);
       mbar_init(smem_u32(&sm.vmfree[i]), 1);
@@ -820,6 +869,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       producer_v(sm, P, &tmv);
     } else if (warp == 1) {
       mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
+    } else {
+      k_gatherer(sm, P);
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
