@@ -11,7 +11,7 @@
 //               chunk; chunks = local query blocks j of head h with
 //               g_q - kb = o for a selected slash o (o = t mod W).  The 8 q heads
 //               of a kv group add into the same dK/dV rows -> bulk tensor
-//               reduce-add.  Tiles run in synchronised waves (below).
+//               reduce-add.  Tile order: see "L2 locality" below.
 //   mode BAR  : tile = q head h x 128 consecutive entries of the origin's
 //               vertical list; chunks = every later local query block; a
 //               (column, block) pair is live iff the column is not covered by a
@@ -37,8 +37,8 @@
 // consecutive key pairs of one head walking the same offset list at the same
 // pace: each query block they touch is reused by ~(2 x 148 x |i_s| / nb) tiles
 // while L2-resident (measured: DRAM traffic 1.84 TB -> 0.20 TB per 512K launch,
-// L2 hit 19% -> 70%).  MT_BWD_WAVE=1 additionally starts each wave of 148 tiles
-// together behind a soft grid barrier (bounded spin); measured slower.
+// L2 hit 19% -> 70%).  (Starting each wave of 148 tiles together behind a grid
+// barrier was measured slower and dropped.)
 #include <cstdlib>
 
 #include "common.cuh"
@@ -114,10 +114,6 @@ struct Params {
   float* dv;
   int* tile_counter;        // dynamic tile scheduler (zeroed before the launch)
   int static_tiles;         // 1: round-robin tiles instead (A/B switch, MT_BWD_STATIC=1)
-  int wave;                 // BLOCK: 1 = synchronised waves (MT_BWD_WAVE=1; default dynamic)
-  int wave_pairs;           // key-block pairs per wave (<= gridDim.x)
-  int waves_per_head;
-  int* wave_counter;        // soft grid barrier (zeroed before the launch)
   int bar_parts;            // BAR: query-range parts per column group
   int bar_part_len;         // BAR: query blocks per part
   int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
@@ -220,31 +216,9 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     ++c;
   };
 
-  const bool waves = P.mode == kModeBlock && P.wave;
-  const int npairs = (P.nloc + 1) / 2;
   for (int it = 0;; ++it) {
     int tile = 0;
-    if (waves) {
-      if (it >= pl.Hq * P.waves_per_head) break;
-      if (it > 0) {  // soft barrier: wave it starts when every CTA has emitted wave it-1
-        if (lane == 0) {
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.wave_counter) : "memory");
-          const int target = (int)gridDim.x * it;
-          const long long t0 = clock64();
-          for (;;) {
-            int v;
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.wave_counter) : "memory");
-            if (v >= target || clock64() - t0 > (1ll << 16)) break;
-            __nanosleep(128);
-          }
-        }
-        __syncwarp();
-      }
-      const int h = it / P.waves_per_head, w = it % P.waves_per_head;
-      const int pair = w * P.wave_pairs + (int)blockIdx.x;
-      if ((int)blockIdx.x >= P.wave_pairs || pair >= npairs) continue;  // idle in this wave
-      tile = h * npairs + pair;
-    } else if (P.static_tiles) {
+    if (P.static_tiles) {
       tile = blockIdx.x + it * gridDim.x;
     } else {
       if (lane == 0) tile = atomicAdd(P.tile_counter, 1);
@@ -965,8 +939,6 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.static_tiles = static_tiles;
   static const int dbg = getenv("MT_BWD_DBG") ? atoi(getenv("MT_BWD_DBG")) : 0;
   P.dbg = dbg;
-  static const int wave = getenv("MT_BWD_WAVE") ? atoi(getenv("MT_BWD_WAVE")) : 0;
-  P.wave = wave;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv;
   if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 64) ||
@@ -986,14 +958,11 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
     attr_done = true;
   }
   // block (slash) part
-  cudaMemsetAsync(P.tile_counter, 0, 3 * sizeof(int), st);  // 2 tile counters + wave barrier
+  cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);  // one tile counter per launch
   P.mode = kModeBlock;
   const int npairs = (nloc + 1) / 2;
   P.n_tiles = plan.Hq * npairs;
-  P.wave_counter = plan.scratch + 4;
-  P.waves_per_head = (npairs + num_sms - 1) / num_sms;
-  P.wave_pairs = P.waves_per_head > 0 ? (npairs + P.waves_per_head - 1) / P.waves_per_head : 0;
-  int grid = P.wave ? P.wave_pairs : (P.n_tiles < num_sms ? P.n_tiles : num_sms);
+  int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   if (grid > 0)
     attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
   MT_TRY(check_launch("attn_bwd_kernel(block)"));

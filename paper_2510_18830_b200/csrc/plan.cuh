@@ -27,7 +27,7 @@ struct VSPlan {
   const int32_t* vptr;  // [Hq][W + 1]
   const int32_t* vcol;  // [Hq][S] (global column ids, grouped by origin)
   int32_t* scratch;     // [16 + Hq * nb] ints: [0] fwd fix-up count, [1] fwd tile counter,
-                        // [2], [3] bwd tile counters, [4] bwd wave barrier, [16..] fix-up list
+                        // [2], [3] bwd tile counters, [16..] fix-up list
 };
 
 __device__ __forceinline__ bool plan_has_slash(const VSPlan& p, int h, int o) {
