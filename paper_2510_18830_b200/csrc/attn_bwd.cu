@@ -51,7 +51,7 @@ namespace mt {
 
 namespace bwd {
 
-constexpr int kStages = 3;      // Q / dO / LSE / D stages
+constexpr int kStages = 4;      // Q / dO / LSE / D stages
 constexpr int kThreads = 384;   // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
 constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
@@ -82,9 +82,10 @@ struct Smem {
   uint8_t v[kTileKV];
   uint8_t q[kStages][kTileQ];
   uint8_t dO[kStages][kTileQ];
-  // per softmax warpgroup: P^T (16 KB) then dS^T (16 KB); the same 32 KB also
-  // stages that warpgroup's dQ tile [64 q][128 d] fp32 for the bulk reduce-add
-  uint8_t pd[2][2 * kTileP];
+  // per softmax warpgroup: dS^T (16 KB, the B operand of dQ^T); once the gradient
+  // MMAs are done the same 16 KB stages its dQ tile, 32 queries [32][128] fp32 at
+  // a time, for the bulk reduce-adds (P^T lives in TMEM)
+  uint8_t pd[2][kTileP];
   alignas(16) float lse[kStages][64];
   alignas(16) float dd[kStages][64];
   ChunkMeta meta[kStages];
@@ -358,7 +359,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dO0 = make_sdesc(smem_u32(sm.dO[0]), 16, 1024);
   const uint64_t dQmn0 = make_sdesc(smem_u32(sm.q[0]), 8192, 1024);
   const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
-  const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.pd[0] + kTileP), 8192, 1024);
+  const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.pd[0]), 8192, 1024);
   uint32_t c = 0, ntile = 0;
   uint32_t sq0 = 0, sq1 = 0;                    // S^T/dP^T issued into region 0 / 1
   uint32_t ds0 = 0, ds1 = 0;  // per buffer: dsfull waits
@@ -403,7 +404,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint32_t st = bg ? pst1 : pst0;
       const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
       const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
-      const uint64_t dstm = sdesc_add(dDSTmn0, bg * 2 * kTileP);
+      const uint64_t dstm = sdesc_add(dDSTmn0, bg * kTileP);
       const uint32_t R = tmem + kColR + 128 * bg;
       if (leader) {
 #pragma unroll
@@ -551,7 +552,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
   const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
   const uint32_t pdbuf = smem_u32(sm.pd[wg]);
-  const uint32_t drow = pdbuf + kTileP + row * 128;  // dS^T row in SMEM (B of dQ^T)
+  const uint32_t drow = pdbuf + row * 128;  // dS^T row in SMEM (B of dQ^T)
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
   uint32_t su = 0, gw = 0;  // sfull events, gdone waits
   uint32_t ntile = 0;
@@ -592,32 +593,34 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       for (int c = 0; c < 32; ++c) red_add_f32(dst + (c + 32) * qs, __uint_as_float(r1[c]));
       return;
     }
-    // stage dQ[q][d] (fp32, [64][128]) in this warpgroup's P/dS buffer, then one
-    // bulk tensor reduce-add into the fp32 dQ accumulator
+    // stage dQ[q][d] (fp32) in this warpgroup's 16 KB buffer, 32 queries at a time,
+    // each half one bulk tensor reduce-add into the fp32 dQ accumulator
 #pragma unroll
-    for (int c = 0; c < 32; ++c)
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)(c * 128 + row) * 4),
-                   "f"(__uint_as_float(r0[c]))
-                   : "memory");
+    for (int hf = 0; hf < 2; ++hf) {
+      if (hf == 1) {  // the first half's reduce must have read the buffer
+        if (row == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        named_bar_sync(wg_bar, 128);
+      }
+      const uint32_t(&rv)[32] = hf ? r1 : r0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c)
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)((c + 32) * 128 + row) * 4),
-                   "f"(__uint_as_float(r1[c]))
-                   : "memory");
-    fence_proxy_async_smem();
-    if (row == 0) MT_CRUMB(3 + wg, 4000000);
-    named_bar_sync(wg_bar, 128);
-    if (row == 0) {
-      asm volatile(
-          "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
-          " [%0, {%1, %2, %3}], [%4];" ::"l"(tmdq),
-          "r"(0), "r"(h), "r"(j * 64), "r"(pdbuf)
-          : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
-      MT_TL(7, seq);
-#endif
+      for (int c = 0; c < 32; ++c)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)(c * 128 + row) * 4),
+                     "f"(__uint_as_float(rv[c]))
+                     : "memory");
+      fence_proxy_async_smem();
+      named_bar_sync(wg_bar, 128);
+      if (row == 0) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+            " [%0, {%1, %2, %3}], [%4];" ::"l"(tmdq),
+            "r"(0), "r"(h), "r"(j * 64 + hf * 32), "r"(pdbuf)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     }
+#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
+    if (row == 0) MT_TL(7, seq);
+#endif
     staging_busy = true;
   };
 
@@ -733,30 +736,25 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       // (rows past the chunk end are clipped by the tensor map; they hold zeros anyway)
       const CUtensorMap* tm = wg == 0 ? tmdk : tmdv;
 #pragma unroll 1
-      for (int rd = 0; rd < 2; ++rd) {
+      for (int rd = 0; rd < 4; ++rd) {  // 32 d-columns (16 KB of staging) per round
+        uint32_t a[32];
+        tmem_ld32(tmem + lb + col + rd * 32, a);
+        tmem_ld_wait();
+        const uint32_t base = pdbuf + row * 128;
 #pragma unroll
-        for (int g2 = 0; g2 < 2; ++g2) {
-          uint32_t a[32];
-          tmem_ld32(tmem + lb + col + (rd * 2 + g2) * 32, a);
-          tmem_ld_wait();
-          const uint32_t base = pdbuf + g2 * 16384 + row * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                             base + ((uint32_t)(c ^ (row & 7)) << 4)),
-                         "r"(a[4 * c]), "r"(a[4 * c + 1]), "r"(a[4 * c + 2]), "r"(a[4 * c + 3])
-                         : "memory");
-        }
+        for (int c = 0; c < 8; ++c)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                           base + ((uint32_t)(c ^ (row & 7)) << 4)),
+                       "r"(a[4 * c]), "r"(a[4 * c + 1]), "r"(a[4 * c + 2]), "r"(a[4 * c + 3])
+                       : "memory");
         fence_proxy_async_smem();
         named_bar_sync(wg_bar, 128);
         if (row == 0 && any_chunk) {
-#pragma unroll
-          for (int g2 = 0; g2 < 2; ++g2)
-            asm volatile(
-                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
-                " [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
-                "r"((rd * 2 + g2) * 32), "r"(T.g), "r"(T.lb0 * 64), "r"(pdbuf + g2 * 16384)
-                : "memory");
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+              " [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+              "r"(rd * 32), "r"(T.g), "r"(T.lb0 * 64), "r"(pdbuf)
+              : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
@@ -941,7 +939,7 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.dbg = dbg;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv;
-  if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 64) ||
+  if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 32) ||
       make_tmap_f32_3d(&tmdk, dk, 128, plan.Hkv, S_loc, 32, 1, 128, true) ||
       make_tmap_f32_3d(&tmdv, dv, 128, plan.Hkv, S_loc, 32, 1, 128, true) ||
       make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
