@@ -107,6 +107,10 @@ typedef struct mt_comm mt_comm;
 mt_status mt_comm_unique_id(uint8_t id[128]);
 mt_status mt_comm_create(const uint8_t id[128], int world, int rank, int inner, mt_comm** out);
 mt_status mt_comm_destroy(mt_comm* comm);
+/* Surface asynchronous failures: MT_ENCCL if any of the
+ * communicator's NCCL comms reports an async error, MT_ECUDA for a sticky or
+ * pending CUDA error, else MT_OK.  Non-blocking. */
+mt_status mt_comm_check(mt_comm* comm);
 
 /* Ring step profiling (per-step compute vs communication, ring
  * GB/s).  mt_comm_profile(comm, 1) makes later ring calls on `comm` record CUDA
@@ -252,6 +256,30 @@ mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* shape, const void* q_l
  * rank x holds at step t, for a ring of `world` ranks with `inner` ranks per
  * node (inner == world: flat).  out must hold world * world ints. */
 mt_status mt_ring_schedule(int world, int inner, int32_t* out);
+
+/* ------------------------------------------------------------------ format */
+/* The per-query-block key lists of an index — the sparseformat step (PAPER.md
+ * P:231-232, reading I9), global layout (world 1).  For q head h and query block g:
+ *   B_g = blk_idx[blk_ptr[h*(nb+1)+g] .. blk_ptr[h*(nb+1)+g+1])  key blocks g - o, o in
+ *         i_s[h], o <= g, ascending;
+ *   C_g = col_idx[col_ptr[...] .. col_ptr[...+1])  columns m in i_v[h] with m/64 < g and
+ *         (g - m/64) not in i_s[h] (covered verticals dropped), ascending.
+ * blk_ptr / col_ptr: device int64 [Hq][nb + 1], global offsets (head h's rows follow
+ * head h-1's).  Two passes: mt_vs_format_count fills the pointers and returns the
+ * totals n_blk / n_col to the host (it synchronizes the stream); mt_vs_format_fill
+ * writes the lists (blk_idx, col_idx: device int32, capacities >= the totals, else
+ * MT_ECAPACITY).  The attention kernels do not need this format (they derive the
+ * lists on the fly); it exists for verification and for callers that want CSR.
+ * Errors: MT_ESHAPE, MT_EWINDOW, MT_EUNSUPPORTED, MT_EWORKSPACE, MT_ECAPACITY,
+ * MT_ECUDA. */
+size_t mt_vs_format_workspace_bytes(const mt_shape* shape);
+mt_status mt_vs_format_count(const mt_shape* shape, const mt_vs_index* index, int64_t* blk_ptr,
+                             int64_t* col_ptr, int64_t* n_blk, int64_t* n_col, void* workspace,
+                             size_t ws_bytes, mt_stream_t stream);
+mt_status mt_vs_format_fill(const mt_shape* shape, const mt_vs_index* index,
+                            const int64_t* blk_ptr, const int64_t* col_ptr, int32_t* blk_idx,
+                            int64_t blk_cap, int32_t* col_idx, int64_t col_cap, int64_t n_blk,
+                            int64_t n_col, void* workspace, size_t ws_bytes, mt_stream_t stream);
 
 /* ------------------------------------------------------------------ layout */
 /* Block-striped context-parallel layout (SURVEY §8 a1,

@@ -76,6 +76,7 @@ _SIGS: dict[str, list] = {
     "mt_comm_unique_id": [P],
     "mt_comm_create": [P, I, I, I, P],
     "mt_comm_destroy": [P],
+    "mt_comm_check": [P],
     "mt_comm_profile": [P, I],
     "mt_comm_step_times": [P, I, I, P, P],
     "mt_sparse_attn_bwd_workspace_bytes": [P],
@@ -88,13 +89,17 @@ _SIGS: dict[str, list] = {
     "mt_ring_attn_bwd": [P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "mt_ring_schedule": [I, I, P],
     "mt_stripe": [I64, I64, I, I, P, P, P],
+    "mt_vs_format_workspace_bytes": [P],
+    "mt_vs_format_count": [P, P, P, P, P, P, P, SZ, P],
+    "mt_vs_format_fill": [P, P, P, P, P, I64, P, I64, I64, I64, P, SZ, P],
     "mt_unstripe": [I64, I64, I, I, P, P, P],
 }
 _RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
             "mt_build_vs_index_workspace_bytes": ctypes.c_size_t,
             "mt_sparse_attn_bwd_workspace_bytes": ctypes.c_size_t,
             "mt_attn_step_workspace_bytes": ctypes.c_size_t,
-            "mt_ring_attn_workspace_bytes": ctypes.c_size_t}
+            "mt_ring_attn_workspace_bytes": ctypes.c_size_t,
+            "mt_vs_format_workspace_bytes": ctypes.c_size_t}
 
 
 def declared_symbols() -> list[str]:

@@ -171,6 +171,21 @@ extern "C" mt_status mt_comm_step_times(mt_comm* c, int backward, int max_steps,
   return MT_OK;
 }
 
+extern "C" mt_status mt_comm_check(mt_comm* c) {
+  if (!c) return mt::fail(MT_ESHAPE, "comm is NULL");
+#ifdef MT_HAVE_NCCL
+  for (ncclComm_t nc : {c->nccl, c->nccl2, c->nccl3}) {
+    if (!nc) continue;
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(nc, &ar) != ncclSuccess || ar != ncclSuccess)
+      return mt::fail(MT_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ar));
+  }
+#endif
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return mt::fail(MT_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  return MT_OK;
+}
+
 extern "C" mt_status mt_comm_destroy(mt_comm* c) {
   if (!c) return MT_OK;
   prof_free(c);

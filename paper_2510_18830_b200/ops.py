@@ -212,6 +212,10 @@ class Comm:
             _lib.check(_lib.lib().mt_comm_destroy(self.handle))
             self.handle = None
 
+    def check(self):
+        """Raise if the communicator saw an asynchronous NCCL/CUDA failure (mt_comm_check)."""
+        _lib.check(_lib.lib().mt_comm_check(self.handle))
+
     def profile(self, enable: bool = True):
         """Record per-step CUDA events in later ring calls (mt_comm_profile)."""
         _lib.check(_lib.lib().mt_comm_profile(self.handle, int(enable)))
@@ -224,6 +228,28 @@ class Comm:
         _lib.check(_lib.lib().mt_comm_step_times(self.handle, int(backward), 64, out,
                                                  ctypes.byref(n)))
         return [tuple(out[4 * t + k] for k in range(4)) for t in range(n.value)]
+
+
+def vs_format(idx: VSIndex, seq_len: int, n_kv_heads: int = 1):
+    """Per-query-block key lists (mt_vs_format_count/fill): (blk_ptr, blk_idx, col_ptr,
+    col_idx) device tensors, pointers int64 [Hq][nb + 1] with global offsets."""
+    Hq, nb = idx.v_cnt.numel(), seq_len // BLOCK
+    sh = shape(seq_len, Hq, n_kv_heads)
+    L = _lib.lib()
+    ws = workspace(L.mt_vs_format_workspace_bytes(ctypes.byref(sh)))
+    bp = torch.empty(Hq, nb + 1, dtype=torch.int64, device=idx.v_cnt.device)
+    cp = torch.empty_like(bp)
+    nbk, ncl = ctypes.c_int64(), ctypes.c_int64()
+    ci = idx.c_struct()
+    _lib.check(L.mt_vs_format_count(ctypes.byref(sh), ctypes.byref(ci), _ptr(bp), _ptr(cp),
+                                    ctypes.byref(nbk), ctypes.byref(ncl), _ptr(ws), ws.numel(),
+                                    _stream()))
+    bi = torch.empty(max(nbk.value, 1), dtype=torch.int32, device=bp.device)
+    cl = torch.empty(max(ncl.value, 1), dtype=torch.int32, device=bp.device)
+    _lib.check(L.mt_vs_format_fill(ctypes.byref(sh), ctypes.byref(ci), _ptr(bp), _ptr(cp), _ptr(bi),
+                                   bi.numel(), _ptr(cl), cl.numel(), nbk.value, ncl.value, _ptr(ws),
+                                   ws.numel(), _stream()))
+    return bp, bi[: nbk.value], cp, cl[: ncl.value]
 
 
 def stripe(x_global: torch.Tensor, world: int, rank: int) -> torch.Tensor:

@@ -85,6 +85,7 @@ def main():
                           "errs": {k_: float(v_) for k_, v_ in errs.items()}}), flush=True)
     flag = torch.tensor([1 if all(ok.values()) else 0], device=dev)
     dist.broadcast(flag, 0)
+    comm.check()  # no asynchronous NCCL / CUDA failure surfaced (mt_comm_check)
     comm.destroy()
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 1 else 1)
