@@ -62,7 +62,7 @@ def test_bwd_random_index_many_bars_gqa(cuda_lib, S):
     _check(q, k, v, dO, iv, is_)
 
 
-@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("W", [2, 4, 8])
 def test_bwd_ring_steps_emulated(cuda_lib, W):
     """Every (rank, step) of the backward ring on one GPU vs the oracle ring backward."""
     S, Hq, Hkv = 2048, 4, 2

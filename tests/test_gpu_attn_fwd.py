@@ -65,7 +65,7 @@ def test_fwd_random_index_many_bars_gqa(cuda_lib, S):
     _check(q, k, v, iv, is_)
 
 
-@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("W", [2, 4, 8])
 def test_fwd_ring_steps_emulated(cuda_lib, W):
     """Every (rank, step) of a W-rank striped ring on one GPU vs the oracle ring."""
     S, Hq, Hkv = 2048, 4, 2
