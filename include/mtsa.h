@@ -281,6 +281,24 @@ mt_status mt_vs_format_fill(const mt_shape* shape, const mt_vs_index* index,
                             int64_t blk_cap, int32_t* col_idx, int64_t col_cap, int64_t n_blk,
                             int64_t n_col, void* workspace, size_t ws_bytes, mt_stream_t stream);
 
+/* ------------------------------------------------------------------ rope */
+/* Rotary position embedding, the step upstream of the index and the attention
+ * (SURVEY §8(f) f3).  PAPER.md Appendix A: the half-split pairs
+ * (x[i], x[i + 64]) of a 128-wide head vector at global position n rotate by
+ * n * theta_i; YaRN with factor 32 (readings: DESIGN.md R-rope).
+ * mt_rope_inv_freq (host only): theta[0..63] = base^(-2i/128), YaRN-adjusted
+ * (NTK-by-parts, beta_fast 32, beta_slow 1, original context
+ * original_max_position) when yarn_factor > 1, and the YaRN scale mscale
+ * (0.1 ln(factor) + 1; 1 without YaRN).
+ * mt_rope: in place on a token-major bf16 [S/W][n_heads][128] device tensor of
+ * rank `rank` in the block-striped layout (global positions as mt_stripe);
+ * x <- mscale * R(n) x, or mscale * R(-n) x when inverse (the backward map).
+ * Errors: MT_ESHAPE, MT_EWINDOW, MT_ELAYOUT, MT_ECUDA. */
+mt_status mt_rope_inv_freq(int head_dim, double base, double yarn_factor,
+                           int64_t original_max_position, double* theta, float* mscale);
+mt_status mt_rope(int64_t seq_len, int world, int rank, int n_heads, const double* theta,
+                  float mscale, int inverse, void* x, mt_stream_t stream);
+
 /* ------------------------------------------------------------------ layout */
 /* Block-striped context-parallel layout (SURVEY §8 a1,
  * reading Q12): global 64-token block b lives on rank b mod W as local block

@@ -89,6 +89,8 @@ _SIGS: dict[str, list] = {
     "mt_ring_attn_bwd": [P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "mt_ring_schedule": [I, I, P],
     "mt_stripe": [I64, I64, I, I, P, P, P],
+    "mt_rope_inv_freq": [I, ctypes.c_double, ctypes.c_double, I64, P, P],
+    "mt_rope": [I64, I, I, I, P, ctypes.c_float, I, P, P],
     "mt_vs_format_workspace_bytes": [P],
     "mt_vs_format_count": [P, P, P, P, P, P, P, SZ, P],
     "mt_vs_format_fill": [P, P, P, P, P, I64, P, I64, I64, I64, P, SZ, P],

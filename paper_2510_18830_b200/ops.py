@@ -252,6 +252,25 @@ def vs_format(idx: VSIndex, seq_len: int, n_kv_heads: int = 1):
     return bp, bi[: nbk.value], cp, cl[: ncl.value]
 
 
+def rope_freqs(base: float = 1e6, yarn_factor: float = 1.0, original_max_position: int = 32768):
+    """(theta[64] as ctypes doubles, mscale) from the library (mt_rope_inv_freq)."""
+    th = (ctypes.c_double * 64)()
+    ms = ctypes.c_float()
+    _lib.check(_lib.lib().mt_rope_inv_freq(128, base, yarn_factor, original_max_position, th,
+                                           ctypes.byref(ms)))
+    return th, ms.value
+
+
+def rope_(x: torch.Tensor, freqs, seq_len: int | None = None, world: int = 1, rank: int = 0,
+          inverse: bool = False) -> torch.Tensor:
+    """In-place RoPE on a token-major bf16 [S/W][H][128] tensor (mt_rope)."""
+    th, ms = freqs
+    S = seq_len or x.shape[0] * world
+    _lib.check(_lib.lib().mt_rope(S, world, rank, x.shape[1], th, ms, int(inverse), _ptr(x),
+                                  _stream()))
+    return x
+
+
 def stripe(x_global: torch.Tensor, world: int, rank: int) -> torch.Tensor:
     """Rank `rank`'s block-striped share of a token-major tensor (mt_stripe)."""
     S = x_global.shape[0]
