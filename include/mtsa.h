@@ -281,6 +281,68 @@ mt_status mt_vs_format_fill(const mt_shape* shape, const mt_vs_index* index,
                             int64_t blk_cap, int32_t* col_idx, int64_t col_cap, int64_t n_blk,
                             int64_t n_col, void* workspace, size_t ws_bytes, mt_stream_t stream);
 
+/* ---------------------------------------------------- block-sparse index */
+/* Sparse attention over an explicit block index: the paper's kernel interface
+ * block_bar_sparse_attention_forward(Q, K, V, I_block, I_bar) with I_bar
+ * empty, the form an XAttention block index takes ("w/ XAttn Idx.", P:347, P:826;
+ * SURVEY §8(f) f2).  Single GPU (world 1), same shapes and layouts as
+ * mt_sparse_attn_fwd/bwd.  The index is the CSR of mt_vs_format: for q head h and
+ * query block g the key blocks blk_idx[blk_ptr[h*(nb+1)+g] .. blk_ptr[h*(nb+1)+g+1]),
+ * device int64 pointers with global offsets, device int32 entries, n_blk entries
+ * in total.  Each row must be strictly ascending with entries <= g (causal); the
+ * block g itself is masked causally.  These properties are NOT checked on the
+ * device (a violation is undefined behaviour; mt_xattn_index and mt_vs_format
+ * produce valid rows).  Query rows with no key block get O = 0, LSE = -inf.
+ * The backward builds the transposed (key-pair-major) lists in its workspace
+ * (mt_block_sparse_attn_bwd_workspace_bytes(shape, n_blk)); the forward's
+ * workspace is mt_block_sparse_attn_fwd_workspace_bytes(shape).
+ * Errors: MT_ESHAPE, MT_EWINDOW, MT_EUNSUPPORTED, MT_EWORKSPACE, MT_ECUDA. */
+size_t mt_block_sparse_attn_fwd_workspace_bytes(const mt_shape* shape);
+mt_status mt_block_sparse_attn_fwd(const mt_shape* shape, const void* q, const void* k,
+                                   const void* v, const int64_t* blk_ptr, const int32_t* blk_idx,
+                                   int64_t n_blk, void* o, float* lse, void* workspace,
+                                   size_t ws_bytes, mt_stream_t stream);
+size_t mt_block_sparse_attn_bwd_workspace_bytes(const mt_shape* shape, int64_t n_blk);
+mt_status mt_block_sparse_attn_bwd(const mt_shape* shape, const void* q, const void* k,
+                                   const void* v, const void* o, const float* lse,
+                                   const void* dO, const int64_t* blk_ptr,
+                                   const int32_t* blk_idx, int64_t n_blk, void* dq, void* dk,
+                                   void* dv, void* workspace, size_t ws_bytes,
+                                   mt_stream_t stream);
+
+/* XAttention antidiagonal block index ("w/ XAttn Idx."; block 128,
+ * stride 16, threshold 0.9; reading R25 in DESIGN.md).  Per q head, on the stride
+ * grid i, j < S/16: A[i][j] = sum_s q[16i+15-s] . k[16j+s] / (16 sqrt d); row
+ * softmax over j <= i; block scores Bs[I][J] = sums of 8 x 8 sub-blocks (J <= I);
+ * per query block I the shortest descending prefix of Bs[I][.] reaching
+ * threshold * row total is kept (ties: smaller J first), plus the diagonal; the
+ * kept 128-blocks are written as the 64-token CSR of mt_block_sparse_attn_*
+ * (query blocks 2I, 2I+1; key blocks 2J, 2J+1; for J = I the causal half).
+ * q [S][Hq][128], k [S][Hkv][128] bf16 device (post-RoPE), world 1, S % 128 == 0.
+ * Two calls sharing one workspace: mt_xattn_index_count computes everything,
+ * writes blk_ptr (device int64 [Hq][nb + 1], global offsets) and the total n_blk
+ * to the HOST (it synchronizes the stream), and optionally copies the block scores
+ * to block_scores (device fp32 [Hq][nI (nI + 1) / 2], row I at I (I + 1) / 2,
+ * nI = S / 128; may be NULL); mt_xattn_index_fill then writes blk_idx (device
+ * int32, capacity >= n_blk) from the selection left in the workspace.
+ * The strided score GEMM is a cuBLAS bf16 GEMM (fp32 output); everything else is
+ * this library's kernels.  Errors: MT_ESHAPE, MT_EWINDOW (S % 128), MT_EUNSUPPORTED
+ * (block/stride other than 128/16), MT_EWORKSPACE, MT_ECAPACITY, MT_ECUDA. */
+typedef struct {
+  int block;       /* 128 */
+  int stride;      /* 16 */
+  float threshold; /* in [0, 1]; the paper's 0.9 */
+} mt_xattn_params;
+size_t mt_xattn_index_workspace_bytes(const mt_shape* shape);
+mt_status mt_xattn_index_count(const mt_shape* shape, const mt_xattn_params* params,
+                               const void* q, const void* k, int64_t* blk_ptr, int64_t* n_blk,
+                               float* block_scores, void* workspace, size_t ws_bytes,
+                               mt_stream_t stream);
+mt_status mt_xattn_index_fill(const mt_shape* shape, const mt_xattn_params* params,
+                              const int64_t* blk_ptr, int32_t* blk_idx, int64_t capacity,
+                              int64_t n_blk, void* workspace, size_t ws_bytes,
+                              mt_stream_t stream);
+
 /* ------------------------------------------------------------------ rope */
 /* Rotary position embedding, the step upstream of the index and the attention
  * (SURVEY §8(f) f3).  PAPER.md Appendix A: the half-split pairs

@@ -48,7 +48,8 @@ def lib() -> ctypes.CDLL:
         _lib.mt_last_error.restype = ctypes.c_char_p
         for name, argtypes in _SIGS.items():
             fn = getattr(_lib, name)
-            fn.restype = _RESTYPE.get(name, ctypes.c_int)
+            fn.restype = _RESTYPE.get(
+                name, ctypes.c_size_t if name.endswith("_workspace_bytes") else ctypes.c_int)
             fn.argtypes = argtypes
     return _lib
 
@@ -89,6 +90,13 @@ _SIGS: dict[str, list] = {
     "mt_ring_attn_bwd": [P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
     "mt_ring_schedule": [I, I, P],
     "mt_stripe": [I64, I64, I, I, P, P, P],
+    "mt_block_sparse_attn_fwd_workspace_bytes": [P],
+    "mt_block_sparse_attn_fwd": [P, P, P, P, P, P, I64, P, P, P, SZ, P],
+    "mt_block_sparse_attn_bwd_workspace_bytes": [P, I64],
+    "mt_block_sparse_attn_bwd": [P, P, P, P, P, P, P, P, P, I64, P, P, P, P, SZ, P],
+    "mt_xattn_index_workspace_bytes": [P],
+    "mt_xattn_index_count": [P, P, P, P, P, P, P, P, SZ, P],
+    "mt_xattn_index_fill": [P, P, P, P, I64, I64, P, SZ, P],
     "mt_rope_inv_freq": [I, ctypes.c_double, ctypes.c_double, I64, P, P],
     "mt_rope": [I64, I, I, I, P, ctypes.c_float, I, P, P],
     "mt_vs_format_workspace_bytes": [P],

@@ -87,6 +87,51 @@ def pairs_by_origin(i_v, i_s, S: int, W: int, layout: str) -> np.ndarray:
     return M
 
 
+def pairs_by_origin_csr(ptr, idx, S: int, W: int, layout: str) -> np.ndarray:
+    """Activated pairs [rank r][origin s] of an explicit block index in CSR form
+    (mt_block_sparse_attn_* / mt_xattn_index): ptr int64 [Hq][nb + 1] (global
+    offsets), idx the key blocks; a diagonal block is causal (2080 pairs), any
+    other full (4096)."""
+    nb = S // BLOCK
+    own = block_owner(nb, W, layout)
+    ptr = np.asarray(ptr, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int64)
+    M = np.zeros(W * W, dtype=np.float64)
+    for h in range(ptr.shape[0]):
+        b, e = ptr[h, 0], ptr[h, nb]
+        if e == b:
+            continue
+        g = np.repeat(np.arange(nb, dtype=np.int64), np.diff(ptr[h]))
+        kb = idx[b:e]
+        M += np.bincount(own[g] * W + own[kb], weights=np.where(kb == g, 2080.0, 4096.0),
+                         minlength=W * W)
+    return M.reshape(W, W).astype(np.int64)
+
+
+def pairs_by_origin_blocks(B, S: int, W: int, layout: str) -> np.ndarray:
+    """pairs_by_origin_csr for rows B[h][g] (key blocks of query block g of head h)."""
+    nb = S // BLOCK
+    ptr = np.zeros((len(B), nb + 1), dtype=np.int64)
+    flat, run = [], 0
+    for h, rows in enumerate(B):
+        for g in range(nb):
+            ptr[h, g] = run
+            run += len(rows[g])
+            flat.append(np.asarray(rows[g], dtype=np.int64))
+        ptr[h, nb] = run
+    idx = np.concatenate(flat) if flat else np.zeros(0, np.int64)
+    return pairs_by_origin_csr(ptr, idx, S, W, layout)
+
+
+def analyse_csr(ptr, idx, S: int, W: int, layout: str, held: np.ndarray | None = None) -> dict:
+    """analyse() for an explicit block index in CSR form."""
+    M = pairs_by_origin_csr(ptr, idx, S, W, layout)
+    held = flat_schedule(W) if held is None else np.asarray(held)
+    P = pairs_by_step(M, held)
+    return {"layout": layout, "world": W, "pairs": int(M.sum()), "metrics": imbalance(P).as_dict(),
+            "pairs_by_step": P.tolist()}
+
+
 def pairs_by_step(M: np.ndarray, held: np.ndarray) -> np.ndarray:
     """[rank][step] from [rank][origin] and a schedule held[t][r] = origin."""
     W = M.shape[0]

@@ -73,7 +73,8 @@ def build(verbose: bool = False) -> Path:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if LIB.exists() and LIB.stat().st_mtime >= max(o.stat().st_mtime for o in objs):
         return LIB
-    link = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+    link = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs),
+            "-lcublas", "-Xlinker=-rpath,/usr/local/cuda/lib64"]
     nccl = _nccl_dirs()
     if nccl:
         link += ["-L", str(nccl[1]), "-l:libnccl.so.2", f"-Xlinker=-rpath,{nccl[1]}"]

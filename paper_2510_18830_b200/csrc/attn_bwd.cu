@@ -280,7 +280,37 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     if (P.mode == kModeBlock) {
       const bool v1 = T.lb0 + 1 < P.nloc;
       const int kb0 = T.lb0 * W + P.s;
-      {
+      if (pl.tptr) {
+        // block-CSR mode (W = 1): the pair's sorted (gq << 1 | slot) entries; a query
+        // block attending both slots has two adjacent entries, emitted once (at the
+        // second) with both slot flags
+        const int64_t seg = (int64_t)T.h * pl.npairs + (T.lb0 >> 1);
+        const int64_t eb = pl.tptr[seg], ee = pl.tptr[seg + 1];
+        int carry = -1;  // last entry of the previous batch
+        for (int64_t base = eb; base < ee; base += 32) {
+          const int64_t i = base + lane;
+          const bool live = i < ee;
+          const int e = live ? pl.tidx[i] : -1;
+          const int nx0 = __shfl_down_sync(0xffffffffu, e, 1);
+          const int nx = i + 1 < ee ? (lane < 31 ? nx0 : pl.tidx[i + 1]) : -1;
+          const int pv0 = __shfl_up_sync(0xffffffffu, e, 1);
+          const int pv = lane == 0 ? carry : pv0;
+          const int gq = e >> 1;
+          uint32_t flags = 0;
+          if (live) {
+            flags |= (e & 1) ? (gq == kb0 + 1 ? 10u : 2u) : (gq == kb0 ? 5u : 1u);
+            if (pv >= 0 && (pv >> 1) == gq)
+              flags |= (pv & 1) ? (gq == kb0 + 1 ? 10u : 2u) : (gq == kb0 ? 5u : 1u);
+          }
+          uint32_t bal = __ballot_sync(0xffffffffu, live && (nx < 0 || (nx >> 1) != gq));
+          while (bal) {
+            const int l = __ffs(bal) - 1;
+            bal &= bal - 1;
+            emit(T.h, __shfl_sync(0xffffffffu, gq, l), __shfl_sync(0xffffffffu, flags, l));
+          }
+          carry = __shfl_sync(0xffffffffu, e, 31);
+        }
+      } else {
         // query blocks gq = kb0 + x with x on the lattice t + mW (gq = r mod W): slot 0
         // (key block kb0) is live iff x is a selected offset, slot 1 (kb0 + W) iff x - W
         // is.  32 lattice points per ballot from the slash bitmap: a scalar walk of the
@@ -307,6 +337,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
           }
         }
       }
+      (void)v1;
     } else {
       const int bfirst = sm.cols[0] >> 6;
       // first rank-local query block with global block > bfirst
@@ -964,6 +995,7 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   if (grid > 0)
     attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
   MT_TRY(check_launch("attn_bwd_kernel(block)"));
+  if (plan.bptr) return MT_OK;  // block-CSR mode: no vertical part
   // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
   P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;

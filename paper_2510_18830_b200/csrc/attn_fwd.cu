@@ -183,8 +183,6 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     }
     // ---- slash blocks of residue t, two per chunk
     {
-      const int ns = pl.s_cnt[h];
-      const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
       auto emit_pair = [&](int o0, int o1) {  // o1 < 0: second slot empty
         const int lb0 = (g - o0 - P.s) / W;
         const int lb1 = o1 >= 0 ? (g - o1 - P.s) / W : lb0;
@@ -221,6 +219,32 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
       // walk costs one dependent global load per offset, and at W > 1 it skips the
       // (W-1)/W offsets of other steps (measured: 3.2K cycles per chunk at W = 4).
       int pending = -1;
+      auto take = [&](int ov) {
+        if (pending < 0) {
+          pending = ov;
+        } else {
+          emit_pair(pending, ov);
+          pending = -1;
+        }
+      };
+      if (pl.bptr) {
+        // block-CSR mode (W = 1): the row's key blocks, last first (offsets ascending,
+        // the diagonal first as in VS mode)
+        const int64_t rb = pl.bptr[(int64_t)h * (pl.nb + 1) + g];
+        const int64_t re = pl.bptr[(int64_t)h * (pl.nb + 1) + g + 1];
+        for (int64_t top = re - 1; top >= rb; top -= 32) {
+          const int64_t i = top - lane;
+          const int o = i >= rb ? g - pl.bidx[i] : 0;
+          uint32_t bal = __ballot_sync(0xffffffffu, i >= rb);
+          while (bal) {
+            const int l = __ffs(bal) - 1;
+            bal &= bal - 1;
+            take(__shfl_sync(0xffffffffu, o, l));
+          }
+        }
+      }
+      const int ns = pl.bptr ? 0 : pl.s_cnt[h];
+      const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
       for (int base = 0; base < ns; base += 32) {
         const int o = base + lane < ns ? offs[base + lane] : INT_MAX;
         const bool past = o > g;  // ascending: nothing later matches
@@ -228,13 +252,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         while (bal) {
           const int l = __ffs(bal) - 1;
           bal &= bal - 1;
-          const int ov = __shfl_sync(0xffffffffu, o, l);
-          if (pending < 0) {
-            pending = ov;
-          } else {
-            emit_pair(pending, ov);
-            pending = -1;
-          }
+          take(__shfl_sync(0xffffffffu, o, l));
         }
         if (__any_sync(0xffffffffu, past)) break;
       }
@@ -891,6 +909,16 @@ template <typename F>
 __device__ __forceinline__ void for_each_key(const Params& P, int h, int g, int i, F&& fn) {
   const VSPlan& pl = P.plan;
   const int W = pl.W;
+  if (pl.bptr) {  // block-CSR mode (W = 1)
+    const int64_t rb = pl.bptr[(int64_t)h * (pl.nb + 1) + g];
+    const int64_t re = pl.bptr[(int64_t)h * (pl.nb + 1) + g + 1];
+    for (int64_t x = rb; x < re; ++x) {
+      const int kb = pl.bidx[x];
+      const int lim = (kb == g) ? i : 63;
+      for (int kk = 0; kk <= lim; ++kk) fn(kb * 64 + kk);
+    }
+    return;
+  }
   const int ns = pl.s_cnt[h];
   const int32_t* offs = pl.s_off + (int64_t)h * pl.s_stride;
   for (int x = 0; x < ns; ++x) {

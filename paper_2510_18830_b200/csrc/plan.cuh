@@ -28,6 +28,13 @@ struct VSPlan {
   const int32_t* vcol;  // [Hq][S] (global column ids, grouped by origin)
   int32_t* scratch;     // [16 + Hq * nb] ints: [0] fwd fix-up count, [1] fwd tile counter,
                         // [2], [3] bwd tile counters, [16..] fix-up list
+  // Block-CSR mode (mt_block_sparse_attn_*, W = 1): explicit key-block
+  // lists replace the slash lists (s_cnt = 0, no verticals).  nullptr: VS mode.
+  const int64_t* bptr;  // [Hq][nb + 1] row pointers into bidx
+  const int32_t* bidx;  // key blocks of query block g (ascending, <= g, unique)
+  const int64_t* tptr;  // [Hq * npairs + 1] segment offsets (backward only)
+  const int32_t* tidx;  // per (head, key pair p): (g << 1 | kb - 2p) ascending
+  int npairs;           // ceil(nb / 2)
 };
 
 __device__ __forceinline__ bool plan_has_slash(const VSPlan& p, int h, int o) {

@@ -252,6 +252,94 @@ def vs_format(idx: VSIndex, seq_len: int, n_kv_heads: int = 1):
     return bp, bi[: nbk.value], cp, cl[: ncl.value]
 
 
+@dataclass
+class BlockIndex:
+    """Explicit block index (the CSR of mt_vs_format / mt_xattn_index): key blocks of
+    query block g of head h are idx[ptr[h, g] : ptr[h, g + 1]] (global offsets)."""
+    ptr: torch.Tensor   # int64 [Hq][nb + 1]
+    idx: torch.Tensor   # int32 [n]
+
+    @property
+    def n(self) -> int:
+        return int(self.idx.numel())
+
+    @staticmethod
+    def from_lists(B, device="cuda") -> "BlockIndex":
+        """B[h][g]: ascending key blocks (<= g) of query block g of head h."""
+        Hq, nb = len(B), len(B[0])
+        ptr = torch.zeros(Hq, nb + 1, dtype=torch.int64)
+        flat, run = [], 0
+        for h in range(Hq):
+            for g in range(nb):
+                ptr[h, g] = run
+                flat.extend(int(x) for x in B[h][g])
+                run += len(B[h][g])
+            ptr[h, nb] = run
+        idx = torch.tensor(flat if flat else [0], dtype=torch.int32)[: run]
+        return BlockIndex(ptr.to(device), idx.to(device))
+
+    def to_lists(self):
+        p, x = self.ptr.cpu().numpy(), self.idx.cpu().numpy()
+        return [[x[p[h, g]: p[h, g + 1]].copy() for g in range(p.shape[1] - 1)]
+                for h in range(p.shape[0])]
+
+
+class XAttnParams(ctypes.Structure):
+    _fields_ = [("block", ctypes.c_int), ("stride", ctypes.c_int), ("threshold", ctypes.c_float)]
+
+
+def xattn_index(q: torch.Tensor, k: torch.Tensor, threshold: float = 0.9,
+                with_scores: bool = False):
+    """XAttention block index on the GPU (mt_xattn_index_count/fill) -> BlockIndex
+    (and the fp32 block scores [Hq][nI (nI + 1) / 2] when with_scores)."""
+    S, Hq, _ = q.shape
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    prm = XAttnParams(128, 16, threshold)
+    ws = workspace(L.mt_xattn_index_workspace_bytes(ctypes.byref(sh)))
+    nI = S // 128
+    ptr = torch.empty(Hq, S // 64 + 1, dtype=torch.int64, device=q.device)
+    scores = (torch.empty(Hq, nI * (nI + 1) // 2, dtype=torch.float32, device=q.device)
+              if with_scores else None)
+    n = ctypes.c_int64()
+    _lib.check(L.mt_xattn_index_count(ctypes.byref(sh), ctypes.byref(prm), _ptr(q), _ptr(k),
+                                      _ptr(ptr), ctypes.byref(n), _ptr(scores), _ptr(ws),
+                                      ws.numel(), _stream()))
+    idx = torch.empty(max(n.value, 1), dtype=torch.int32, device=q.device)
+    _lib.check(L.mt_xattn_index_fill(ctypes.byref(sh), ctypes.byref(prm), _ptr(ptr), _ptr(idx),
+                                     idx.numel(), n.value, _ptr(ws), ws.numel(), _stream()))
+    bi = BlockIndex(ptr, idx[: n.value])
+    return (bi, scores) if with_scores else bi
+
+
+def block_sparse_attn_fwd(q, k, v, bidx: BlockIndex):
+    """mt_block_sparse_attn_fwd -> (o bf16 [S][Hq][128], lse f32 [Hq][S])."""
+    S, Hq, _ = q.shape
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_block_sparse_attn_fwd_workspace_bytes(ctypes.byref(sh)))
+    o = torch.empty_like(q)
+    lse = torch.empty(Hq, S, dtype=torch.float32, device=q.device)
+    _lib.check(L.mt_block_sparse_attn_fwd(ctypes.byref(sh), _ptr(q), _ptr(k), _ptr(v),
+                                          _ptr(bidx.ptr), _ptr(bidx.idx), bidx.n, _ptr(o),
+                                          _ptr(lse), _ptr(ws), ws.numel(), _stream()))
+    return o, lse
+
+
+def block_sparse_attn_bwd(q, k, v, o, lse, dO, bidx: BlockIndex):
+    """mt_block_sparse_attn_bwd -> (dq, dk, dv) bf16."""
+    S, Hq, _ = q.shape
+    sh = shape(S, Hq, k.shape[1])
+    L = _lib.lib()
+    ws = workspace(L.mt_block_sparse_attn_bwd_workspace_bytes(ctypes.byref(sh), bidx.n))
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    _lib.check(L.mt_block_sparse_attn_bwd(ctypes.byref(sh), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                          _ptr(lse), _ptr(dO), _ptr(bidx.ptr), _ptr(bidx.idx),
+                                          bidx.n, _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws),
+                                          ws.numel(), _stream()))
+    return dq, dk, dv
+
+
 def rope_freqs(base: float = 1e6, yarn_factor: float = 1.0, original_max_position: int = 32768):
     """(theta[64] as ctypes doubles, mscale) from the library (mt_rope_inv_freq)."""
     th = (ctypes.c_double * 64)()

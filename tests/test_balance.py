@@ -79,3 +79,28 @@ def test_imbalance_metrics_closed_forms():
     assert m.step_id == pytest.approx(1.4)
     assert m.comp_ratio == pytest.approx((3 + 2) / (4 + 3))
     assert m.total_id == pytest.approx(1.0)
+
+
+@pytest.mark.parametrize("layout", balance.LAYOUTS)
+def test_block_index_pairs_match_bruteforce_mask(layout):
+    """Explicit block rows (the XAttention / block-CSR form): brute-force count over
+    the materialised causal block mask."""
+    S, W = 1024, 4
+    nb = S // 64
+    rng = np.random.default_rng(3)
+    B = [[np.unique(np.r_[rng.choice(g + 1, min(g + 1, 3), replace=False), g]).astype(np.int32)
+          for g in range(nb)] for _ in range(2)]
+    M = balance.pairs_by_origin_blocks(B, S, W, layout)
+    own = _owner_tokens(S, W, layout)
+    ref = np.zeros((W, W), dtype=np.int64)
+    tok = np.arange(S)
+    for rows in B:
+        mask = np.zeros((S, S), bool)
+        for g, r in enumerate(rows):
+            for kb in r:
+                mask[g * 64:(g + 1) * 64, kb * 64:(kb + 1) * 64] = True
+        mask &= tok[:, None] >= tok[None, :]
+        for a in range(W):
+            for b in range(W):
+                ref[a, b] += mask[np.ix_(own == a, own == b)].sum()
+    assert np.array_equal(M, ref)

@@ -1,0 +1,110 @@
+"""GPU block-CSR sparse attention (mt_block_sparse_attn_fwd/bwd: the paper's
+block_bar_sparse_attention_forward(Q, K, V, I_block, I_bar) with I_bar empty, P:878;
+the XAttention-index path of SURVEY §8(f) f2) vs the fp64 oracle's per-block
+forward/backward (oracle/attention.py forward_block / backward_block with C_g
+empty).  Random ascending block rows with and without the diagonal, some empty
+rows, GQA, a ragged pair tail (odd nb).  Tolerance: north_star 2e-2 normwise (R20),
+LSE absolute 1e-3; empty rows: O = 0, LSE = -inf."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as OA
+from oracle.sparseformat import sparseformat
+from paper_2510_18830_b200 import ops
+from synth.generator import make_grad_out, make_qkv
+from tests.gpu_util import f64, normwise_err, random_index, to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _random_rows(S, Hq, seed, p, p_diag=0.9, p_empty=0.05):
+    rng = np.random.default_rng(seed)
+    nb = S // 64
+    B = []
+    for h in range(Hq):
+        rows = []
+        for g in range(nb):
+            if rng.random() < p_empty:
+                rows.append(np.zeros(0, np.int32))
+                continue
+            r = np.flatnonzero(rng.random(g) < p).astype(np.int32)
+            if rng.random() < p_diag:
+                r = np.append(r, np.int32(g))
+            rows.append(r)
+        B.append(rows)
+    return B
+
+
+def _oracle(q, k, v, dO, B):
+    qf, kf, vf, dOf = f64(q), f64(k), f64(v), f64(dO)
+    S, Hq, d = qf.shape
+    grp = Hq // kf.shape[1]
+    O = np.zeros((S, Hq, d))
+    L = np.full((Hq, S), -np.inf)
+    for h in range(Hq):
+        for g, row in enumerate(B[h]):
+            if len(row) == 0:  # empty row: O = 0, LSE = -inf (the API's definition)
+                continue
+            sl = slice(g * 64, g * 64 + 64)
+            O[sl, h], L[h, sl] = OA.forward_block(qf, kf, vf, h, g, row, [])
+    dQ, dK, dV = np.zeros_like(qf), np.zeros_like(kf), np.zeros_like(vf)
+    for h in range(Hq):
+        for g, row in enumerate(B[h]):
+            if len(row) == 0:
+                continue
+            dq, keys, dk, dv = OA.backward_block(qf, kf, vf, O, L, dOf, h, g, row, [])
+            dQ[g * 64: g * 64 + 64, h] += dq
+            dK[keys, h // grp] += dk
+            dV[keys, h // grp] += dv
+    return O, L, dQ, dK, dV
+
+
+def _run(q, k, v, dO, B):
+    bi = ops.BlockIndex.from_lists(B)
+    qd, kd, vd, dOd = (to_dev_bf16(x) for x in (q, k, v, dO))
+    o, lse = ops.block_sparse_attn_fwd(qd, kd, vd, bi)
+    dq, dk, dv = ops.block_sparse_attn_bwd(qd, kd, vd, o, lse, dOd, bi)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)
+    return f(o), lse.cpu().numpy().astype(np.float64), f(dq), f(dk), f(dv)
+
+
+def _compare(got, ref):
+    o, lse, dq, dk, dv = got
+    O, L, dQ, dK, dV = ref
+    empty = ~np.isfinite(L)
+    assert np.array_equal(~np.isfinite(lse), empty)
+    assert np.all(o.transpose(1, 0, 2)[empty] == 0)
+    assert np.max(np.abs(lse[~empty] - L[~empty])) <= 1e-3
+    errs = [normwise_err(a, b, 1) for a, b in ((o, O), (dq, dQ), (dk, dK), (dv, dV))]
+    assert max(errs) <= TOL, errs
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,p", [(2112, 4, 2, 0.15), (4096, 8, 1, 0.05), (1024, 2, 2, 1.0)])
+def test_block_csr_matches_oracle(cuda_lib, S, Hq, Hkv, p):
+    q, k, v = make_qkv(S, Hq, Hkv, seed=S + Hq, a=6.0)
+    dO = make_grad_out(S, Hq, seed=S)
+    B = _random_rows(S, Hq, seed=S, p=p, p_empty=0.0 if p == 1.0 else 0.05)
+    _compare(_run(q, k, v, dO, B), _oracle(q, k, v, dO, B))
+
+
+def test_block_csr_of_vs_index_equals_vs_path(cuda_lib):
+    """The CSR of a VS index without verticals (mt_vs_format's B_g) through the block
+    path gives the VS path's result: same key sets, same kernels (bit-identical O is
+    not required — chunk order differs — but both are within the bound of the oracle
+    and of each other)."""
+    S, Hq, Hkv = 4096, 4, 2
+    q, k, v = make_qkv(S, Hq, Hkv, seed=5, a=6.0)
+    dO = make_grad_out(S, Hq, seed=5)
+    _, is_ = random_index(S, Hq, seed=9, n_off=8, n_col=0)
+    iv = [np.zeros(0, np.int32)] * Hq
+    B = [sparseformat(iv[h], is_[h], S)[0] for h in range(Hq)]
+    got = _run(q, k, v, dO, B)
+    qd, kd, vd, dOd = (to_dev_bf16(x) for x in (q, k, v, dO))
+    idx = ops.VSIndex.from_lists(iv, is_, S)
+    o2, lse2 = ops.sparse_attn_fwd(qd, kd, vd, idx)
+    torch.cuda.synchronize()
+    assert normwise_err(got[0], o2.float().cpu().numpy().astype(np.float64), 1) <= 1e-2
+    assert np.max(np.abs(got[1] - lse2.cpu().numpy())) <= 1e-4
