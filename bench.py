@@ -333,6 +333,12 @@ def run_ours(args):
             "traffic": None,
             "fwd_tflops": round(fl_fwd / t_fwd / 1e12, 1),
             "phase_ms": {"index": round(ph[0], 3), "fwd": round(ph[1], 3), "bwd": round(ph[2], 3)}}
+    if W == 1:
+        # live share of the backward block pass's 128-key MMA rows:
+        # "achieved" counts algorithmic FLOPs; the block pass executes 1/occupancy of them
+        from paper_2510_18830_b200 import balance
+        occ = balance.bwd_slot_occupancy(is_, S // 64)
+        roof["bwd_block_slot_occupancy"] = round(occ["occupancy"], 4)
     tr = ROOT / "profiles" / "traffic.json"
     if tr.exists():
         try:

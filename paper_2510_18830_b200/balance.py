@@ -132,6 +132,28 @@ def analyse_csr(ptr, idx, S: int, W: int, layout: str, held: np.ndarray | None =
             "pairs_by_step": P.tolist()}
 
 
+def bwd_slot_occupancy(i_s, nb: int) -> dict:
+    """Share of the backward block pass's 128-key rows that are live (single GPU).
+
+    The key-major backward tile holds key blocks (k, k + 1), k even, and walks the
+    query blocks g that attend either (g - k in O or g - k - 1 in O, O = i_s[h]); every
+    chunk computes all 128 key rows, so a query block attending only one of the two
+    wastes half the chunk's MMA rows.  Returns chunks, live slots and live / (2 chunks)
+    summed over heads.  Counting: a value x contributes one chunk per even k with
+    k + x < nb, i.e. ceil((nb - x) / 2) of them."""
+    chunks = live = 0
+    for offs in i_s:
+        O = np.unique(np.asarray(offs, dtype=np.int64))
+        O = O[(O >= 0) & (O < nb)]
+        U = np.union1d(O, O + 1)
+        U = U[U < nb]
+        n_even = lambda x: np.maximum(0, (nb - x + 1) // 2)  # even k in [0, nb - x)
+        chunks += int(n_even(U).sum())
+        live += int(n_even(O).sum() + np.maximum(0, (nb - O) // 2).sum())
+    return {"chunks": chunks, "live_slots": live,
+            "occupancy": live / (2 * chunks) if chunks else 1.0}
+
+
 def pairs_by_step(M: np.ndarray, held: np.ndarray) -> np.ndarray:
     """[rank][step] from [rank][origin] and a schedule held[t][r] = origin."""
     W = M.shape[0]

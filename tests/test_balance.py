@@ -104,3 +104,22 @@ def test_block_index_pairs_match_bruteforce_mask(layout):
             for b in range(W):
                 ref[a, b] += mask[np.ix_(own == a, own == b)].sum()
     assert np.array_equal(M, ref)
+
+
+def test_bwd_slot_occupancy_matches_enumeration():
+    """Brute force over the tiles (k, k + 1), k even, and query blocks g."""
+    rng = np.random.default_rng(11)
+    for nb in (17, 32):
+        i_s = [np.unique(np.r_[0, rng.choice(nb, 6, replace=False)]) for _ in range(3)]
+        chunks = live = 0
+        for O in i_s:
+            Os = set(int(x) for x in O)
+            for k in range(0, nb, 2):
+                for g in range(nb):
+                    a = (g - k) in Os
+                    b = k + 1 < nb and (g - k - 1) in Os
+                    if a or b:
+                        chunks += 1
+                        live += int(a) + int(b)
+        occ = balance.bwd_slot_occupancy(i_s, nb)
+        assert (occ["chunks"], occ["live_slots"]) == (chunks, live)
