@@ -325,8 +325,10 @@ mt_status mt_block_sparse_attn_bwd(const mt_shape* shape, const void* q, const v
  * to block_scores (device fp32 [Hq][nI (nI + 1) / 2], row I at I (I + 1) / 2,
  * nI = S / 128; may be NULL); mt_xattn_index_fill then writes blk_idx (device
  * int32, capacity >= n_blk) from the selection left in the workspace.
- * The strided score GEMM is a cuBLAS bf16 GEMM (fp32 output); everything else is
- * this library's kernels.  Errors: MT_ESHAPE, MT_EWINDOW (S % 128), MT_EUNSUPPORTED
+ * The strided score GEMM is a cuBLAS bf16 GEMM (fp32 output) that runs in a 32 MiB
+ * slice of the caller's workspace; everything else is this library's kernels.  The
+ * process-wide cuBLAS handle (created on first use) holds cuBLAS's own small
+ * internal state, the one allocation outside caller workspaces.  Errors: MT_ESHAPE, MT_EWINDOW (S % 128), MT_EUNSUPPORTED
  * (block/stride other than 128/16), MT_EWORKSPACE, MT_ECAPACITY, MT_ECUDA. */
 typedef struct {
   int block;       /* 128 */

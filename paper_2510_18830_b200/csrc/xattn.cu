@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kSt = 16, kB = 128, kR = kB / kSt;  // 8 stride rows per block
 constexpr int kD = 128, kWide = kSt * kD;         // 2048
+constexpr size_t kGemmWs = size_t(32) << 20;      // cuBLAS workspace slice
 
 // dst[i][s * 128 + c] = src[(i st + (rev ? st-1-s : s)) * H + h][c], 16 B per thread
 __global__ void reshape_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
@@ -233,6 +234,7 @@ struct XWs {
   int64_t *cnt, *scan;
   void* cub_tmp;
   size_t cub_bytes;
+  void* gemm_ws;   // cuBLAS workspace (cublasSetWorkspace): no allocation inside the GEMM
   int64_t R;  // stride rows per GEMM chunk
   size_t total;
 };
@@ -273,6 +275,7 @@ XWs carve(void* base, const mt_shape* sh) {
                                 Hq * nb + 1);
   w.cub_bytes = a > b ? a : b;
   w.cub_tmp = take(w.cub_bytes);
+  w.gemm_ws = take(kGemmWs);
   w.total = o;
   return w;
 }
@@ -319,7 +322,9 @@ extern "C" mt_status mt_xattn_index_count(const mt_shape* sh, const mt_xattn_par
   const int64_t T = nI * (nI + 1) / 2;
   cublasHandle_t hb = handle();
   if (!hb) return fail(MT_ECUDA, "cublasCreate failed");
-  if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return fail(MT_ECUDA, "cublasSetStream failed");
+  if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetWorkspace(hb, w.gemm_ws, kGemmWs) != CUBLAS_STATUS_SUCCESS)
+    return fail(MT_ECUDA, "cublasSetStream/SetWorkspace failed");
   const float alpha = 1.f / (kSt * sqrtf((float)kD)), beta = 0.f;
   const int rgrid = 148 * 8;
   for (int h = 0; h < Hq; ++h) {
