@@ -79,15 +79,25 @@ extern "C" mt_status mt_comm_create(const uint8_t id[128], int world, int rank, 
   if (const char* e = getenv("MT_EMU_INTER_GBPS")) c->emu_gbps = atof(e);
   c->emu_node = getenv("MT_EMU_NODE") ? atoi(getenv("MT_EMU_NODE")) : inner;
   if (c->emu_node <= 0) c->emu_node = world;
+  if (const char* e = getenv("MT_RING_RESERVE_SMS")) c->reserve_sms = atoi(e);
+  if (const char* e = getenv("MT_RING_RESERVE_SMS_BWD")) c->reserve_sms_bwd = atoi(e);
+  if (c->reserve_sms < 0 || c->reserve_sms > 32) c->reserve_sms = 0;
+  if (c->reserve_sms_bwd < 0 || c->reserve_sms_bwd > 32) c->reserve_sms_bwd = 0;
   ncclUniqueId u;
   memcpy(&u, id, 128);
-  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  const int cap = c->reserve_sms > c->reserve_sms_bwd ? c->reserve_sms : c->reserve_sms_bwd;
+  if (cap > 0) {
+    cfg.minCTAs = 1;
+    cfg.maxCTAs = cap;
+  }
+  ncclResult_t r = ncclCommInitRankConfig(&c->nccl, world, u, rank, &cfg);
   if (r != ncclSuccess) {
     delete c;
-    return fail(MT_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    return fail(MT_ENCCL, "ncclCommInitRankConfig: %s", ncclGetErrorString(r));
   }
-  if (ncclCommSplit(c->nccl, 0, rank, &c->nccl2, nullptr) != ncclSuccess ||
-      ncclCommSplit(c->nccl, 0, rank, &c->nccl3, nullptr) != ncclSuccess) {
+  if (ncclCommSplit(c->nccl, 0, rank, &c->nccl2, &cfg) != ncclSuccess ||
+      ncclCommSplit(c->nccl, 0, rank, &c->nccl3, &cfg) != ncclSuccess) {
     ncclCommDestroy(c->nccl);
     delete c;
     return fail(MT_ENCCL, "ncclCommSplit failed");

@@ -36,6 +36,13 @@ struct mt_comm {
   // bytes / emu_gbps on their comm stream (a host function: no SM is taken).
   double emu_gbps = 0.0;  // 0 = off
   int emu_node = 0;       // ranks per emulated node
+  // SMs left free by the ring's forward / backward attention launches so the NCCL
+  // kernels (capped at max(reserve_sms, reserve_sms_bwd) CTAs when either is set)
+  // find an SM: the persistent attention kernels hold one CTA per SM for a whole
+  // step, and a transfer that cannot start until the step ends delays the next
+  // step (env MT_RING_RESERVE_SMS / MT_RING_RESERVE_SMS_BWD; 0 = off).
+  int reserve_sms = 0;
+  int reserve_sms_bwd = 0;
 };
 
 namespace mt {

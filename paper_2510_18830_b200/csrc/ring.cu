@@ -143,6 +143,12 @@ extern "C" size_t mt_ring_attn_workspace_bytes(const mt_shape* sh, int world, in
 namespace mt {
 namespace {
 #ifdef MT_HAVE_NCCL
+// SMs for the ring's attention launches: all but the ones kept free for NCCL.
+int ring_sms(const mt_comm* c, bool bwd) {
+  const int n = device_num_sms() - (c->world > 1 ? (bwd ? c->reserve_sms_bwd : c->reserve_sms) : 0);
+  return n > 0 ? n : 1;
+}
+
 // KV rotation shared by the forward and backward rings.  Buffers: the caller's
 // chunk, two inner buffers (alternating receive targets of the node ring) and
 // two outer buffers (alternating receive targets of the outer ring).  The chunk
@@ -262,7 +268,7 @@ extern "C" mt_status mt_ring_attn_fwd(mt_comm* comm, const mt_shape* sh, const v
     MT_TRY(ring.post(t, stream));
     prof_mark(comm, 0, t, RingProfile::kCompB, stream);
     MT_TRY(attn_fwd_step(plan, r, sched[t][r], nloc, q_loc, ring.curK, ring.curV, o_loc, w.o_acc,
-                         lse_loc, t == 0, t == W - 1, device_num_sms(), stream));
+                         lse_loc, t == 0, t == W - 1, ring_sms(comm, false), stream));
     prof_mark(comm, 0, t, RingProfile::kCompE, stream);
     ring.advance(t, stream);
   }
@@ -329,7 +335,7 @@ extern "C" mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* sh, const v
     }
     prof_mark(comm, 1, t, RingProfile::kCompB, stream);
     MT_TRY(attn_bwd_step(plan, r, s, nloc, q_loc, ring.curK, ring.curV, dO_loc, lse_loc, w.D,
-                         w.dq, dk, dk + nkv, device_num_sms(), stream));
+                         w.dq, dk, dk + nkv, ring_sms(comm, true), stream));
     prof_mark(comm, 1, t, RingProfile::kCompE, stream);
     // partial of the held chunk -> its owner; my own chunk's partial <- its holder
     if (s != r || holder != r) {
