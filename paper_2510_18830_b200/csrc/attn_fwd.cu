@@ -35,7 +35,13 @@ namespace mt {
 
 namespace fwd {
 
-constexpr int kKSt = 2, kVSt = 3;  // V lives ~2 chunks longer than K (O^T lags S^T)
+#ifndef MT_FWD_KST
+#define MT_FWD_KST 2
+#endif
+#ifndef MT_FWD_VST
+#define MT_FWD_VST 3
+#endif
+constexpr int kKSt = MT_FWD_KST, kVSt = MT_FWD_VST;  // V lives ~2 chunks longer than K (O^T lags S^T)
 constexpr int kThreads = 384;  // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr int kSoftmax = 256;
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB

@@ -16,8 +16,11 @@ S = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 524288
 q, k, v = make_qkv(S, 16, 2, seed=0)
 t = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).cuda()
 qd, kd, vd = t(q), t(k), t(v)
+idx = ops.build_vs_index(qd, kd, 0.9, 0.9)
+if "--bars" in sys.argv:  # the bench index's bars only (slash part reduced to the diagonal)
+    iv, _ = idx.to_lists()
+    idx = ops.VSIndex.from_lists(iv, [np.array([0], np.int32)] * 16, S)
 for _ in range(2):
-    idx = ops.build_vs_index(qd, kd, 0.9, 0.9)
     o, lse = ops.sparse_attn_fwd(qd, kd, vd, idx)
 torch.cuda.synchronize()
 buf = np.zeros((8, 4096), dtype=np.int64)
