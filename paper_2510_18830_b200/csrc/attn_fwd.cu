@@ -49,20 +49,22 @@ constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB
 constexpr float kOverflow = 64.f;            // log2 headroom before the stabiliser moves
 
-enum : int { kBlk = 0, kBar = 1, kEnd = 2, kDone = 3 };
+// kBarP: a bar chunk of 128 consecutive packed rows (TMA), live rows in `mask`
+enum : int { kBlk = 0, kBar = 1, kEnd = 2, kDone = 3, kBarP = 4 };
 
 struct alignas(16) ChunkMeta {  // per K slot: what the MMA / softmax need
   int kind;
   int n;           // kBar: live rows
   uint32_t flags;  // kBlk: bit0 rows 64..127 live, bit1 rows 0..63 diagonal, bit2 rows 64..127 diagonal
   int tile;        // kEnd: the tile it closes
+  uint32_t mask[4];  // kBarP: live rows (not covered by a selected slash, inside the prefix)
 };
 
 struct alignas(16) VMeta {  // per data chunk: what the producers need to stage K/V
   int kind;
   int n;
-  int lb0, lb1;
-  int gkv;
+  int lb0, lb1;    // kBarP: lb0 = first packed row
+  int gkv;         // kBarP: the q head (packed rows are per q head)
   int pad[3];
   int rows[128];   // kBar local rows
 };
@@ -75,6 +77,7 @@ struct SMeta {
   uint32_t flags;
   int tile;
   int seq;  // data chunk index (timeline probe)
+  uint32_t mask[4];  // kBarP live rows
 };
 
 struct Smem {
@@ -122,6 +125,7 @@ struct Params {
   int* fix_list;
   int* tile_counter;  // dynamic tile scheduler (zeroed before the launch)
   int order;          // tile order (MT_FWD_ORDER): 1 head-major (default; L2 reuse of K/V), 0 query-block-major
+  int packed;         // bar chunks from the packed rows (plan.kp / vp) by TMA (MT_FWD_PACK, default 1)
 };
 
 constexpr uint32_t kColO = 0, kColS = 64;  // TMEM: O^T [0,64), S^T buffers [64,128) [128,192)
@@ -144,7 +148,7 @@ __device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h, i
 // the next K.  K slots (and the per-chunk meta the MMA reads) are indexed by
 // every chunk including END markers; V slots only by data chunks.
 __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
-                           const CUtensorMap* tmk) {
+                           const CUtensorMap* tmk, const CUtensorMap* tmkp) {
   const int lane = lane_id();
   const VSPlan& pl = P.plan;
   const int W = pl.W;
@@ -280,6 +284,47 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
       auto covered = [&](int o) {
         return bits_smem ? ((sm.sbits[o >> 5] >> (o & 31)) & 1u) != 0u : plan_has_slash(pl, h, o);
       };
+      if (P.packed && ve - vb <= pl.pcap) {
+        // packed path: the head's columns of origin s are packed rows 0 .. ve-vb-1; the
+        // columns of blocks < g are a prefix; chunk = 128 consecutive rows (TMA), rows
+        // covered by a selected slash masked out (all-masked chunks are skipped)
+        for (int i0 = 0; vb + i0 < ve; i0 += 128) {
+          uint32_t msk[4];
+          bool past = false;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int i = vb + i0 + 32 * w + lane;
+            const int m = i < ve ? vc[i] : INT_MAX;
+            const bool in = (m >> 6) < g;
+            msk[w] = __ballot_sync(0xffffffffu, in && !covered(g - (m >> 6)));
+            past |= __ballot_sync(0xffffffffu, in) != 0xffffffffu;
+          }
+          if (msk[0] | msk[1] | msk[2] | msk[3]) {
+            VMeta& vm = vmacquire();
+            kacquire();
+            if (lane == 0) {
+              vm.kind = kBarP;
+              vm.lb0 = i0;
+              vm.gkv = h;
+              const uint32_t ks = c % kKSt;
+              ChunkMeta& m = sm.meta[ks];
+              m.kind = kBarP;
+              m.n = 128;
+#pragma unroll
+              for (int w = 0; w < 4; ++w) m.mask[w] = msk[w];
+              const uint32_t kb = smem_u32(&sm.kfull[ks]);
+              mbar_expect_tx(kb, kTileKV);
+              for (int cc = 0; cc < 2; ++cc)
+                for (int x = 0; x < 2; ++x)
+                  tma_load_3d(smem_u32(sm.k[ks] + cc * 16384 + x * 8192), tmkp, kb, cc * 64, h,
+                              i0 + 64 * x);
+            }
+            vmrelease();
+            ++c;
+          }
+          if (past) break;
+        }
+      } else {
       auto emit = [&](int n) {
         VMeta& vm = vmacquire();
         kacquire();
@@ -338,6 +383,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         if (!__any_sync(0xffffffffu, more)) break;
       }
       if (nst > 0) emit(nst);
+      }
     }
     // ---- END (K slot + meta only)
     kacquire();
@@ -400,7 +446,8 @@ __device__ void k_gatherer(Smem& sm, const Params& P) {
   }
 }
 
-__device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
+__device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv,
+                           const CUtensorMap* tmvp) {
   const int lane = lane_id();
   const VSPlan& pl = P.plan;
   for (uint32_t dv = 0;; ++dv) {
@@ -421,6 +468,14 @@ __device__ void producer_v(Smem& sm, const Params& P, const CUtensorMap* tmv) {
           for (int x = 0; x < 2; ++x)
             tma_load_3d(smem_u32(sm.v[vs] + cc * 16384 + x * 8192), tmv, vb, cc * 64, vm.gkv,
                         (x ? vm.lb1 : vm.lb0) * 64);
+      }
+    } else if (kind == kBarP) {
+      if (lane == 0) {
+        mbar_expect_tx(vb, kTileKV);
+        for (int cc = 0; cc < 2; ++cc)
+          for (int x = 0; x < 2; ++x)
+            tma_load_3d(smem_u32(sm.v[vs] + cc * 16384 + x * 8192), tmvp, vb, cc * 64, vm.gkv,
+                        vm.lb0 + 64 * x);
       }
     } else {
       const uint32_t vbase = smem_u32(sm.v[vs]);
@@ -549,6 +604,8 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         sm.smeta[b].kind = kind;
         sm.smeta[b].n = sm.meta[ks].n;
         sm.smeta[b].flags = sm.meta[ks].flags;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) sm.smeta[b].mask[w] = sm.meta[ks].mask[w];
         mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
         const uint64_t dk = sdesc_add(dk0, ks * kTileKV);
         const uint32_t ts = tmem + kColS + 64 * b;
@@ -651,6 +708,9 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
       if (cm.kind == kBlk) {
         live = row < 64 || (cm.flags & 1u);
         diag = (row < 64) ? (cm.flags & 2u) : (cm.flags & 4u);
+      } else if (cm.kind == kBarP) {
+        live = (cm.mask[row >> 5] >> (row & 31)) & 1u;
+        diag = false;
       } else {
         live = row < cm.n;
         diag = false;
@@ -839,7 +899,9 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
-                    const __grid_constant__ CUtensorMap tmv) {
+                    const __grid_constant__ CUtensorMap tmv,
+                    const __grid_constant__ CUtensorMap tmkp,
+                    const __grid_constant__ CUtensorMap tmvp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // dynamic shared memory starts 1024-aligned (no static __shared__ in this kernel);
   // using it directly keeps LDS/STS (not generic) addressing for every Smem field
@@ -880,6 +942,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmq);
     tma_prefetch_desc(&tmk);
     tma_prefetch_desc(&tmv);
+    if (P.packed) {
+      tma_prefetch_desc(&tmkp);
+      tma_prefetch_desc(&tmvp);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -888,9 +954,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
     if (warp == 0) {
-      producer_k(sm, P, &tmq, &tmk);
+      producer_k(sm, P, &tmq, &tmk, &tmkp);
     } else if (warp == 2) {
-      producer_v(sm, P, &tmv);
+      producer_v(sm, P, &tmv, &tmvp);
     } else if (warp == 1) {
       mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
     } else {
@@ -1008,6 +1074,34 @@ __global__ void __launch_bounds__(256) attn_fwd_fixup(const __grid_constant__ Pa
   }
 }
 
+// Packed vertical rows of origin s (VSPlan.kp / vp): row i of q head h = the held
+// chunk's K / V row of the head's i-th column of that origin; rows up to the next
+// multiple of 128 zero-filled.  Heads with more than pcap columns are skipped (their
+// bar chunks use the gather path).  One thread per 16 B of a row's K or V.
+__global__ void pack_bars_kernel(VSPlan pl, int s, const __nv_bfloat16* __restrict__ k,
+                                 const __nv_bfloat16* __restrict__ v) {
+  const int h = blockIdx.y;
+  const int W = pl.W, grp = pl.Hq / pl.Hkv;
+  const int vb = pl.vptr[h * (W + 1) + s], ve = pl.vptr[h * (W + 1) + s + 1];
+  const int n = ve - vb;
+  if (n > pl.pcap) return;
+  const int nr = (n + 127) / 128 * 128;
+  const int32_t* vc = pl.vcol + (int64_t)h * pl.S + vb;
+  uint4* kp = static_cast<uint4*>(pl.kp);
+  uint4* vp = static_cast<uint4*>(pl.vp);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nr * 32; t += gridDim.x * blockDim.x) {
+    const int i = t >> 5, part = t & 31, c16 = part & 15;
+    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+    if (i < n) {
+      const int m = vc[i];
+      const int64_t lrow = (int64_t)(((m >> 6) - s) / W) * 64 + (m & 63);
+      const __nv_bfloat16* src = (part < 16 ? k : v) + (lrow * pl.Hkv + h / grp) * 128;
+      val = reinterpret_cast<const uint4*>(src)[c16];
+    }
+    (part < 16 ? kp : vp)[((int64_t)i * pl.Hq + h) * 16 + c16] = val;
+  }
+}
+
 }  // namespace fwd
 
 size_t fwd_smem_bytes() { return sizeof(fwd::Smem); }  // the dynamic base is 1024-aligned
@@ -1036,12 +1130,24 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   static const int ord = getenv("MT_FWD_ORDER") ? atoi(getenv("MT_FWD_ORDER")) : 1;
   P.order = ord;
   P.fix_list = plan.scratch + 16;
+  static const int pack = getenv("MT_FWD_PACK") ? atoi(getenv("MT_FWD_PACK")) : 1;
+  P.packed = pack && plan.kp && plan.pcap > 0;
   const uint64_t S_loc = (uint64_t)nloc * 64;
-  CUtensorMap tmq, tmk, tmv;
+  CUtensorMap tmq, tmk, tmv, tmkp, tmvp;
   if (make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmk, k, 128, plan.Hkv, S_loc, 64, 1, 64) ||
       make_tmap_bf16_3d(&tmv, v, 128, plan.Hkv, S_loc, 64, 1, 64))
     return fail(MT_ECUDA, "cuTensorMapEncodeTiled failed");
+  tmkp = tmk;
+  tmvp = tmv;
+  if (P.packed) {
+    if (make_tmap_bf16_3d(&tmkp, plan.kp, 128, plan.Hq, plan.pcap, 64, 1, 64) ||
+        make_tmap_bf16_3d(&tmvp, plan.vp, 128, plan.Hq, plan.pcap, 64, 1, 64))
+      return fail(MT_ECUDA, "cuTensorMapEncodeTiled (packed) failed");
+    pack_bars_kernel<<<dim3(16, plan.Hq), 256, 0, st>>>(plan, s, static_cast<const __nv_bfloat16*>(k),
+                                                        static_cast<const __nv_bfloat16*>(v));
+    MT_TRY(check_launch("pack_bars_kernel"));
+  }
   const size_t smem = fwd_smem_bytes();
   static bool attr_done = false;
   if (!attr_done) {
@@ -1052,7 +1158,7 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   }
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   cudaMemsetAsync(P.fix_count, 0, 2 * sizeof(int), st);  // fix-up count, tile counter
-  if (grid > 0) attn_fwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv);
+  if (grid > 0) attn_fwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv, tmkp, tmvp);
   MT_TRY(check_launch("attn_fwd_kernel"));
   attn_fwd_fixup<<<num_sms, 256, 0, st>>>(P, static_cast<const __nv_bfloat16*>(q));
   return check_launch("attn_fwd_fixup");

@@ -35,6 +35,13 @@ struct VSPlan {
   const int64_t* tptr;  // [Hq * npairs + 1] segment offsets (backward only)
   const int32_t* tidx;  // per (head, key pair p): (g << 1 | kb - 2p) ascending
   int npairs;           // ceil(nb / 2)
+  // Packed vertical rows for the forward (bar chunks as TMA tile loads): per step,
+  // the held chunk's K / V rows of each head's vertical list of that origin, row i of
+  // head h at [i][h][128] bf16 (rows up to the next multiple of 128 zero-filled).
+  // Heads with more than pcap columns of one origin use the cp.async gather path.
+  void* kp;
+  void* vp;
+  int pcap;             // packed rows per head (multiple of 128; 0 = no packing)
 };
 
 __device__ __forceinline__ bool plan_has_slash(const VSPlan& p, int h, int o) {

@@ -78,6 +78,14 @@ __global__ void __launch_bounds__(kThreads) vs_plan_kernel(VSPlan p, const int32
 
 }  // namespace
 
+// Packed-row capacity per head (forward bar chunks): the origin's columns, at most
+// 16384, rounded to whole 128-row chunks.
+int packed_cap(int64_t S, int W) {
+  int64_t c = S / W;
+  if (c > 16384) c = 16384;
+  return (int)((c + 127) / 128 * 128);
+}
+
 size_t vs_plan_bytes(int64_t S, int Hq, int W) {
   const int nb = (int)(S / 64);
   const int words = (nb + 31) / 32;
@@ -89,6 +97,8 @@ size_t vs_plan_bytes(int64_t S, int Hq, int W) {
   b += (size_t)Hq * S * 4;
   b = (b + 255) & ~size_t(255);
   b += (size_t)(16 + (int64_t)Hq * nb) * 4;  // scratch
+  b = (b + 255) & ~size_t(255);
+  b += 2 * (size_t)packed_cap(S, W) * Hq * 128 * 2;  // packed vertical K / V rows
   return (b + 255) & ~size_t(255);
 }
 
@@ -106,6 +116,10 @@ mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const in
   int32_t* vcol = reinterpret_cast<int32_t*>(p + off);
   off = (off + (size_t)Hq * S * 4 + 255) & ~size_t(255);
   int32_t* scratch = reinterpret_cast<int32_t*>(p + off);
+  off = (off + (size_t)(16 + (int64_t)Hq * nb) * 4 + 255) & ~size_t(255);
+  const int pcap = packed_cap(S, W);
+  void* kp = p + off;
+  void* vp = p + off + (size_t)pcap * Hq * 128 * 2;
   VSPlan pl{};
   pl.S = S;
   pl.Hq = Hq;
@@ -120,6 +134,9 @@ mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const in
   pl.vptr = vptr;
   pl.vcol = vcol;
   pl.scratch = scratch;
+  pl.kp = kp;
+  pl.vp = vp;
+  pl.pcap = pcap;
   vs_plan_kernel<<<Hq, kThreads, 0, st>>>(pl, v_cnt, v_idx, v_stride, bits, vptr, vcol);
   MT_TRY(check_launch("vs_plan_kernel"));
   *out = pl;
