@@ -362,7 +362,7 @@ def run_ours(args):
                           if os.environ.get("MT_EMU_INTER_GBPS") else {})},
             "roofline": roof, "e2e": e2e, "clocks": clk,
             **({"ring": ring} if ring else {}),
-            "gpu_launches": args.steps * (18 if W == 1 else 17 + 7 * W)}
+            "gpu_launches": args.steps * (19 if W == 1 else 18 + 7 * W)}
     if rank == 0 and W == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {kk: vv for kk, vv in oracle_sample(q, k, v, dO, p, S, Hq, Hkv).items()
                                 if kk != "seconds"}

@@ -427,7 +427,7 @@ __device__ void k_gatherer(Smem& sm, const Params& P) {
   const int Hkv = P.plan.Hkv;
   for (uint32_t n = 0;; ++n) {
     const uint32_t gi = n & 1;
-    mbar_wait(smem_u32(&sm.gqfull[gi]), (n >> 1) & 1);
+    mbar_wait_idle(smem_u32(&sm.gqfull[gi]), (n >> 1) & 1);
     const int ks = sm.greq[gi].ks, gkv = sm.greq[gi].gkv;
     if (ks < 0) break;
     const uint32_t kbase = smem_u32(sm.k[ks]);

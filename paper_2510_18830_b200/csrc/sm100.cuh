@@ -120,6 +120,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
   }
 }
+// Unbounded wait for a warp that may legitimately idle for a whole launch (the
+// forward's K gatherer when every bar chunk goes through the packed TMA path): the
+// bounded mbar_wait would trap once a launch runs longer than its timeout (large S,
+// or a kernel slowed down by a profiler).  Backs off with nanosleep while idle.
+__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(256);
+}
 // cp.async (LDGSTS) completion -> mbarrier arrive (non-counting variant: the
 // arrive counts toward the barrier's expected arrivals).
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
