@@ -352,7 +352,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded RoPE vertical-slash generator, DESIGN.md §3)",
-            "config": {"workload": f"C4-shape layer at W={W}: S={S}, Hq={Hq}, Hkv={Hkv}, d=128, "
+            "config": {"workload": f"{ {4096: 'C1', 65536: 'C2', 131072: 'C3', 524288: 'C4', 1048576: 'C5'}.get(S, 'custom') }-shape layer at W={W}: S={S}, Hq={Hq}, Hkv={Hkv}, d=128, "
                                    f"p_v=p_s={p}, {'flat' if not args.inner or args.inner == W else f'{W // args.inner}x{args.inner}'} ring",
                        "seq_len": S, "global_batch": 1, "parallelism": f"cp{W}",
                        "density": round(dens, 4), "activated_pairs": pairs,
@@ -362,7 +362,7 @@ def run_ours(args):
                           if os.environ.get("MT_EMU_INTER_GBPS") else {})},
             "roofline": roof, "e2e": e2e, "clocks": clk,
             **({"ring": ring} if ring else {}),
-            "gpu_launches": args.steps * (19 if W == 1 else 18 + 7 * W)}
+            "gpu_launches": args.steps * (17 if W == 1 else 16 + 7 * W)}
     if rank == 0 and W == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {kk: vv for kk, vv in oracle_sample(q, k, v, dO, p, S, Hq, Hkv).items()
                                 if kk != "seconds"}

@@ -8,12 +8,15 @@
 //                  (no MUFU ex2, no FMA contraction); E = sum floor(e 2^31) (uint64)
 //   stage3  I5-I6  w = floor(RN(e / l) 2^32); V_m = sum_i w; P_kb = sum_{m in kb} V_m;
 //                  sort keys (score desc, index asc) packed into uint64
-//   select  I7-I8  segmented radix sort, exact integer top-p, forced members,
+//   select  I7-I8  one radix sort of every head's keys (head id in the top key
+//                  bits, so each head's keys come out contiguous and in (score
+//                  desc, index asc) order), exact integer top-p, forced members,
 //                  ascending compaction -> i_v, i_s
 // The window scoring is deliberately on CUDA cores in fp32: the tensor cores'
 // accumulation order is unspecified, which would break bit-exactness
 // ("what differs from the paper").
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "vsidx.cuh"
@@ -24,8 +27,25 @@ namespace vsi {
 
 constexpr int kThreads = 256;   // keys per CTA in stages 1-3
 constexpr int kRG = 8;          // window rows per register group
-constexpr int kIdxBits = 22;    // S <= 4M
-constexpr int kScoreBits = 40;  // scores < 2^39
+constexpr int kScoreBits = 39;  // V_m, P_kb <= 64 * 2^32 * (1 + 2^-9) < 2^39
+
+// Sort-key layout: key = (h << (kScoreBits + ib)) | ((2^39 - 1 - score) << ib) | index,
+// ib = bits of the largest index; hb = head bits, 0 when they do not fit in 64 bits
+// (then each head is sorted on its own).
+struct KeyLayout {
+  int ib, hb;
+};
+__host__ __device__ inline int bits_for(int64_t n) {  // bits of the values 0..n-1, >= 1
+  int b = 1;
+  while ((1LL << b) < n) ++b;
+  return b;
+}
+inline KeyLayout key_layout(int64_t n, int Hq) {
+  // MT_VS_SORT_PER_HEAD=1 forces the per-head sorts (the equality test of both paths)
+  static const bool per_head = getenv("MT_VS_SORT_PER_HEAD") && atoi(getenv("MT_VS_SORT_PER_HEAD"));
+  const int ib = bits_for(n), hb = bits_for(Hq);
+  return {ib, !per_head && kScoreBits + ib + hb <= 64 ? hb : 0};
+}
 
 __constant__ uint32_t kExp2CoefBits[8] = {0x3F800000u, 0x3F317218u, 0x3E75FDF0u, 0x3D635847u,
                                           0x3C1D955Bu, 0x3AAEC3FFu, 0x39218489u, 0x377FE5FEu};
@@ -179,11 +199,12 @@ __global__ void __launch_bounds__(kThreads) stage2_exp(Geo g, float* t, const fl
 }
 
 // ---------------------------------------------------------------- stage 3
-// V_m, P_kb, packed sort keys: key = ((2^40 - 1 - score) << 22) | index.
+// V_m, P_kb, packed sort keys (KeyLayout above).
 __global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
                                                           const unsigned long long* E,
                                                           uint64_t* keysV, uint64_t* keysP,
-                                                          uint64_t* colV, uint64_t* blkP) {
+                                                          uint64_t* colV, uint64_t* blkP,
+                                                          KeyLayout kv, KeyLayout kp) {
   __shared__ float l_s[64];
   __shared__ uint64_t half[kThreads / 32];
   const int h = blockIdx.y;
@@ -209,7 +230,8 @@ __global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
   const uint64_t smax = (1ull << kScoreBits) - 1;
   if (in) {
     const int64_t mg = global_col(g, m);
-    keysV[(size_t)h * g.S_loc + m] = ((smax - V) << kIdxBits) | (uint64_t)mg;
+    const uint64_t hk = kv.hb ? (uint64_t)h << (kScoreBits + kv.ib) : 0ull;
+    keysV[(size_t)h * g.S_loc + m] = hk | ((smax - V) << kv.ib) | (uint64_t)mg;
     if (colV) colV[(size_t)h * g.S + mg] = V;
   }
   // block sums over 64 consecutive local keys = one global block
@@ -226,7 +248,8 @@ __global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
       const int64_t kb = lb * g.W + g.r;
       const int64_t nb = g.S / 64;
       const int64_t o = nb - 1 - kb;  // slash offset scored by this block (I6, reading R1)
-      keysP[(size_t)h * (g.S_loc / 64) + lb] = ((smax - P) << kIdxBits) | (uint64_t)o;
+      const uint64_t hk = kp.hb ? (uint64_t)h << (kScoreBits + kp.ib) : 0ull;
+      keysP[(size_t)h * (g.S_loc / 64) + lb] = hk | ((smax - P) << kp.ib) | (uint64_t)o;
       if (blkP) blkP[(size_t)h * nb + o] = P;
     }
   }
@@ -238,13 +261,15 @@ __global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
 __global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const uint64_t* sortedP,
                                                    int64_t nV, int64_t nP, uint64_t pq_v,
                                                    uint64_t pq_s, uint32_t* bitsV,
-                                                   uint32_t* bitsP, int* kout) {
+                                                   uint32_t* bitsP, int* kout, int ibV,
+                                                   int ibP) {
   const int h = blockIdx.x, which = blockIdx.y;
   const int64_t n = which ? nP : nV;
   const uint64_t* keys = (which ? sortedP : sortedV) + (size_t)h * n;
   uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * ((n + 31) / 32);
   const uint64_t pq = which ? pq_s : pq_v;
   const uint64_t smax = (1ull << kScoreBits) - 1;
+  const int ib = which ? ibP : ibV;
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long tot_s;
   __shared__ long long kmin;
@@ -253,7 +278,7 @@ __global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const
   const int64_t b = tid * per, e = min(n, b + per);
   // chunk sums
   unsigned long long cs = 0;
-  for (int64_t x = b; x < e; ++x) cs += smax - (keys[x] >> kIdxBits);
+  for (int64_t x = b; x < e; ++x) cs += smax - ((keys[x] >> ib) & smax);
   // inclusive scan of chunk sums (warp + smem)
   const int lane = tid & 31, warp = tid >> 5;
   unsigned long long incl = cs;
@@ -285,7 +310,7 @@ __global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const
     const unsigned long long rhs = pq * T;
     long long found = LLONG_MAX;
     for (int64_t x = b; x < e; ++x) {
-      cum += smax - (keys[x] >> kIdxBits);
+      cum += smax - ((keys[x] >> ib) & smax);
       if ((cum << 24) >= rhs) { found = x + 1; break; }
     }
     if (found != LLONG_MAX) atomicMin(&kmin, found);
@@ -293,7 +318,7 @@ __global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const
     k = kmin;
     if (k == LLONG_MAX) k = n;
   }
-  const uint64_t imask = (1ull << kIdxBits) - 1;
+  const uint64_t imask = (1ull << ib) - 1;
   for (int64_t x = tid; x < k; x += nt) {
     const uint64_t idx = keys[x] & imask;
     atomicOr(&bits[idx >> 5], 1u << (idx & 31));
@@ -377,7 +402,6 @@ struct VSIndexWs {
   uint64_t* sortP;              // [Hq][nb]
   uint32_t* bitsV;              // [Hq][S/32]
   uint32_t* bitsP;              // [Hq][ceil(nb/32)]
-  int* segV;                    // [Hq+1]
   int* segP;                    // [Hq+1]
   __nv_bfloat16* qwin;          // [64][Hq][128]
   void* cub_tmp;
@@ -389,15 +413,16 @@ static size_t cub_sort_bytes(int Hq, int64_t n) {
   size_t b = 0;
   cub::DeviceSegmentedRadixSort::SortKeys(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                           (int)(Hq * n), Hq, (const int*)nullptr,
-                                          (const int*)nullptr, 0, vsi::kIdxBits + vsi::kScoreBits);
+                                          (const int*)nullptr, 0, 64);
   return b;
 }
-// One device-wide radix sort of n keys (the column scores of one head): a segmented
-// sort over Hq segments of S keys keeps only ~Hq CTAs busy per pass.
+// Device-wide radix sorts: all heads at once when the head id fits in the key (a
+// segmented sort over Hq segments keeps only ~Hq CTAs busy per pass; per-head sorts
+// cost ~10 launches per head, which dominates the index below ~128K tokens).
 static size_t cub_sort1_bytes(int64_t n) {
   size_t b = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)n,
-                                 0, vsi::kIdxBits + vsi::kScoreBits);
+                                 0, 64);
   return b;
 }
 
@@ -422,10 +447,10 @@ static VSIndexWs carve_vsidx(void* base, int64_t S, int Hq, int W) {
   w.sortP = (uint64_t*)take((size_t)Hq * nb * 8);
   w.bitsV = (uint32_t*)take((size_t)Hq * ((S + 31) / 32) * 4);
   w.bitsP = (uint32_t*)take((size_t)Hq * ((nb + 31) / 32) * 4);
-  w.segV = (int*)take((size_t)(Hq + 1) * 4);
   w.segP = (int*)take((size_t)(Hq + 1) * 4);
   w.qwin = (__nv_bfloat16*)take((size_t)64 * Hq * 128 * 2);
-  w.cub_bytes = std::max(cub_sort1_bytes(S), cub_sort_bytes(Hq, nb));
+  w.cub_bytes = std::max(std::max(cub_sort1_bytes((int64_t)Hq * S), cub_sort1_bytes((int64_t)Hq * nb)),
+                         cub_sort_bytes(Hq, nb));
   w.cub_tmp = take(w.cub_bytes);
   w.total = off;
   return w;
@@ -464,34 +489,48 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   MT_TRY(check_launch("vs stage2"));
   if (coll) MT_TRY(coll->allreduce_sum_u64(w.E, (size_t)Hq * 64, st));
   if (dbg_colV) cudaMemsetAsync(dbg_colV, 0, (size_t)Hq * S * 8, st);
+  const KeyLayout kv = key_layout(S, Hq), kp = key_layout(nb, Hq);
   stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, coll ? w.keysV_loc : w.keysV,
-                                           coll ? w.keysP_loc : w.keysP, dbg_colV, dbg_blkP);
+                                           coll ? w.keysP_loc : w.keysP, dbg_colV, dbg_blkP, kv,
+                                           kp);
   MT_TRY(check_launch("vs stage3"));
   if (coll) {
     MT_TRY(coll->allgather_keys(w.keysV_loc, w.keysV, Hq, S_loc, st));
     MT_TRY(coll->allgather_keys(w.keysP_loc, w.keysP, Hq, nloc, st));
   }
-  seg_offsets<<<1, 64, 0, st>>>(w.segV, Hq, S);
-  seg_offsets<<<1, 64, 0, st>>>(w.segP, Hq, nb);
   size_t tb;
-  for (int h = 0; h < Hq; ++h) {  // per head: a device-wide sort (see cub_sort1_bytes)
+  if (kv.hb) {  // one sort of every head's keys (see cub_sort1_bytes)
     tb = w.cub_bytes;
-    if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysV + (size_t)h * S,
-                                       w.sortV + (size_t)h * S, (int)S, 0, kIdxBits + kScoreBits,
-                                       st) != cudaSuccess)
+    if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysV, w.sortV, (int)(Hq * S), 0,
+                                       kScoreBits + kv.ib + kv.hb, st) != cudaSuccess)
       return fail(MT_ECUDA, "radix sort (verticals) failed");
+  } else {
+    for (int h = 0; h < Hq; ++h) {  // per head: a device-wide sort
+      tb = w.cub_bytes;
+      if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysV + (size_t)h * S,
+                                         w.sortV + (size_t)h * S, (int)S, 0, kScoreBits + kv.ib,
+                                         st) != cudaSuccess)
+        return fail(MT_ECUDA, "radix sort (verticals) failed");
+    }
   }
   tb = w.cub_bytes;
-  if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb), Hq,
-                                              w.segP, w.segP + 1, 0, kIdxBits + kScoreBits,
-                                              st) != cudaSuccess)
-    return fail(MT_ECUDA, "segmented sort (slashes) failed");
+  if (kp.hb) {
+    if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb), 0,
+                                       kScoreBits + kp.ib + kp.hb, st) != cudaSuccess)
+      return fail(MT_ECUDA, "radix sort (slashes) failed");
+  } else {
+    seg_offsets<<<1, 64, 0, st>>>(w.segP, Hq, nb);
+    if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb),
+                                                Hq, w.segP, w.segP + 1, 0, kScoreBits + kp.ib,
+                                                st) != cudaSuccess)
+      return fail(MT_ECUDA, "segmented sort (slashes) failed");
+  }
   cudaMemsetAsync(w.bitsV, 0, (size_t)Hq * ((S + 31) / 32) * 4, st);
   cudaMemsetAsync(w.bitsP, 0, (size_t)Hq * ((nb + 31) / 32) * 4, st);
   const uint64_t pq_v = (uint64_t)llrint((double)p_v * 16777216.0);
   const uint64_t pq_s = (uint64_t)llrint((double)p_s * 16777216.0);
   topp_mark<<<dim3(Hq, 2), 1024, 0, st>>>(w.sortV, w.sortP, S, nb, pq_v, pq_s, w.bitsV, w.bitsP,
-                                          nullptr);
+                                          nullptr, kv.ib, kp.ib);
   MT_TRY(check_launch("vs topp"));
   compact_bits<<<dim3(Hq, 2), 1024, 0, st>>>(w.bitsV, w.bitsP, S, nb, v_cnt, v_idx, v_stride,
                                              s_cnt, s_off, s_stride);
@@ -564,6 +603,6 @@ extern "C" mt_status mt_vs_column_scores(const mt_shape* sh, const void* q, cons
                                            w.M);
   stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
   stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, w.keysV, w.keysP, col_scores,
-                                           slash_scores);
+                                           slash_scores, key_layout(S, Hq), key_layout(S / 64, Hq));
   return check_launch("mt_vs_column_scores");
 }

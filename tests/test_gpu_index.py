@@ -65,3 +65,37 @@ def test_index_rejects_bad_p(cuda_lib):
     with pytest.raises(_lib.MTError) as e:
         ops.build_vs_index(q, q[:, :1].contiguous(), 0.0, 0.5)
     assert e.value.name == "MT_ECONFIG"
+
+
+_PER_HEAD_SCRIPT = r"""
+import sys, numpy as np, torch
+from paper_2510_18830_b200 import ops
+from synth.generator import make_qkv
+from tests.gpu_util import to_dev_bf16
+S, Hq, Hkv, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+q, k, _ = make_qkv(S, Hq, Hkv, seed=S + 7)
+iv, is_ = ops.build_vs_index(to_dev_bf16(q), to_dev_bf16(k), 0.9, 0.9).to_lists()
+np.savez(out, *(list(iv) + list(is_)))
+"""
+
+
+@pytest.mark.parametrize("S,Hq,Hkv", [(65536, 16, 2), (4096, 8, 1)])
+def test_index_sort_paths_agree(cuda_lib, tmp_path, S, Hq, Hkv):
+    """The one-sort path (head id in the key's top bits) and the per-head sorts
+    (forced by MT_VS_SORT_PER_HEAD=1, the layout used when the head bits do not fit)
+    give the same lists."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "per_head.npz")
+    env = dict(os.environ, MT_VS_SORT_PER_HEAD="1", PYTHONPATH=root)
+    subprocess.run([sys.executable, "-c", _PER_HEAD_SCRIPT, str(S), str(Hq), str(Hkv), out],
+                   check=True, env=env, cwd=root, timeout=600)
+    ref = np.load(out)
+    q, k, _ = make_qkv(S, Hq, Hkv, seed=S + 7)
+    iv, is_ = ops.build_vs_index(to_dev_bf16(q), to_dev_bf16(k), 0.9, 0.9).to_lists()
+    got = list(iv) + list(is_)
+    assert len(got) == len(ref.files)
+    for i, x in enumerate(got):
+        assert np.array_equal(x, ref[f"arr_{i}"]), i
