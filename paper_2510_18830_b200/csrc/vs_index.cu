@@ -26,7 +26,6 @@ namespace mt {
 namespace vsi {
 
 constexpr int kThreads = 256;   // keys per CTA in stages 1-3
-constexpr int kRG = 8;          // window rows per register group
 constexpr int kScoreBits = 39;  // V_m, P_kb <= 64 * 2^32 * (1 + 2^-9) < 2^39
 
 // Sort-key layout: key = (h << (kScoreBits + ib)) | ((2^39 - 1 - score) << ib) | index,
@@ -88,10 +87,16 @@ __device__ __forceinline__ uint64_t shfl_down_u64(uint64_t v, int o) {
 }
 
 // ---------------------------------------------------------------- stage 1
-// t[h][i][m] (fp32) and row max M[h][i].
-__global__ void __launch_bounds__(kThreads) stage1_scores(Geo g, const __nv_bfloat16* qwin,
-                                                          const __nv_bfloat16* k, float* t,
-                                                          float* M) {
+// t[h][i][m] (fp32) and row max M[h][i].  Thread = key m.  Each accumulator still
+// folds c = 0..127 in order (I1); the loops only tile it: 32 window rows per pass
+// (32 accumulators) x 32 k values per block in registers, ~80 registers, so three
+// CTAs (24 warps) share an SM to hide the shared-memory broadcast latency
+// (kMinBlocks = 3: 80 registers; 2: 128 registers, no spill; MT_VS_S1_MINB picks).
+constexpr int kRows = 32, kKB = 32;
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, const __nv_bfloat16* qwin,
+                                                             const __nv_bfloat16* k, float* t,
+                                                             float* M) {
   __shared__ __align__(16) float qs[64][128];
   __shared__ float wmax[kThreads / 32][64];
   const int h = blockIdx.y;
@@ -103,45 +108,43 @@ __global__ void __launch_bounds__(kThreads) stage1_scores(Geo g, const __nv_bflo
   __syncthreads();
   const int64_t m = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   const bool in = m < g.S_loc;
-  float kf[128];
-  if (in) {
-    const uint4* src = reinterpret_cast<const uint4*>(k + ((size_t)m * g.Hkv + h / grp) * 128);
-#pragma unroll
-    for (int v = 0; v < 16; ++v) {
-      uint4 u = src[v];
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        kf[v * 8 + 2 * j] = __uint_as_float(w[j] << 16);
-        kf[v * 8 + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < 128; ++c) kf[c] = 0.f;
-  }
+  const uint4* src = reinterpret_cast<const uint4*>(k + ((size_t)(in ? m : 0) * g.Hkv + h / grp) * 128);
   const int64_t mg = in ? global_col(g, m) : INT64_MAX;
   const int64_t n0 = g.S - 64;
   float* th = t + (size_t)h * 64 * g.S_loc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll 1
-  for (int i0 = 0; i0 < 64; i0 += kRG) {
-    float acc[kRG];
+  for (int i0 = 0; i0 < 64; i0 += kRows) {
+    float acc[kRows];
 #pragma unroll
-    for (int r = 0; r < kRG; ++r) acc[r] = 0.f;
+    for (int r = 0; r < kRows; ++r) acc[r] = 0.f;
+#pragma unroll 1
+    for (int cb = 0; cb < 128; cb += kKB) {
+      float kf[kKB];
 #pragma unroll
-    for (int c = 0; c < 128; c += 4) {
+      for (int v = 0; v < kKB / 8; ++v) {
+        const uint4 u = in ? src[cb / 8 + v] : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int r = 0; r < kRG; ++r) {
-        const float4 qv = *reinterpret_cast<const float4*>(&qs[i0 + r][c]);
-        acc[r] = __fmaf_rn(qv.x, kf[c], acc[r]);
-        acc[r] = __fmaf_rn(qv.y, kf[c + 1], acc[r]);
-        acc[r] = __fmaf_rn(qv.z, kf[c + 2], acc[r]);
-        acc[r] = __fmaf_rn(qv.w, kf[c + 3], acc[r]);
+        for (int j = 0; j < 4; ++j) {
+          kf[v * 8 + 2 * j] = __uint_as_float(w[j] << 16);
+          kf[v * 8 + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kKB; c += 4) {
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+          const float4 qv = *reinterpret_cast<const float4*>(&qs[i0 + r][cb + c]);
+          acc[r] = __fmaf_rn(qv.x, kf[c], acc[r]);
+          acc[r] = __fmaf_rn(qv.y, kf[c + 1], acc[r]);
+          acc[r] = __fmaf_rn(qv.z, kf[c + 2], acc[r]);
+          acc[r] = __fmaf_rn(qv.w, kf[c + 3], acc[r]);
+        }
       }
     }
 #pragma unroll
-    for (int r = 0; r < kRG; ++r) {
+    for (int r = 0; r < kRows; ++r) {
       const int i = i0 + r;
       const bool causal = mg <= n0 + i;
       const float tv = causal ? acc[r] : -INFINITY;
@@ -159,6 +162,15 @@ __global__ void __launch_bounds__(kThreads) stage1_scores(Geo g, const __nv_bflo
     for (int w = 0; w < kThreads / 32; ++w) mx = fmaxf(mx, wmax[w][threadIdx.x]);
     if (mx > -INFINITY) atomic_max_f32(&M[h * 64 + threadIdx.x], mx);
   }
+}
+
+inline void stage1_launch(dim3 grid, const Geo& g, const __nv_bfloat16* qwin,
+                          const __nv_bfloat16* k, float* t, float* M, cudaStream_t st) {
+  static const int minb = getenv("MT_VS_S1_MINB") ? atoi(getenv("MT_VS_S1_MINB")) : 3;
+  if (minb == 2)
+    stage1_scores<2><<<grid, kThreads, 0, st>>>(g, qwin, k, t, M);
+  else
+    stage1_scores<3><<<grid, kThreads, 0, st>>>(g, qwin, k, t, M);
 }
 
 // ---------------------------------------------------------------- stage 2
@@ -481,8 +493,7 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   fill_f32<<<(Hq * 64 + 255) / 256, 256, 0, st>>>(w.M, -INFINITY, Hq * 64);
   cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
   const dim3 grid((unsigned)((S_loc + kThreads - 1) / kThreads), Hq);
-  stage1_scores<<<grid, kThreads, 0, st>>>(g, w.qwin, static_cast<const __nv_bfloat16*>(k_loc),
-                                           w.t, w.M);
+  stage1_launch(grid, g, w.qwin, static_cast<const __nv_bfloat16*>(k_loc), w.t, w.M, st);
   MT_TRY(check_launch("vs stage1"));
   if (coll) MT_TRY(coll->allreduce_max(w.M, (size_t)Hq * 64, st));
   stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
@@ -599,8 +610,7 @@ extern "C" mt_status mt_vs_column_scores(const mt_shape* sh, const void* q, cons
   fill_f32<<<(Hq * 64 + 255) / 256, 256, 0, st>>>(w.M, -INFINITY, Hq * 64);
   cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
   const dim3 grid((unsigned)((S + kThreads - 1) / kThreads), Hq);
-  stage1_scores<<<grid, kThreads, 0, st>>>(g, w.qwin, static_cast<const __nv_bfloat16*>(k), w.t,
-                                           w.M);
+  stage1_launch(grid, g, w.qwin, static_cast<const __nv_bfloat16*>(k), w.t, w.M, st);
   stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
   stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, w.keysV, w.keysP, col_scores,
                                            slash_scores, key_layout(S, Hq), key_layout(S / 64, Hq));
