@@ -118,6 +118,8 @@ struct Params {
   int bar_parts;            // BAR: query-range parts per column group
   int bar_part_len;         // BAR: query blocks per part
   int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
+  int hpt;                  // BLOCK: q heads per tile (of one kv head; their dK/dV sum stays in
+                            // TMEM, so the tile's K/V load and dK/dV epilogue are shared)
 };
 
 // ---- tile decoding
@@ -137,9 +139,9 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
   const int W = pl.W;
   if (P.mode == kModeBlock) {
     const int npairs = (P.nloc + 1) / 2;
-    if (tile < 0 || tile >= pl.Hq * npairs) return T;
+    if (tile < 0 || tile >= (pl.Hq / P.hpt) * npairs) return T;
     T.ok = true;
-    T.h = tile / npairs;
+    T.h = (tile / npairs) * P.hpt;  // first q head of the tile
     T.g = T.h / (pl.Hq / pl.Hkv);
     T.lb0 = 2 * (tile % npairs);  // early key blocks (most work) first
     return T;
@@ -315,7 +317,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         // (key block kb0) is live iff x is a selected offset, slot 1 (kb0 + W) iff x - W
         // is.  32 lattice points per ballot from the slash bitmap: a scalar walk of the
         // offset list costs a dependent global load per offset and skips (W-1)/W of them.
-        const int h = T.h;
+        for (int h = T.h; h < T.h + P.hpt; ++h) {  // the tile's q heads one after another
         const uint32_t* bits = pl.s_bits + (int64_t)h * pl.bits_words;
         auto has = [&](int x) { return x >= 0 && ((bits[x >> 5] >> (x & 31)) & 1u) != 0u; };
         const int xmax = pl.nb - kb0;  // gq < nb
@@ -335,6 +337,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
             if ((bb >> l) & 1u) flags |= xs == W ? 10u : 2u;     // slot 1 live (+ diagonal)
             emit(h, (kb0 + xs - P.r) / W, flags);
           }
+        }
         }
       }
       (void)v1;
@@ -968,6 +971,15 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.static_tiles = static_tiles;
   static const int dbg = getenv("MT_BWD_DBG") ? atoi(getenv("MT_BWD_DBG")) : 0;
   P.dbg = dbg;
+  // q heads per block-pass tile: 4 by default (MT_BWD_HPT overrides), the largest divisor
+  // of the GQA group size not above it; block-CSR mode keeps one head per tile.  Measured
+  // (profiles/r01_bwd_hpt_ab.json): the K/V load and dK/dV epilogue of a tile are shared by
+  // 4 heads' chunk streams; 8 heads lose Q/dO locality in L2.
+  static const int hpt_env = getenv("MT_BWD_HPT") ? atoi(getenv("MT_BWD_HPT")) : 4;
+  const int grp = plan.Hq / plan.Hkv;
+  int hpt = hpt_env < 1 ? 1 : hpt_env;
+  while (grp % hpt) --hpt;
+  P.hpt = (plan.bptr || plan.tptr) ? 1 : hpt;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv;
   if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 32) ||
@@ -990,7 +1002,7 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);  // one tile counter per launch
   P.mode = kModeBlock;
   const int npairs = (nloc + 1) / 2;
-  P.n_tiles = plan.Hq * npairs;
+  P.n_tiles = (plan.Hq / P.hpt) * npairs;
   int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   if (grid > 0)
     attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
@@ -999,6 +1011,7 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
   P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;
+  P.hpt = 1;
   P.bar_part_len = nloc < 1024 ? (nloc > 0 ? nloc : 1) : 1024;
   P.bar_parts = (nloc + P.bar_part_len - 1) / P.bar_part_len;
   P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128) * P.bar_parts;
