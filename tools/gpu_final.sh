@@ -1,8 +1,8 @@
-# round-1 final pass on one 4-GPU box (writes gpurun_out/r01v12_*): every GPU test (incl. 2/4-GPU rings),
+# round-1 final pass on one 4-GPU box (writes gpurun_out/$TAG_*): every GPU test (incl. 2/4-GPU rings),
 # smoke, the default bench line (e2e + cpu_baseline), the reference arm, the ncu launch list, and every
 # BASELINE config (C1-C5) at 1/2/4 GPUs, flat and 2x2.
 set -x
-P=gpurun_out/r01v12
+P=gpurun_out/${TAG:-r01v13}
 timeout 1500 python -m pytest tests -m gpu -q > ${P}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > ${P}_smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > ${P}_bench.json 2> ${P}_bench.err; echo "bench rc=$?"
