@@ -9,6 +9,7 @@ timeout 900 python bench.py > ${P}_bench.json 2> ${P}_bench.err; echo "bench rc=
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > ${P}_bench_ref.json 2> ${P}_bench_ref.err; echo "ref rc=$?"
 CMD='python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline'
 timeout 300 $CMD > ${P}_plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${P}_launches.csv $CMD > ${P}_ncu_launch.log 2>&1; echo "launches rc=$?"
+CUDA_VISIBLE_DEVICES=0 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_bwd_kernel -c 1 -o ${P}_bwd_block python tools/prof_step.py --seq 524288 --reps 1 > ${P}_ncu_bwd_block.log 2>&1; echo "ncu bwd block rc=$?"
 one() {  # name, n, args...
   name=$1; n=$2; shift 2
   if [ "$n" = 1 ]; then
