@@ -1,0 +1,135 @@
+"""Out-of-bounds and uninitialised-read checks for the C ABI calls (index, forward, backward).
+
+compute-sanitizer is closed on the GPU pool, so this is the substitute: every device buffer a call
+touches (inputs, outputs, index arrays, workspace) is a view into a larger allocation whose guard
+regions before and after are filled with 0xFF bytes, and outputs and workspace start as 0xFF too
+(NaN in bf16 / fp32). After the call:
+- every guard byte is still 0xFF (no write outside the buffer the header declares, include/mtsa.h);
+- the inputs are unchanged (const pointers are not written);
+- the outputs hold no NaN (every element written, and nothing read from unwritten workspace or output);
+- the results equal the same call on ordinary buffers (the index bit for bit; attention to 1e-2 of the
+  tensor's max, since the dQ reduce-add and the dynamic tile order do not fix the fp32 summation order).
+Sizes: an odd block count (S = 37 x 64) and the C1 shape, with GQA.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2510_18830_b200 import _lib, ops
+from synth.generator import make_grad_out, make_qkv
+from tests.gpu_util import random_index, to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+
+G = 1 << 16  # guard bytes on each side (keeps the 1 KiB / 16 B alignment TMA and the kernels expect)
+
+
+class Guarded:
+    """A tensor view at byte offset G inside a 0xFF-filled allocation of nbytes + 2 G."""
+
+    def __init__(self, shape, dtype, src: torch.Tensor | None = None):
+        n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        self.n = n
+        self.base = torch.full((n + 2 * G,), 0xFF, dtype=torch.uint8, device="cuda")
+        self.t = self.base[G:G + n].view(dtype).view(*shape)
+        if src is not None:
+            self.t.copy_(src)
+        self.before = src.clone() if src is not None else None
+
+    def guards_intact(self) -> bool:
+        return bool((self.base[:G] == 0xFF).all()) and bool((self.base[G + self.n:] == 0xFF).all())
+
+
+def _case(S, Hq, Hkv, seed):
+    q, k, v = make_qkv(S, Hq, Hkv, seed=seed)
+    dO = make_grad_out(S, Hq, seed=seed + 1)
+    return tuple(to_dev_bf16(x) for x in (q, k, v, dO))
+
+
+def _guarded_index(S, Hq, src: ops.VSIndex | None = None):
+    nb = S // ops.BLOCK
+    parts = [Guarded((Hq,), torch.int32, None if src is None else src.v_cnt),
+             Guarded((Hq, S), torch.int32, None if src is None else src.v_idx),
+             Guarded((Hq,), torch.int32, None if src is None else src.s_cnt),
+             Guarded((Hq, nb), torch.int32, None if src is None else src.s_off)]
+    return parts, ops.VSIndex(*(p.t for p in parts))
+
+
+def _close(name, got, want):
+    err = (got.float() - want.float()).abs().max().item()
+    assert err <= 1e-2 * want.float().abs().max().item(), (name, err)
+
+
+def _check_all(bufs):
+    for name, b in bufs.items():
+        assert b.guards_intact(), f"write outside {name}"
+        if b.before is not None:
+            assert torch.equal(b.t, b.before), f"input {name} modified"
+
+
+@pytest.mark.parametrize("S,Hq,Hkv", [(37 * 64, 8, 1), (4096, 16, 2)])
+def test_guarded_index(cuda_lib, S, Hq, Hkv):
+    q, k, _, _ = _case(S, Hq, Hkv, seed=3)
+    ref = ops.build_vs_index(q, k, 0.9, 0.9)
+    sh = ops.shape(S, Hq, Hkv)
+    L = _lib.lib()
+    nws = L.mt_build_vs_index_workspace_bytes(ctypes.byref(sh), 1)
+    bufs = {"q": Guarded(q.shape, q.dtype, q), "k": Guarded(k.shape, k.dtype, k),
+            "ws": Guarded((nws,), torch.uint8)}
+    parts, idx = _guarded_index(S, Hq)
+    bufs.update({f"idx{i}": p for i, p in enumerate(parts)})
+    prm = ops.VSParams(0.9, 0.9)
+    ci = idx.c_struct()
+    _lib.check(L.mt_build_vs_index(None, ctypes.byref(sh), ctypes.byref(prm), bufs["q"].t.data_ptr(),
+                                   bufs["k"].t.data_ptr(), ctypes.byref(ci), bufs["ws"].t.data_ptr(), nws,
+                                   ops._stream()))
+    torch.cuda.synchronize()
+    _check_all(bufs)
+    a, b = idx.to_lists(), ref.to_lists()
+    for h in range(Hq):
+        assert np.array_equal(a[0][h], b[0][h]) and np.array_equal(a[1][h], b[1][h]), h
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,gen", [(37 * 64, 8, 1, True), (4096, 16, 2, False)])
+def test_guarded_fwd_bwd(cuda_lib, S, Hq, Hkv, gen):
+    q, k, v, dO = _case(S, Hq, Hkv, seed=5)
+    if gen:
+        ref_idx = ops.build_vs_index(q, k, 0.9, 0.9)
+    else:  # many bars and offsets, GQA
+        ref_idx = ops.VSIndex.from_lists(*random_index(S, Hq, seed=9, n_off=12, n_col=300), S)
+    o_ref, lse_ref = ops.sparse_attn_fwd(q, k, v, ref_idx)
+    g_ref = ops.sparse_attn_bwd(q, k, v, o_ref, lse_ref, dO, ref_idx)
+    torch.cuda.synchronize()
+
+    sh = ops.shape(S, Hq, Hkv)
+    L = _lib.lib()
+    parts, idx = _guarded_index(S, Hq, ref_idx)
+    ci = idx.c_struct()
+    ins = {n: Guarded(x.shape, x.dtype, x) for n, x in (("q", q), ("k", k), ("v", v), ("dO", dO))}
+    nf = L.mt_sparse_attn_fwd_workspace_bytes(ctypes.byref(sh), 1)
+    fw = {"o": Guarded(q.shape, q.dtype), "lse": Guarded((Hq, S), torch.float32),
+          "ws_fwd": Guarded((nf,), torch.uint8)}
+    p = lambda b: b.t.data_ptr()
+    _lib.check(L.mt_sparse_attn_fwd(ctypes.byref(sh), p(ins["q"]), p(ins["k"]), p(ins["v"]), ctypes.byref(ci),
+                                    p(fw["o"]), p(fw["lse"]), p(fw["ws_fwd"]), nf, ops._stream()))
+    torch.cuda.synchronize()
+    assert not torch.isnan(fw["o"].t.float()).any() and not torch.isnan(fw["lse"].t).any()
+    _close("o", fw["o"].t, o_ref)
+    assert (fw["lse"].t - lse_ref).abs().max().item() <= 1e-4
+
+    # the backward reads O / LSE from guarded buffers of their own
+    o_in, lse_in = Guarded(q.shape, q.dtype, fw["o"].t), Guarded((Hq, S), torch.float32, fw["lse"].t)
+    nb_ = L.mt_sparse_attn_bwd_workspace_bytes(ctypes.byref(sh))
+    bw = {"dq": Guarded(q.shape, q.dtype), "dk": Guarded(k.shape, k.dtype), "dv": Guarded(v.shape, v.dtype),
+          "ws_bwd": Guarded((nb_,), torch.uint8)}
+    _lib.check(L.mt_sparse_attn_bwd(ctypes.byref(sh), p(ins["q"]), p(ins["k"]), p(ins["v"]), p(o_in), p(lse_in),
+                                    p(ins["dO"]), ctypes.byref(ci), p(bw["dq"]), p(bw["dk"]), p(bw["dv"]),
+                                    p(bw["ws_bwd"]), nb_, ops._stream()))
+    torch.cuda.synchronize()
+    _check_all({**ins, **fw, **bw, "o_in": o_in, "lse_in": lse_in,
+                **{f"idx{i}": b for i, b in enumerate(parts)}})
+    for name, got, want in zip(("dq", "dk", "dv"), (bw["dq"].t, bw["dk"].t, bw["dv"].t), g_ref):
+        assert not torch.isnan(got.float()).any(), name
+        _close(name, got, want)
