@@ -133,3 +133,71 @@ def test_guarded_fwd_bwd(cuda_lib, S, Hq, Hkv, gen):
     for name, got, want in zip(("dq", "dk", "dv"), (bw["dq"].t, bw["dk"].t, bw["dv"].t), g_ref):
         assert not torch.isnan(got.float()).any(), name
         _close(name, got, want)
+
+
+def test_guarded_ring_steps(cuda_lib, monkeypatch):
+    """Every (rank, step) of a W = 4 ring emulated on one GPU (mt_attn_fwd_step, mt_attn_bwd_preprocess,
+    mt_attn_bwd_step), 9 local blocks per rank, with every buffer and each call's workspace guarded."""
+    from oracle.ring import schedule
+    from oracle.sparseformat import stripe_perm
+
+    W, S, Hq, Hkv = 4, 4 * 9 * 64, 4, 2
+    Lq = S // W
+    q, k, v, dO = _case(S, Hq, Hkv, seed=11)
+    idx = ops.VSIndex.from_lists(*random_index(S, Hq, seed=12, n_off=6, n_col=80), S)
+    wss = []
+
+    def guarded_ws(nbytes, device=None):
+        wss.append(Guarded((max(nbytes, 1),), torch.uint8))
+        return wss[-1].t
+
+    perm = stripe_perm(S, W)
+    pt = [torch.from_numpy(perm[r]).cuda() for r in range(W)]
+    sched = schedule(W)
+
+    def run(guard):
+        mk = (lambda shape, dt, src=None: Guarded(shape, dt, src)) if guard else \
+             (lambda shape, dt, src=None: type("T", (), {"t": src.clone() if src is not None else
+                                                       torch.empty(shape, dtype=dt, device="cuda")})())
+        loc = lambda x, r: mk(x[pt[r]].shape, x.dtype, x[pt[r]].contiguous())
+        bufs = {}
+        for n, x in (("q", q), ("k", k), ("v", v), ("dO", dO)):
+            for r in range(W):
+                bufs[f"{n}{r}"] = loc(x, r)
+        for r in range(W):
+            bufs[f"o{r}"] = mk((Lq, Hq, 128), torch.bfloat16)
+            bufs[f"oacc{r}"] = mk((Lq, Hq, 128), torch.float32)
+            bufs[f"lse{r}"] = mk((Hq, Lq), torch.float32)
+            bufs[f"D{r}"] = mk((Hq, Lq), torch.float32)
+            for n, h in (("dq", Hq), ("dk", Hkv), ("dv", Hkv)):
+                bufs[f"{n}{r}"] = mk((Lq, h, 128), torch.float32, torch.zeros(Lq, h, 128, device="cuda"))
+        B = lambda n: bufs[n].t
+        for t, held in enumerate(sched):
+            for r in range(W):
+                s = held[r]
+                ops.attn_fwd_step(S, W, r, s, t == 0, t == W - 1, B(f"q{r}"), B(f"k{s}"), B(f"v{s}"), idx,
+                                  B(f"o{r}"), B(f"oacc{r}"), B(f"lse{r}"))
+        for r in range(W):
+            ops.attn_bwd_preprocess(S, W, B(f"o{r}"), B(f"dO{r}"), B(f"D{r}"))
+        for held in sched:
+            for r in range(W):
+                s = held[r]
+                ops.attn_bwd_step(S, W, r, s, B(f"q{r}"), B(f"k{s}"), B(f"v{s}"), B(f"dO{r}"), B(f"lse{r}"),
+                                  B(f"D{r}"), idx, B(f"dq{r}"), B(f"dk{s}"), B(f"dv{s}"))
+        torch.cuda.synchronize()
+        return bufs
+
+    ref = run(False)
+    monkeypatch.setattr(ops, "workspace", guarded_ws)
+    got = run(True)
+    assert wss
+    for i, w in enumerate(wss):
+        assert w.guards_intact(), f"write outside workspace {i}"
+    for n, b in got.items():
+        assert b.guards_intact(), f"write outside {n}"
+        if n[:1] in "qkv" or n.startswith("dO"):
+            if b.before is not None and not n.startswith(("dq", "dk", "dv")):
+                assert torch.equal(b.t, b.before), f"input {n} modified"
+        if n.startswith(("o", "lse", "D", "dq", "dk", "dv")) and not n.startswith("oacc"):
+            assert not torch.isnan(b.t.float()).any(), n
+            _close(n, b.t, ref[n].t)
