@@ -249,3 +249,41 @@ def test_guarded_vs_format(cuda_lib):
     _check_all({"bp": bp, "cp": cp, "ws": ws, "bi": bi, "cl": cl, **{f"idx{i}": b for i, b in enumerate(parts)}})
     for got, want in zip((bp.t, bi.t, cp.t, cl.t), ref):
         assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("S", [524288, 1048576])
+def test_guarded_fullsize(cuda_lib, S):
+    """The bench configuration (C4 512K, and C5's 1M on one GPU): index, forward and backward with every
+    buffer and workspace guarded, against the same calls on ordinary buffers (large-offset arithmetic)."""
+    Hq, Hkv = 16, 2
+    q, k, v, dO = _case(S, Hq, Hkv, seed=0)
+    idx_ref = ops.build_vs_index(q, k, 0.9, 0.9)
+    o_ref, lse_ref = ops.sparse_attn_fwd(q, k, v, idx_ref)
+    g_ref = ops.sparse_attn_bwd(q, k, v, o_ref, lse_ref, dO, idx_ref)
+    torch.cuda.synchronize()
+    ins = {n: Guarded(x.shape, x.dtype, x) for n, x in (("q", q), ("k", k), ("v", v), ("dO", dO))}
+    del q, k, v, dO
+    wss = []
+    ws_plain = ops.workspace
+
+    def guarded_ws(nbytes, device=None):
+        wss.append(Guarded((max(nbytes, 1),), torch.uint8))
+        return wss[-1].t
+
+    ops.workspace = guarded_ws
+    try:
+        idx = ops.build_vs_index(ins["q"].t, ins["k"].t, 0.9, 0.9)
+        o, lse = ops.sparse_attn_fwd(ins["q"].t, ins["k"].t, ins["v"].t, idx)
+        g = ops.sparse_attn_bwd(ins["q"].t, ins["k"].t, ins["v"].t, o, lse, ins["dO"].t, idx)
+        torch.cuda.synchronize()
+    finally:
+        ops.workspace = ws_plain
+    _check_all({**ins, **{f"ws{i}": w for i, w in enumerate(wss)}})
+    for a, b in zip((idx.v_cnt, idx.v_idx, idx.s_cnt, idx.s_off), (idx_ref.v_cnt, idx_ref.v_idx, idx_ref.s_cnt,
+                                                                   idx_ref.s_off)):
+        assert torch.equal(a, b)
+    _close("o", o, o_ref)
+    assert (lse - lse_ref).abs().max().item() <= 1e-4
+    for name, got, want in zip(("dq", "dk", "dv"), g, g_ref):
+        assert not torch.isnan(got.float()).any(), name
+        _close(name, got, want)
