@@ -4,9 +4,13 @@
  * oracle/vsidx.py (window_scores, window_stats, column_and_slash_scores),
  * written out loop by loop so it can be read against PAPER.md Alg. 1
  * and DESIGN.md §2.1.  Compile with -ffp-contract=off and without fast-math:
- * every float operation below is one IEEE binary32 round-to-nearest-even op.
+ * every float operation below is one IEEE binary32 round-to-nearest-even op,
+ * except I1's fused multiply-add, written as (float)((double)acc + (double)q *
+ * (double)k): the bf16 x bf16 product is exact in double and the double sum is
+ * either exact or too far from a float rounding boundary for the second
+ * rounding to matter (R11), so it equals fmaf(q, k, acc).
  *
- *   I1 t[i,m] = fold_c RN(acc + q[i,c]*k[m,c])   (q*k of bf16 values is exact)
+ *   I1 t[i,m] = fold_c RN(acc + q[i,c]*k[m,c])   (fused: the product is not rounded)
  *   I2 M_i = max over causal m (m <= n_i = S-nq+i)
  *   I3 e = exp2s(RN(RN(t - M_i) * C_d))
  *   I4 E_i = sum floor(e * 2^31)
@@ -81,8 +85,7 @@ int vsidx_ref_column_scores(const float* q, const float* k, int64_t S, int d, in
           const float qc = q[(size_t)i * d + ch];
           const float* kc = kT + (size_t)ch * S;
           for (int64_t m = m0; m < m1; ++m) {
-            float prod = qc * kc[m];
-            ti[m] = ti[m] + prod;
+            ti[m] = (float)((double)ti[m] + (double)qc * (double)kc[m]);
           }
         }
         for (int64_t m = m0; m < m1; ++m)

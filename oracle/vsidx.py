@@ -13,6 +13,8 @@ the reading used here (VS-IDX v1, steps I1-I8), chosen so that an independent
 implementation can reach the same bits:
 
   I1 t[i,m] = fold_c RN(acc + q[n_i,c] k[m,c]), n_i = S-64+i, causal m <= n_i
+            (the product is exact, not rounded on its own: one fused multiply-add
+            per channel, IEEE 754 fusedMultiplyAdd)
   I2 M_i    = max_m t[i,m]
   I3 e      = exp2s(RN(RN(t - M_i) * C_d)),  C_d = RN(log2(e)/sqrt(d))
   I4 E_i    = sum_m floor(e * 2^31)                     (uint64, exact)
@@ -21,9 +23,12 @@ implementation can reach the same bits:
   I7 k      = min{k >= 1 : 2^24 cumsum_k >= rint(p 2^24) T}  (all items if p = 1)
   I8 i_v    = sort_asc(top k_v by (score desc, idx asc) U {0}); same for i_s
 
-All float arithmetic is numpy float32 (IEEE round-to-nearest-even per
-operation, no fused multiply-add); all integer arithmetic is uint64 or
-Python int.
+Float arithmetic is numpy float32 (IEEE round-to-nearest-even per operation)
+except I1's fused step, which is evaluated as RN32(RN64(acc + q k)): q k of two
+bf16 values is exact in float64, and the float64 sum is either exact or so far
+from a float32 rounding boundary that the second rounding cannot move it
+(reading R11), so this equals fmaf(q, k, acc) for every bf16 input,
+tiny and huge ones included.  Integer arithmetic is uint64 or Python int.
 """
 from __future__ import annotations
 
@@ -82,13 +87,16 @@ def window_scores(q_win: np.ndarray, k: np.ndarray) -> np.ndarray:
 
     q_win: [64][d] float32 (exact bf16 values), k: [S][d] float32.  Returns
     t [64][S] float32; entries with m > n_i (non-causal) are set to -inf.
-    Sequential fold over the d channels, one RN addition per channel.
+    Sequential fold over the d channels, one fused multiply-add (one float32
+    rounding of acc + q k, the product exact) per channel.
     """
     nq, d = q_win.shape
     S = k.shape[0]
+    q64 = np.asarray(q_win, np.float64)
+    k64 = np.asarray(k, np.float64)
     acc = np.zeros((nq, S), F32)
     for c in range(d):
-        acc = (acc + (q_win[:, c:c + 1] * k[None, :, c]).astype(F32)).astype(F32)
+        acc = (acc.astype(np.float64) + q64[:, c:c + 1] * k64[None, :, c]).astype(F32)
     n = S - nq + np.arange(nq)
     acc[np.arange(S)[None, :] > n[:, None]] = -np.inf
     return acc

@@ -1,6 +1,8 @@
 // api_attn.cu — C-ABI entry points for the sparse attention forward/backward
 // (include/mtsa.h).  Validation is synchronous; compute is enqueued on the
 // caller's stream.
+#include <mutex>
+
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -14,15 +16,25 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
                         const void* k, const void* v, void* o, float* o_acc, float* lse,
                         int first, int last, int num_sms, cudaStream_t st);
 
+// SM count of the CURRENT device, cached per device (a process may drive several GPUs
+// from several threads: the cache is per device and its fill is serialised).
 int device_num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  constexpr int kMaxDev = 64;
+  static int n[kMaxDev] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) {
+    int x = 0;
+    cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev);
+    return x > 0 ? x : 148;
   }
-  return n;
+  std::lock_guard<std::mutex> lk(mu);
+  if (n[dev] == 0) {
+    cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (n[dev] <= 0) n[dev] = 148;
+  }
+  return n[dev];
 }
 
 mt_status check_device() {
@@ -53,12 +65,18 @@ mt_status check_shape(const mt_shape* sh, int W) {
   return MT_OK;
 }
 
+// Row strides must hold a full list (v_stride >= S, s_stride >= S/64): the plan builder
+// reads up to min(count, stride) entries per head and drops out-of-range entries, so a
+// malformed caller index cannot make it write outside its own head's plan rows.
 mt_status check_index(const mt_vs_index* idx, const mt_shape* sh) {
   if (!idx || !idx->v_cnt || !idx->v_idx || !idx->s_cnt || !idx->s_off)
     return fail(MT_ESHAPE, "index pointers must be non-NULL");
   if (idx->v_stride < 1 || idx->s_stride < 1 || idx->s_stride > (1LL << 30))
     return fail(MT_ESHAPE, "bad index strides");
-  (void)sh;
+  if (sh && (idx->v_stride < sh->seq_len || idx->s_stride < sh->seq_len / 64))
+    return fail(MT_ESHAPE, "index strides (%lld, %lld) below (seq_len, seq_len/64) = (%lld, %lld)",
+                (long long)idx->v_stride, (long long)idx->s_stride, (long long)sh->seq_len,
+                (long long)(sh->seq_len / 64));
   return MT_OK;
 }
 

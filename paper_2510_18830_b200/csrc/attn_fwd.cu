@@ -1149,13 +1149,10 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
     MT_TRY(check_launch("pack_bars_kernel"));
   }
   const size_t smem = fwd_smem_bytes();
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_fwd) failed (smem %zu)", smem);
-    attr_done = true;
-  }
+  // set on every launch: the attribute applies to the current device only
+  if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_fwd) failed (smem %zu)", smem);
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   cudaMemsetAsync(P.fix_count, 0, 2 * sizeof(int), st);  // fix-up count, tile counter
   if (grid > 0) attn_fwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv, tmkp, tmvp);

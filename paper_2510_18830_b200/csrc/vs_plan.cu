@@ -4,6 +4,8 @@
 // origin s = floor(m / 64) mod W with order kept (stable compaction), which is
 // the per-origin vertical list of convert_index (Alg. 2, P:845;
 // DESIGN.md I10).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -50,13 +52,15 @@ __global__ void __launch_bounds__(kThreads) vs_plan_kernel(VSPlan p, const int32
   uint32_t* bits = s_bits + (int64_t)h * p.bits_words;
   for (int w = threadIdx.x; w < p.bits_words; w += blockDim.x) bits[w] = 0u;
   __syncthreads();
-  const int ns = p.s_cnt[h];
+  // counts are clamped to the row stride and out-of-range entries dropped: a malformed
+  // caller index must not write outside this head's rows (check_index: stride >= nb, S)
+  const int ns = min(max(p.s_cnt[h], 0), p.s_stride);
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
     const int o = p.s_off[(int64_t)h * p.s_stride + i];
-    atomicOr(&bits[o >> 5], 1u << (o & 31));
+    if (o >= 0 && o < p.nb) atomicOr(&bits[o >> 5], 1u << (o & 31));
   }
   // (2) stable split of i_v[h] by origin
-  const int nv = v_cnt[h];
+  const int nv = (int)min((int64_t)max(v_cnt[h], 0), min(v_stride, p.S));
   const int32_t* vin = v_idx + (int64_t)h * v_stride;
   int32_t* vout = vcol + (int64_t)h * p.S;
   int32_t* ptr = vptr + (int64_t)h * (p.W + 1);
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) vs_plan_kernel(VSPlan p, const int32
     for (int base = 0; base < nv; base += blockDim.x) {
       const int i = base + threadIdx.x;
       int m = (i < nv) ? vin[i] : 0;
-      const int keep = (i < nv) && (((m >> 6) % p.W) == s);
+      const int keep = (i < nv) && m >= 0 && m < p.S && (((m >> 6) % p.W) == s);
       int total;
       const int pos = block_exclusive_scan(keep, scan_smem, total);
       if (keep) vout[written + pos] = m;
@@ -79,10 +83,13 @@ __global__ void __launch_bounds__(kThreads) vs_plan_kernel(VSPlan p, const int32
 }  // namespace
 
 // Packed-row capacity per head (forward bar chunks): the origin's columns, at most
-// 16384, rounded to whole 128-row chunks.
+// 16384 (MT_PACK_CAP lowers it, so tests reach the gather fallback of heads with more
+// columns at small sizes), rounded to whole 128-row chunks.
 int packed_cap(int64_t S, int W) {
+  static const int64_t cap = getenv("MT_PACK_CAP") ? atoll(getenv("MT_PACK_CAP")) : 16384;
   int64_t c = S / W;
-  if (c > 16384) c = 16384;
+  if (c > cap) c = cap;
+  if (c < 0) c = 0;
   return (int)((c + 127) / 128 * 128);
 }
 

@@ -13,6 +13,7 @@
 //      < tau * row total; the diagonal is always kept (bitmap [Hq][nI][nI/32]);
 //   5. 64-token CSR: count, scan, fill (query blocks 2I, 2I+1; key blocks 2J, 2J+1,
 //      the diagonal's causal half).
+#include <mutex>
 #include <cublas_v2.h>
 
 #include <cub/cub.cuh>
@@ -288,13 +289,27 @@ mt_status check_x(const mt_shape* sh, const mt_xattn_params* prm) {
                 prm->stride);
   if (!(prm->threshold >= 0.f && prm->threshold <= 1.f)) return fail(MT_ESHAPE, "threshold not in [0, 1]");
   if (sh->seq_len % kB) return fail(MT_EWINDOW, "xattn: seq_len must be a multiple of 128");
+  {  // the segmented sort counts items in int: Hq * nI (nI + 1) / 2 must fit
+    const int64_t nI = sh->seq_len / kB;
+    if ((int64_t)sh->n_q_heads * (nI * (nI + 1) / 2) > (int64_t)INT32_MAX)
+      return fail(MT_ESHAPE, "xattn: Hq x causal block pairs exceeds INT_MAX (seq_len %lld, Hq %d)",
+                  (long long)sh->seq_len, sh->n_q_heads);
+  }
   return MT_OK;
 }
 
+// one cuBLAS handle per device (a handle is bound to the device current at creation),
+// created under a lock so concurrent host threads do not race on the cache
 cublasHandle_t handle() {
-  static cublasHandle_t h = nullptr;
-  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
-  return h;
+  constexpr int kMaxDev = 64;
+  static cublasHandle_t h[kMaxDev] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!h[dev] && cublasCreate(&h[dev]) != CUBLAS_STATUS_SUCCESS) h[dev] = nullptr;
+  return h[dev];
 }
 
 }  // namespace

@@ -51,8 +51,24 @@ class VSIndex:
 
     @staticmethod
     def from_lists(i_v, i_s, seq_len: int, device="cuda") -> "VSIndex":
-        """Upload explicit per-head lists (e.g. a controlled-density pattern)."""
+        """Upload explicit per-head lists (e.g. a controlled-density pattern).
+
+        The lists must be what Alg. 1 produces (include/mtsa.h, mt_vs_index): strictly
+        ascending, columns in [0, seq_len), offsets in [0, seq_len/64), offset 0 present
+        (reading R7: every query keeps its diagonal).  Violations raise ValueError here
+        instead of producing unspecified attention results.
+        """
         Hq = len(i_v)
+        nb = seq_len // BLOCK
+        for h in range(Hq):
+            for name, x, hi in (("i_v", i_v[h], seq_len), ("i_s", i_s[h], nb)):
+                x = [int(t) for t in x]
+                if any(b <= a for a, b in zip(x, x[1:])):
+                    raise ValueError(f"{name}[{h}] is not strictly ascending")
+                if x and (x[0] < 0 or x[-1] >= hi):
+                    raise ValueError(f"{name}[{h}] has entries outside [0, {hi})")
+            if len(i_s[h]) == 0 or int(i_s[h][0]) != 0:
+                raise ValueError(f"i_s[{h}] must contain offset 0 (the diagonal)")
         idx = VSIndex.empty(seq_len, Hq, device="cpu")
         for h in range(Hq):
             a, b = torch.as_tensor(i_v[h], dtype=torch.int32), torch.as_tensor(i_s[h], dtype=torch.int32)
@@ -200,7 +216,10 @@ class Comm:
         if rank == 0:
             _lib.check(L.mt_comm_unique_id(buf))
         ids = [bytes(buf)] if rank == 0 else [None]
-        dist.broadcast_object_list(ids, src=0, group=group)
+        # `rank` is the ring rank (rank within `group`): the id travels from the group's
+        # rank 0, whose global rank is not 0 when a sub-group is passed
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(ids, src=src, group=group)
         uid = (ctypes.c_uint8 * 128).from_buffer_copy(ids[0])
         h = ctypes.c_void_p()
         inner = world if not inner else inner

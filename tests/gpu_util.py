@@ -37,3 +37,15 @@ def random_index(S: int, Hq: int, seed: int, n_off: int, n_col: int):
     is_ = [np.unique(np.r_[0, r.choice(nb, min(n_off, nb), replace=False)]).astype(np.int32)
            for _ in range(Hq)]
     return iv, is_
+
+
+def p99_rel(got: np.ndarray, ref: np.ndarray, floor: float = 1e-2) -> float:
+    """Elementwise relative error |x - ref| / |ref|, 99th percentile over the entries with
+    |ref| >= floor * max|ref| (reported next to R20's normwise error; near-zero entries
+    make an elementwise relative error meaningless)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    sel = np.abs(ref) >= floor * np.max(np.abs(ref))
+    if not sel.any():
+        return 0.0
+    return float(np.percentile(np.abs(got[sel] - ref[sel]) / np.abs(ref[sel]), 99))

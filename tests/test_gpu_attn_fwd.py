@@ -103,3 +103,35 @@ def test_fwd_rejects_bad_shapes(cuda_lib):
     with pytest.raises(_lib.MTError) as e:
         ops.sparse_attn_fwd(q, q[:, :1].contiguous(), q[:, :1].contiguous(), idx)
     assert e.value.name == "MT_EWINDOW"
+
+
+def test_fwd_stabiliser_overflow_fixup(cuda_lib):
+    # The forward fixes each query column's stabiliser from the tile's first chunk (the
+    # diagonal + next offset) and routes tiles whose later scores exceed it by more than
+    # 2^64 to the exact two-pass attn_fwd_fixup kernel.  Plant such scores: queries of
+    # blocks 6 and 10 (dimension 0 = 40) against vertical columns 5 and 200 (dimension
+    # 0 = 40), which sit in bar chunks after the slash chunk, 1600 / sqrt(128) = 141 nats
+    # (204 log2 units) above anything in chunk 0.  P:879's merge and LSE must still match.
+    S, Hq, Hkv = 1024, 2, 1
+    q, k, v = make_qkv(S, Hq, Hkv, seed=5, a=4.0)
+    from synth.generator import f32_to_bf16_bits
+    qf, kf = bf16_bits_to_f32(q).copy(), bf16_bits_to_f32(k).copy()
+    for g in (6, 10):
+        qf[g * 64:(g + 1) * 64, :, 0] = 40.0
+    kf[[5, 200], :, 0] = 40.0
+    q, k = f32_to_bf16_bits(qf), f32_to_bf16_bits(kf)
+    iv = [np.array([0, 5, 200, 333], np.int32)] * Hq
+    is_ = [np.array([0, 1], np.int32)] * Hq
+    _check(q, k, v, iv, is_)
+    # the backward recomputes P from the fixed-up LSE
+    from synth.generator import make_grad_out
+    dO = make_grad_out(S, Hq, seed=5)
+    O, L = OA.sparse_attention_forward(f64(q), f64(k), f64(v), iv, is_)
+    ref = OA.sparse_attention_backward(f64(q), f64(k), f64(v), O, L, f64(dO), iv, is_)
+    idx = ops.VSIndex.from_lists(iv, is_, S)
+    qd, kd, vd = to_dev_bf16(q), to_dev_bf16(k), to_dev_bf16(v)
+    o, lse = ops.sparse_attn_fwd(qd, kd, vd, idx)
+    g = ops.sparse_attn_bwd(qd, kd, vd, o, lse, to_dev_bf16(dO), idx)
+    torch.cuda.synchronize()
+    for got, r in zip(g, ref):
+        assert normwise_err(got.float().cpu().numpy().astype(np.float64), r, 1) <= TOL_O

@@ -155,3 +155,38 @@ def test_count_pairs_matches_mask():
     cnt = A.count_pairs(iv, is_, S)
     for h in range(2):
         assert cnt[h] == SF.union_mask(iv[h], is_[h], S).sum()
+
+
+def test_gqa_mapping_equals_repeat_interleaved_mha():
+    # Reading R10 ("per head", GQA of Qwen2.5): q head h reads kv head
+    # h // (Hq/Hkv).  Pinned against the plain multi-head computation on K/V repeated
+    # per q head (repeat-interleave: q heads 0..grp-1 -> kv head 0, ...): the GQA
+    # outputs and dQ must equal the MHA ones, and the GQA dK/dV of a kv head must
+    # equal the sum of the MHA dK/dV of its q heads.  Hkv = 2 and 4 with Hq = 8, and
+    # a different index per q head, so a wrong head -> kv-head map fails.
+    rng = np.random.default_rng(31)
+    S, Hq, d = 256, 8, 16
+    for Hkv in (2, 4):
+        grp = Hq // Hkv
+        q = rng.standard_normal((S, Hq, d))
+        k = rng.standard_normal((S, Hkv, d))
+        v = rng.standard_normal((S, Hkv, d))
+        dO = rng.standard_normal((S, Hq, d))
+        iv, is_ = [], []
+        for h in range(Hq):
+            iv.append(np.unique(np.r_[0, rng.choice(S, 12, replace=False)]).astype(np.int32))
+            is_.append(np.unique(np.r_[0, rng.choice(S // 64, 2, replace=False)]).astype(np.int32))
+        k_mha = np.repeat(k, grp, axis=1)   # [S][Hq][d], q head h -> kv head h // grp
+        v_mha = np.repeat(v, grp, axis=1)
+        O, L = A.sparse_attention_forward(q, k, v, iv, is_)
+        Om, Lm = A.sparse_attention_forward(q, k_mha, v_mha, iv, is_)
+        assert np.allclose(O, Om, atol=1e-12) and np.allclose(L, Lm, atol=1e-12)
+        dq, dk, dv = A.sparse_attention_backward(q, k, v, O, L, dO, iv, is_)
+        dqm, dkm, dvm = A.sparse_attention_backward(q, k_mha, v_mha, Om, Lm, dO, iv, is_)
+        assert np.allclose(dq, dqm, atol=1e-12)
+        assert np.allclose(dk, dkm.reshape(S, Hkv, grp, d).sum(axis=2), atol=1e-12)
+        assert np.allclose(dv, dvm.reshape(S, Hkv, grp, d).sum(axis=2), atol=1e-12)
+        # and the map is not the trivial one: a different kv head gives other outputs
+        O_wrong, _ = A.sparse_attention_forward(q, np.roll(k_mha, grp, axis=1),
+                                                 np.roll(v_mha, grp, axis=1), iv, is_)
+        assert not np.allclose(O, O_wrong)

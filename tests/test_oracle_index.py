@@ -153,9 +153,75 @@ def test_full_budget_selects_everything():
     assert is_.tolist() == list(range(4))
 
 
+def _libm_fmaf():
+    import ctypes
+    import ctypes.util
+    m = ctypes.CDLL(ctypes.util.find_library("m") or "libm.so.6")
+    m.fmaf.restype = ctypes.c_float
+    m.fmaf.argtypes = [ctypes.c_float] * 3
+    return m.fmaf
+
+
+def _extreme_bf16(shape, rng):
+    """bf16 values spanning the whole exponent range: normals from 2^-126 to
+    2^100, subnormal bf16s, signed zeros.  Products of two such values underflow
+    below 2^-149 or land in fp32's subnormal range (the cases where a rounded
+    product and a fused multiply-add differ)."""
+    mant = rng.integers(0, 128, shape)
+    sign = rng.integers(0, 2, shape)
+    expo = rng.choice(np.r_[np.arange(1, 40), np.arange(100, 140), np.arange(200, 228)], shape)
+    expo[rng.random(shape) < 0.05] = 0  # bf16 subnormals and zeros
+    bits = (sign << 15) | (expo << 7) | mant
+    return bf16_bits_to_f32(bits.astype(np.uint16))
+
+
+def test_window_scores_fold_is_libm_fmaf():
+    # I1 = sequential fold of IEEE fusedMultiplyAdd (the C library's fmaf), pinned
+    # on ordinary and on extreme bf16 inputs (products below 2^-149, subnormal
+    # partial sums, partial sums near 2^100) where a separately rounded product
+    # would give other bits.
+    fmaf = _libm_fmaf()
+    rng = np.random.default_rng(21)
+    d, S = 16, 96
+    with np.errstate(over="ignore", invalid="ignore"):
+        _fmaf_cases(fmaf, rng, d, S)
+
+
+def _fmaf_cases(fmaf, rng, d, S):
+    for qw, k in [(_extreme_bf16((64, d), rng), _extreme_bf16((S, d), rng)),
+                  (rng.standard_normal((64, d)).astype(F32) * F32(2.0 ** -70),
+                   rng.standard_normal((S, d)).astype(F32) * F32(2.0 ** -70))]:
+        qw = bf16_bits_to_f32(f32_to_bf16_bits(qw))
+        k = bf16_bits_to_f32(f32_to_bf16_bits(k))
+        t = vsidx.window_scores(qw, k)
+        n = S - 64 + np.arange(64)
+        diff_from_rounded_product = 0
+        for i in range(64):
+            for m in range(0, int(n[i]) + 1):
+                acc = 0.0
+                rp = F32(0.0)
+                for c in range(d):
+                    acc = fmaf(float(qw[i, c]), float(k[m, c]), acc)
+                    rp = F32(rp + F32(qw[i, c] * k[m, c]))
+                assert np.array_equal(np.array([acc], F32).view(np.uint32),
+                                      np.array([t[i, m]], F32).view(np.uint32)), (i, m)
+                diff_from_rounded_product += int(F32(acc) != rp)
+        # the extreme inputs really exercise the difference
+        assert diff_from_rounded_product > 0
+
+
 def test_c_fast_path_matches_numpy_bitwise():
-    for S, seed in [(256, 8), (1024, 9)]:
+    # S >= 4096 spans several 1024-key OpenMP chunks of the C helper; the last case
+    # adds planted tiny values (products underflowing fp32) to the generator's keys.
+    rng = np.random.default_rng(22)
+    for S, seed, tiny in [(256, 8, False), (1024, 9, False), (4096, 10, False), (5120, 11, True)]:
         qw, k = _window(S, seed=seed, a=12.0)
+        if tiny:
+            sel = rng.random(k.shape) < 0.2
+            k = np.where(sel, k * F32(2.0 ** -120), k).astype(F32)
+            k = bf16_bits_to_f32(f32_to_bf16_bits(k))
+            qw = np.where(rng.random(qw.shape) < 0.2, qw * F32(2.0 ** -40), qw).astype(F32)
+            qw = bf16_bits_to_f32(f32_to_bf16_bits(qw))
         assert np.array_equal(vsidx.column_scores(qw, k, use_c=True),
                               vsidx.column_scores(qw, k, use_c=False))
 
@@ -166,4 +232,4 @@ def test_bf16_rounding_helper():
     assert bf16_bits_to_f32(b)[0] == 1.0
     assert bf16_bits_to_f32(b)[1] == 1.0          # tie -> even
     assert bf16_bits_to_f32(b)[3] == -2.5
-    assert b[5] == 0                                # |x| < 2^-60 flushed
+    assert b[5] != 0 and abs(bf16_bits_to_f32(b)[5] / F32(1e-30) - 1) < 2 ** -8  # no flushing

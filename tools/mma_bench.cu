@@ -53,6 +53,35 @@ __global__ void __launch_bounds__(128, 1) bench(int variant, int reps, long long
           for (int kk = 0; kk < 128; kk += 16)
             mma_ss(tmem + 384, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
         }
+        if (variant == 5 || variant == 6) {  // dV + dK with A = P^T / dS^T from TMEM (.ts), N = 128
+#pragma unroll
+          for (int kq = 0; kq < 64; kq += 16) {
+            mma_ts(tmem + 128, tmem + 256 + kq / 2, sdesc_add(dom, kq * 128), id_kv, 1);
+            mma_ts(tmem + 0, tmem + 288 + kq / 2, sdesc_add(dqm, kq * 128), id_kv, 1);
+          }
+        }
+        if (variant == 6) {  // + S^T, dP^T, dQ^T: the backward's per-chunk sequence
+#pragma unroll
+          for (int kk = 0; kk < 128; kk += 16) {
+            const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2, qo = (kk >> 6) * 8192 + (kk & 63) * 2;
+            mma_ss(tmem + 320, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
+            mma_ss(tmem + 384, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 128; kk += 16)
+            mma_ss(tmem + 448, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
+        }
+        if (variant == 7) {  // issue rate: 32 tiny MMAs (M128 N8)
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk)
+            mma_ss(tmem + 256, sdesc_add(dK, (kk & 3) * 32), sdesc_add(dq, (kk & 3) * 32),
+                   make_idesc_bf16(128, 8, false, false), kk > 0);
+        }
+        if (variant == 8) {  // S^T with A = K from TMEM (.ts), N = 64
+#pragma unroll
+          for (int kk = 0; kk < 128; kk += 16)
+            mma_ts(tmem + 256, tmem + 448 + kk / 2, sdesc_add(dq, (kk >> 6) * 8192 + (kk & 63) * 2), id_s, kk > 0);
+        }
         if (variant == 4) {  // S^T only, K-major B but N=128 (two query blocks)
 #pragma unroll
           for (int kk = 0; kk < 128; kk += 16) {
@@ -79,10 +108,12 @@ int main() {
   cudaMalloc(&d, 148 * sizeof(long long));
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   const char* names[] = {"S^T+dP^T (16x M128N64 KK)", "dV+dK (8x M128N128 K/MN)", "dQ^T (8x M128N64 MN/MN)",
-                         "all per chunk (32 MMAs)", "S^T-like N128 KK (8x)"};
-  const double ideal[] = {16 * 32, 8 * 64, 8 * 32, 16 * 32 + 8 * 64 + 8 * 32, 8 * 64};
+                         "all per chunk (32 MMAs)", "S^T-like N128 KK (8x)", "dV+dK .ts (8x M128N128)",
+                         "chunk: SS S/dP/dQ + ts dV/dK", "issue: 32x M128N8", "S^T .ts A=K (8x N64)"};
+  const double ideal[] = {16 * 32, 8 * 64, 8 * 32, 16 * 32 + 8 * 64 + 8 * 32, 8 * 64, 8 * 64,
+                          24 * 32 + 8 * 64, 32 * 4, 8 * 32};
   for (int grid : {1, 148}) {
-    for (int v = 0; v < 5; ++v) {
+    for (int v = 0; v < 9; ++v) {
       const int reps = 2000;
       bench<<<grid, 128, 140 * 1024>>>(v, reps, d);
       long long h[148];
