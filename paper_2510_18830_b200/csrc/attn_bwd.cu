@@ -17,18 +17,21 @@
 //               (column, block) pair is live iff the column is not covered by a
 //               selected slash of that block (I9).  dK/dV -> atomic scatter-add
 //               (the paper's "backward for all vertical lines").
-// Per chunk (M = 128 keys, N = 64 queries), in the TMEM region of the softmax
-// warpgroup that owns the chunk:
+// Per chunk (M = 128 keys, N = 64 queries), in TMEM region (chunk event) & 1:
 //   S^T = K Q^T, dP^T = V dO^T              (tcgen05, SMEM x SMEM -> TMEM)
 //   P^T, dS^T (bf16, dS pre-scaled by 1/sqrt d) in registers -> tcgen05.st back
 //     over S^T (A operands of the next two MMAs); dS^T also -> SMEM
 //   dV += P^T dO, dK += dS^T Q              (A from TMEM, N = 128)
 //   dQ^T = K^T dS^T                          (TMEM over dP^T, M = d) -> bulk reduce-add
+// All 8 softmax warps share each chunk (warp = TMEM lane quarter x query half), and
+// the MMA warp issues S(n), dP(n), G(n-1), S(n+1), ...: round-1's per-warpgroup chunks
+// left the tensor pipe idle ~45% of the time behind one warpgroup's softmax latency and
+// its dQ drain (clock64 timeline, profiles/r02_bwd_timeline_*.txt).
 // Keeping P^T/dS^T in TMEM saves 48 KB of shared-memory traffic per chunk: the
 // SMEM x SMEM N = 64 MMAs are shared-memory-bandwidth bound (51 instead of 32
 // cycles per MMA, tools/mma_bench.cu), so SMEM bytes are this kernel's currency.
 // Warp roles: warp 0 producer (TMA / cp.async), warp 1 MMA issuer, warps 4..11
-// two softmax-backward warpgroups (alternate chunks) + dQ drain + epilogue.
+// softmax-backward (two query halves of every chunk) + dQ drain + epilogue.
 //
 // L2 locality (BLOCK): the streamed operands (Q, dO: 32 KB, dQ reduce: 32 KB per
 // chunk) dominate DRAM traffic.  A query block (h, g_q) is needed by the tiles
@@ -52,7 +55,7 @@ namespace mt {
 namespace bwd {
 
 constexpr int kStages = 4;      // Q / dO / LSE / D stages
-constexpr int kThreads = 384;   // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
+constexpr int kThreads = 512;   // warpgroup 0: producer, MMA, 2 idle; 1-2: softmax; 3: dQ drain
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
 constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
@@ -77,6 +80,14 @@ struct alignas(16) ChunkMeta {
   int pad;
 };
 
+// softmax -> dQ-drain warpgroup: one entry per published chunk (and per tile END / DONE)
+struct DrainMeta {
+  int kbp;   // kind | TMEM region << 8 | parity of the region's earlier chunk count << 9
+  int h, j;  // chunk: q head, local query block
+  int seq;   // producer event index (timeline probe)
+};
+constexpr int kDrainRing = 4;
+
 struct Smem {
   uint8_t k[kTileKV];
   uint8_t v[kTileKV];
@@ -91,10 +102,12 @@ struct Smem {
   ChunkMeta meta[kStages];
   ChunkMeta smeta[2];      // handed to softmax warpgroup 0 / 1
   int cols[128];           // BAR: global column of each key row (-1 = padding)
-  int tile_chunks[2];      // chunks each softmax warpgroup saw in the current tile
+  DrainMeta dring[kDrainRing];
   uint64_t full[kStages], empty[kStages];
   uint64_t kvfull, kvempty, tfree;
-  uint64_t sfull[2], dsfull[2], gdone[2], dqfree[2];  // dqfree: region drained
+  uint64_t sfull[2], dsfull[2], gdone[2], dqfree[2];  // dqfree: region's dQ^T read from TMEM
+  uint64_t dqdone[2];                                  // region's dS^T / staging buffer free
+  uint64_t dmfull[kDrainRing], dmfree[kDrainRing], tdrained;
   uint32_t tmem_base;
 };
 
@@ -117,7 +130,10 @@ struct Params {
   int static_tiles;         // 1: round-robin tiles instead (A/B switch, MT_BWD_STATIC=1)
   int bar_parts;            // BAR: query-range parts per column group
   int bar_part_len;         // BAR: query blocks per part
-  int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
+  int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds,
+                            // bit1 skip the softmax math, bit4 skip the dQ^T MMA
+  int dq_red;               // 1: dQ via red.global.add.v4.f32 from registers (MT_BWD_DQ_RED)
+                            // instead of SMEM staging + bulk tensor reduce
   int hpt;                  // BLOCK: q heads per tile (of one kv head; their dK/dV sum stays in
                             // TMEM, so the tile's K/V load and dK/dV epilogue are shared)
 };
@@ -189,7 +205,9 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     const uint32_t stage = c % kStages;
     MT_CRUMB(2, 1000000 + (int)c);
     mbar_wait(smem_u32(&sm.empty[stage]), ((c / kStages) & 1) ^ 1);
+#ifndef MT_TL_ISSUER2
     if (lane == 0) MT_TL(0, c);
+#endif
     if (lane == 0) {
       ChunkMeta& m = sm.meta[stage];
       m.seq = (int)c;
@@ -377,9 +395,19 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
 }
 
 // ------------------------------------------------------------------ MMA issuer
-// Chunk k of a tile goes to softmax warpgroup k & 1.  Per chunk: S^T, dP^T into
-// the shared TMEM pair, then the gradient MMAs of the previous chunk (dV, dK
-// accumulate; dQ^T into that warpgroup's buffer).
+// Chunks are numbered globally (n); softmax events (chunks and tile ENDs) are
+// numbered e, and event e uses TMEM region e & 1.  Per chunk n in region b:
+//   S(n)  S^T = K Q^T into region cols [0, 64)     needs: Q stage landed, G(n-2) issued
+//                                                  (the S half of the region then holds
+//                                                  nothing the pipe still has to read:
+//                                                  tcgen05 MMAs execute in issue order)
+//   P(n)  dP^T = V dO^T into cols [64, 128), then commit sfull[b]
+//                                                  needs: dQ^T of the region's previous
+//                                                  chunk drained (dqfree[b])
+//   G(n)  dV += P^T dO, dK += dS^T Q (A from TMEM), dQ^T = K^T dS^T into cols [64, 128)
+//                                                  needs: P^T/dS^T published (dsfull[b])
+// The issue order S(n), P(n), G(n-1), S(n+1), P(n+1), G(n) keeps the tensor pipe busy
+// while the softmax warps work on chunk n: its gradients follow the next chunk's S/dP.
 __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const bool leader = elect_one();
   const uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // S^T, dP^T
@@ -394,20 +422,32 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dQmn0 = make_sdesc(smem_u32(sm.q[0]), 8192, 1024);
   const uint64_t dOmn0 = make_sdesc(smem_u32(sm.dO[0]), 8192, 1024);
   const uint64_t dDSTmn0 = make_sdesc(smem_u32(sm.pd[0]), 8192, 1024);
-  uint32_t c = 0, ntile = 0;
-  uint32_t sq0 = 0, sq1 = 0;                    // S^T/dP^T issued into region 0 / 1
-  uint32_t ds0 = 0, ds1 = 0;  // per buffer: dsfull waits
+  auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
+  uint32_t c = 0, ntile = 0;          // producer stage events consumed; tiles
+  uint32_t e = 0;                     // softmax events signalled (chunks + ENDs)
+  uint32_t nS = 0, nP = 0, nG = 0;    // chunks whose S^T / dP^T / gradients are issued
+  uint32_t rc0 = 0, rc1 = 0;          // chunks assigned to TMEM region 0 / 1 so far
+  // chunks in flight (slot n & 1): stage, region, chunks of that region before it, seq
+  uint32_t st0 = 0, st1 = 0, rg0 = 0, rg1 = 0, pr0 = 0, pr1 = 0;
+  int sq0 = 0, sq1 = 0;
+  (void)sq0;
+  (void)sq1;
+  auto signal = [&](int kind, int tile) {  // END / DONE as a softmax event
+    const uint32_t b = e & 1;
+    if (leader) {
+      sm.smeta[b].kind = kind;
+      sm.smeta[b].tile = tile;
+      mbar_arrive(smem_u32(&sm.sfull[b]));
+      mbar_arrive(smem_u32(&sm.sfull[b]));
+    }
+    ++e;
+  };
   for (;;) {
-    {  // the next chunk tells whether another tile follows
+    {  // the next producer event tells whether another tile follows
       const uint32_t stage = c % kStages;
       mbar_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1);
       if (sm.meta[stage].kind == kDone) {
-        for (uint32_t b = 0; b < 2; ++b)
-          if (leader) {
-            sm.smeta[b].kind = kDone;
-            mbar_arrive(smem_u32(&sm.sfull[b]));
-            mbar_arrive(smem_u32(&sm.sfull[b]));
-          }
+        signal(kDone, -1);
         break;
       }
     }
@@ -416,113 +456,134 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     ++ntile;
     if (P.mode == kModeBar) fence_proxy_async_smem();
     tc_fence_after();
-    // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and its
-    // warpgroup's TMEM region is drained; the gradient MMAs of chunk g as soon as its
-    // P/dS^T is published.  (A fixed S(k), G(k-1), S(k+1) order makes G(k) wait for chunk
-    // k+1's load, which holds chunk k's stage ~2x longer: measured.)
-    bool acc_started = false, end_seen = false;
-    uint32_t k = 0, g = 0;  // tile-local: chunks whose S^T issued / gradients issued
-    // per region: stage / producer seq of its pending chunk (scalars: no local memory)
-    uint32_t pst0 = 0, pst1 = 0, end_stage = 0;
-    int pseq0 = 0, pseq1 = 0, end_tile = 0;
-    auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
-    auto try_grads = [&]() {  // gradient MMAs of chunk g (softmax warpgroup g & 1)
-      const uint32_t bg = g & 1;
-      uint32_t& ds = bg ? ds1 : ds0;
-      if (!uni(mbar_test_wait(smem_u32(&sm.dsfull[bg]), ds & 1))) return false;
-      ++ds;
-#ifdef MT_TL_ISSUER
-      if (leader) MT_TL(6, bg ? pseq1 : pseq0);
-#endif
-      tc_fence_after();
-      const uint32_t st = bg ? pst1 : pst0;
-      const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
-      const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
-      const uint64_t dstm = sdesc_add(dDSTmn0, bg * kTileP);
-      const uint32_t R = tmem + kColR + 128 * bg;
-      if (leader) {
-#pragma unroll
-        for (int kq = 0; kq < 64; kq += 16) {  // A = P^T / dS^T from TMEM (2 bf16 per column)
-          const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
-          mma_ts(tmem + kColDV, R + kq / 2, sdesc_add(dom, kq * 128), id_kv, acc);
-          mma_ts(tmem + kColDK, R + 32 + kq / 2, sdesc_add(dqm, kq * 128), id_kv, acc);
-        }
-#pragma unroll
-        for (int kk = 0; kk < 128; kk += 16)
-          mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
-        mma_commit(smem_u32(&sm.gdone[bg]));
-        mma_commit(smem_u32(&sm.empty[st]));
-        MT_TL(3, bg ? pseq1 : pseq0);
-      }
-      acc_started = true;
-      ++g;
-      return true;
-    };
-    auto try_s = [&]() {  // S^T/dP^T of the next chunk, or note the tile's END
-      const uint32_t stage = c % kStages;
-      if (!uni(mbar_test_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1))) return false;
-      if (sm.meta[stage].kind == kEnd) {
-        end_seen = true;
-        end_stage = stage;
-        end_tile = sm.meta[stage].tile;  // read before the stage is released
-        ++c;
-        return true;
-      }
-      const uint32_t b = k & 1;
-      // region b is free once the chunk it held two chunks ago was drained
-      const uint32_t nsq = b ? sq1 : sq0;
-      if (nsq > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[b]), (nsq - 1) & 1)))
-        return false;
-#ifdef MT_TL_ISSUER
-      if (leader) MT_TL(7, sm.meta[stage].seq);
-#endif
-      tc_fence_after();
-      const uint32_t R = tmem + kColR + 128 * b;
-      if (leader) {
-        sm.smeta[b] = sm.meta[stage];
-        mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
-        const uint64_t dq = sdesc_add(dQ0, stage * kTileQ), ddo = sdesc_add(dO0, stage * kTileQ);
-#pragma unroll
-        for (int kk = 0; kk < 128; kk += 16) {
-          const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
-          const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
-          mma_ss(R, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
-          mma_ss(R + 64, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
-        }
-        mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
-        MT_TL(2, sm.meta[stage].seq);
-      }
-      if (b) {
-        pst1 = stage;
-        pseq1 = sm.meta[stage].seq;
-        ++sq1;
-      } else {
-        pst0 = stage;
-        pseq0 = sm.meta[stage].seq;
-        ++sq0;
-      }
-      ++k;
-      ++c;
-      return true;
-    };
+    const uint32_t tile_n0 = nS;  // first chunk of this tile: its gradients overwrite dK/dV
+    bool end_seen = false;
+    uint32_t end_stage = 0;
+    int end_tile = 0;
     MT_CRUMB(0, 1);
     for (;;) {
-      if (g < k) try_grads();
-      if (!end_seen) try_s();
-      if (end_seen && g == k) break;
+      // ---- G(nG): gradients of the oldest published chunk
+      if (nG < nP) {
+        const uint32_t sl = nG & 1;
+        const uint32_t b = sl ? rg1 : rg0, pre = sl ? pr1 : pr0;
+        if (uni(mbar_test_wait(smem_u32(&sm.dsfull[b]), pre & 1))) {
+#ifdef MT_TL_ISSUER2
+          if (leader) MT_TL(4, sl ? sq1 : sq0);
+#endif
+          tc_fence_after();
+          const uint32_t st = sl ? st1 : st0;
+          const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
+          const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
+          const uint64_t dstm = sdesc_add(dDSTmn0, b * kTileP);
+          const uint32_t R = tmem + kColR + 128 * b;
+          const bool acc_started = nG > tile_n0;
+          if (leader) {
+#pragma unroll
+            for (int kq = 0; kq < 64; kq += 16) {
+              // A = P^T / dS^T from TMEM: query half hf's 32 queries are packed (2 bf16 per
+              // column) at cols [32 hf, 32 hf + 16) (P^T) and [32 hf + 16, 32 hf + 32) (dS^T)
+              const uint32_t acol = (uint32_t)((kq >> 5) * 32 + (kq & 31) / 2);
+              const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
+              mma_ts(tmem + kColDV, R + acol, sdesc_add(dom, kq * 128), id_kv, acc);
+              mma_ts(tmem + kColDK, R + acol + 16, sdesc_add(dqm, kq * 128), id_kv, acc);
+            }
+            if (!(P.dbg & 16)) {
+#pragma unroll
+              for (int kk = 0; kk < 128; kk += 16)
+                mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
+            }
+            mma_commit(smem_u32(&sm.gdone[b]));
+            mma_commit(smem_u32(&sm.empty[st]));
+#ifdef MT_TL_ISSUER2
+            MT_TL(5, sl ? sq1 : sq0);
+#else
+            MT_TL(3, sl ? sq1 : sq0);
+#endif
+          }
+          ++nG;
+          continue;
+        }
+      }
+      // ---- P(nP): dP^T once the region's previous dQ^T is drained
+      if (nP < nS) {
+        const uint32_t sl = nP & 1;
+        const uint32_t b = sl ? rg1 : rg0, pre = sl ? pr1 : pr0;
+        if (pre == 0 || uni(mbar_test_wait(smem_u32(&sm.dqfree[b]), (pre - 1) & 1))) {
+          tc_fence_after();
+          const uint32_t st = sl ? st1 : st0;
+          const uint32_t R = tmem + kColR + 128 * b;
+          if (leader) {
+#ifdef MT_TL_ISSUER2
+            MT_TL(2, sl ? sq1 : sq0);
+#endif
+            const uint64_t ddo = sdesc_add(dO0, st * kTileQ);
+#pragma unroll
+            for (int kk = 0; kk < 128; kk += 16) {
+              const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
+              const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
+              mma_ss(R + 64, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
+            }
+            mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
+#ifdef MT_TL_ISSUER2
+            MT_TL(3, sl ? sq1 : sq0);
+#else
+            MT_TL(2, sl ? sq1 : sq0);
+#endif
+          }
+          ++nP;
+          continue;
+        }
+      }
+      // ---- S(nS): the next chunk's S^T (or the tile's END)
+      if (!end_seen && nS == nP && nS < nG + 2) {
+        const uint32_t stage = c % kStages;
+        if (uni(mbar_test_wait(smem_u32(&sm.full[stage]), (c / kStages) & 1))) {
+          if (sm.meta[stage].kind == kEnd) {
+            end_seen = true;
+            end_stage = stage;
+            end_tile = sm.meta[stage].tile;  // read before the stage is released
+            ++c;
+            continue;
+          }
+          tc_fence_after();
+          const uint32_t b = e & 1;
+          const uint32_t pre = b ? rc1 : rc0;
+          const uint32_t sl = nS & 1;
+          const int seq = sm.meta[stage].seq;
+          if (sl) { st1 = stage; rg1 = b; pr1 = pre; sq1 = seq; }
+          else    { st0 = stage; rg0 = b; pr0 = pre; sq0 = seq; }
+          const uint32_t R = tmem + kColR + 128 * b;
+          if (leader) {
+#ifdef MT_TL_ISSUER2
+            MT_TL(0, seq);
+#endif
+            sm.smeta[b] = sm.meta[stage];
+            mbar_arrive(smem_u32(&sm.sfull[b]));  // 1 of 2: publishes smeta
+            const uint64_t dq = sdesc_add(dQ0, stage * kTileQ);
+#pragma unroll
+            for (int kk = 0; kk < 128; kk += 16) {
+              const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
+              const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
+              mma_ss(R, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
+            }
+#ifdef MT_TL_ISSUER2
+            MT_TL(1, seq);
+#endif
+          }
+          if (b) ++rc1; else ++rc0;
+          ++e;
+          ++nS;
+          ++c;
+          continue;
+        }
+      }
+      if (end_seen && nG == nS) break;
     }
     if (leader) {
       mma_commit(smem_u32(&sm.kvempty));  // K/V smem reusable after all MMAs so far
       mbar_arrive(smem_u32(&sm.empty[end_stage]));
     }
-    // every chunk's gradients are issued, so each warpgroup consumed its last sfull
-    for (uint32_t b = 0; b < 2; ++b)
-      if (leader) {
-        sm.smeta[b].kind = kEnd;
-        sm.smeta[b].tile = end_tile;
-        mbar_arrive(smem_u32(&sm.sfull[b]));
-        mbar_arrive(smem_u32(&sm.sfull[b]));
-      }
+    signal(kEnd, end_tile);
   }
 }
 
@@ -571,91 +632,36 @@ __device__ __forceinline__ void softmax_half(const uint32_t (&sv)[32], const uin
   }
 }
 
+// All 8 softmax warps work on every chunk: warp w handles TMEM lanes 32 (w % 4).. (key
+// rows) and query half hf = (w - 4) / 4 (queries 32 hf .. 32 hf + 31), so a chunk's
+// softmax latency is half of one warpgroup's.  After publishing chunk n's P/dS^T the
+// warps drain chunk n-1's dQ^T (its gradients ran meanwhile), which frees that region
+// for the dP^T of chunk n+1.
 __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUtensorMap* tmdq,
                             const CUtensorMap* tmdk, const CUtensorMap* tmdv) {
   const int w = warp_id();
-  const int quad = w & 3, wg = (w - 4) >> 2;
+  const int quad = w & 3, hf = (w - 4) >> 2;
   const int lane = lane_id();
   const int row = quad * 32 + lane;  // key row of the tile == TMEM lane; d index for dQ^T
+  const int hrow = hf * 128 + row;   // thread index among the 256 softmax threads
   const int slot = row >> 6, kk = row & 63;
   const uint32_t lb = (uint32_t)(quad * 32) << 16;
   const VSPlan& pl = P.plan;
   const int W = pl.W;
-  const uint32_t sfull = smem_u32(&sm.sfull[wg]);
-  const uint32_t R = tmem + lb + kColR + 128 * wg;  // this warpgroup's TMEM region (own lanes)
-  const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
-  const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
-  const uint32_t pdbuf = smem_u32(sm.pd[wg]);
-  const uint32_t drow = pdbuf + row * 128;  // dS^T row in SMEM (B of dQ^T)
-  const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
-  uint32_t su = 0, gw = 0;  // sfull events, gdone waits
+  const uint32_t hf_bar = 1 + hf;  // named barrier of this query half (128 threads)
+  uint32_t e = 0, rc0 = 0, rc1 = 0;  // softmax events; chunks per TMEM region
   uint32_t ntile = 0;
-  bool staging_busy = false;  // a bulk reduce may still be reading this warpgroup's buffer
 
-  auto wait_staging = [&]() {  // warpgroup-uniform
-    if (!staging_busy) return;
-    if (row == 0) MT_CRUMB(3 + wg, 3000000);
-    if (row == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    named_bar_sync(wg_bar, 128);
-    staging_busy = false;
-  };
-  // dQ^T of this warpgroup's chunk (h, j) -> dQ[q][h][d = row].  Runs right after the
-  // chunk's P/dS^T is published, so it overlaps the next S^T instead of delaying the
-  // gradient MMAs; the reduce's smem read is only waited for before the buffer is
-  // rewritten (next P/dS^T or the epilogue).
-  auto drain_dq = [&](int h, int j, int seq) {
-    if (row == 0) MT_CRUMB(3 + wg, 2000000 + (int)gw);
-    mbar_wait(gdone, gw & 1);  // gradient MMAs done: P/dS^T free, dQ^T complete
-    ++gw;
-#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
-    if (row == 0) MT_TL(6, seq);
-#endif
-    tc_fence_after();
-    uint32_t r0[32], r1[32];
-    tmem_ld32(R + 64, r0);
-    tmem_ld32(R + 96, r1);
-    tmem_ld_wait();
-    tc_fence_before();
-    mbar_arrive(dqfree);
-    if (P.dbg & 1) return;
-    if (P.dbg & 4) {  // A/B: coalesced per-element reduction (thread = d, 64 queries)
-      float* dst = P.dq + ((size_t)j * 64 * pl.Hq + h) * 128 + row;
-      const size_t qs = (size_t)pl.Hq * 128;
-#pragma unroll
-      for (int c = 0; c < 32; ++c) red_add_f32(dst + c * qs, __uint_as_float(r0[c]));
-#pragma unroll
-      for (int c = 0; c < 32; ++c) red_add_f32(dst + (c + 32) * qs, __uint_as_float(r1[c]));
-      return;
-    }
-    // stage dQ[q][d] (fp32) in this warpgroup's 16 KB buffer, 32 queries at a time,
-    // each half one bulk tensor reduce-add into the fp32 dQ accumulator
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      if (hf == 1) {  // the first half's reduce must have read the buffer
-        if (row == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        named_bar_sync(wg_bar, 128);
-      }
-      const uint32_t(&rv)[32] = hf ? r1 : r0;
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)(c * 128 + row) * 4),
-                     "f"(__uint_as_float(rv[c]))
-                     : "memory");
-      fence_proxy_async_smem();
-      named_bar_sync(wg_bar, 128);
-      if (row == 0) {
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
-            " [%0, {%1, %2, %3}], [%4];" ::"l"(tmdq),
-            "r"(0), "r"(h), "r"(j * 64 + hf * 32), "r"(pdbuf)
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
-#if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
-    if (row == 0) MT_TL(7, seq);
-#endif
-    staging_busy = true;
+  uint32_t dn = 0;  // drain-ring entries posted
+  auto post = [&](int kind, int h, int j, uint32_t b, uint32_t pre, int seq) {  // one thread
+    const uint32_t sl = dn % kDrainRing;
+    mbar_wait(smem_u32(&sm.dmfree[sl]), ((dn / kDrainRing) & 1) ^ 1);
+    DrainMeta& d = sm.dring[sl];
+    d.kbp = kind | (int)(b << 8) | (int)((pre & 1u) << 9);
+    d.h = h;
+    d.j = j;
+    d.seq = seq;
+    mbar_arrive(smem_u32(&sm.dmfull[sl]));
   };
 
   for (;;) {
@@ -663,19 +669,32 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
     bool had_chunk = false;
     int tile = -1;
     for (;;) {
-      if (row == 0) MT_CRUMB(3 + wg, 1000000 + (int)su);
-      mbar_wait(sfull, su & 1);
-      ++su;
-      const ChunkMeta cm = sm.smeta[wg];
+      const uint32_t b = e & 1;
+      if (row == 0) MT_CRUMB(3 + hf, 1000000 + (int)e);
+      mbar_wait(smem_u32(&sm.sfull[b]), (e >> 1) & 1);
+      ++e;
+      const ChunkMeta cm = sm.smeta[b];
       if (cm.kind == kEnd || cm.kind == kDone) {
         tile = cm.kind == kEnd ? cm.tile : -1;
         break;
       }
+      const uint32_t pre = b ? rc1 : rc0;
+      if (b) ++rc1; else ++rc0;
       if (P.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
 #ifndef MT_TL_WARPS
-      if (row == 0) MT_TL(4, cm.seq);
+#ifndef MT_TL_ISSUER2
+      if (hrow == 0) MT_TL(4, cm.seq);
+#endif
 #endif
       tc_fence_after();
+      if (P.dbg & 2) {  // knock-out: no softmax work, publish at once
+        tc_fence_before();
+        mbar_arrive(smem_u32(&sm.dsfull[b]));
+        if (hrow == 0) post(kChunk, cm.h, cm.j, b, pre, cm.seq);
+        ++dn;
+        had_chunk = true;
+        continue;
+      }
       // which of the 64 queries see this key row
       uint64_t vis;
       if (P.mode == kModeBlock) {
@@ -691,66 +710,67 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         }
         vis = live ? ~0ull : 0ull;
       }
-      // per-query constants of the chunk, once: -LSE log2(e) and -D / sqrt(d)
-      float* nl = sm.lse[cm.stage];
-      float* nd = sm.dd[cm.stage];
-      if (row < 64)
+      // per-query constants of this half, once: -LSE log2(e) and -D / sqrt(d)
+      float* nl = sm.lse[cm.stage] + 32 * hf;
+      float* nd = sm.dd[cm.stage] + 32 * hf;
+      if (row < 32)
         nl[row] = -nl[row] * 1.4426950408889634f;
-      else
-        nd[row - 64] = -nd[row - 64] * P.inv_sqrt_d;
-      named_bar_sync(wg_bar, 128);
-      uint32_t pk[32], dk[32];
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // 32 queries at a time (register budget)
+      else if (row < 64)
+        nd[row - 32] = -nd[row - 32] * P.inv_sqrt_d;
+      named_bar_sync(hf_bar, 128);
+      const uint32_t R = tmem + lb + kColR + 128 * b;  // this chunk's region (own lanes)
+      uint32_t pk[16], dk[16];
+      {
         uint32_t sv[32], dpv[32];
         tmem_ld32(R + 32 * hf, sv);
         tmem_ld32(R + 64 + 32 * hf, dpv);
         tmem_ld_wait();
         const uint32_t vh = (uint32_t)(vis >> (32 * hf));
         if (vh == 0xffffffffu)
-          softmax_half<false>(sv, dpv, nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
-                              pk + 16 * hf, dk + 16 * hf);
+          softmax_half<false>(sv, dpv, nl, nd, P.scale_log2, P.inv_sqrt_d, vh, pk, dk);
         else
-          softmax_half<true>(sv, dpv, nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
-                             pk + 16 * hf, dk + 16 * hf);
+          softmax_half<true>(sv, dpv, nl, nd, P.scale_log2, P.inv_sqrt_d, vh, pk, dk);
       }
-      // P^T, dS^T over S^T in this warpgroup's TMEM region (A of dV, dK)
-#ifdef MT_TL_WGSPLIT
-      if (row == 0) MT_TL(6, cm.seq);  // math done
-#endif
-      tmem_st32(R, pk);
-      tmem_st32(R + 32, dk);
-      wait_staging();  // the previous chunk's dQ reduce has read the buffer
-#ifdef MT_TL_WGSPLIT
-      if (row == 0) MT_TL(7, cm.seq);  // staging buffer free
-#endif
+      // P^T, dS^T over this half's S^T columns (A of dV, dK); dS^T also -> SMEM (B of dQ^T),
+      // into the region's buffer once the drain warps' dQ staging of its previous chunk
+      // has been read by the bulk reduce
+      tmem_st16(R + 32 * hf, pk);
+      tmem_st16(R + 32 * hf + 16, dk);
+      if (pre > 0) mbar_wait(smem_u32(&sm.dqdone[b]), (pre - 1) & 1);
+      const uint32_t drow = smem_u32(sm.pd[b]) + row * 128;
 #pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) {
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int c16 = 4 * hf + c4;
         const uint32_t sw = (uint32_t)((c16 ^ (row & 7)) << 4);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + sw), "r"(dk[4 * c16]),
-                     "r"(dk[4 * c16 + 1]), "r"(dk[4 * c16 + 2]), "r"(dk[4 * c16 + 3])
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + sw), "r"(dk[4 * c4]),
+                     "r"(dk[4 * c4 + 1]), "r"(dk[4 * c4 + 2]), "r"(dk[4 * c4 + 3])
                      : "memory");
       }
       tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(dsfull);
-#ifdef MT_TL_WARPS
-      if (lane == 0) MT_TL(4 + quad, cm.seq);  // per-warp publish times (quad 0..3)
-#else
-      if (row == 0) MT_TL(5, cm.seq);
+      mbar_arrive(smem_u32(&sm.dsfull[b]));
+#ifndef MT_TL_WARPS
+#ifndef MT_TL_ISSUER2
+      if (hrow == 0) MT_TL(5, cm.seq);
 #endif
-      drain_dq(cm.h, cm.j, cm.seq);
+#endif
+      if (hrow == 0) post(kChunk, cm.h, cm.j, b, pre, cm.seq);  // its dQ^T -> the drain warps
+      ++dn;
       had_chunk = true;
     }
+    if (hrow == 0) post(tile < 0 ? kDone : kEnd, 0, 0, 0, 0, 0);
+    ++dn;
     if (tile < 0) break;  // DONE
+    // every chunk drained (all gradient MMAs complete, staging buffers read)
+    mbar_wait(smem_u32(&sm.tdrained), ntile & 1);
     const Tile T = decode_tile(P, tile);
-    wait_staging();  // the epilogue stages dK/dV in the same buffer
-    tc_fence_after();
-    if (row == 0) sm.tile_chunks[wg] = had_chunk ? 1 : 0;
+    const bool any_chunk = had_chunk;  // else TMEM dK/dV is stale
+    const int wg = hf;
+    const uint32_t pdbuf = smem_u32(sm.pd[wg]);
+    const uint32_t wg_bar = hf_bar;
     if (row == 0) MT_CRUMB(3 + wg, 5000000 + (int)ntile);
-    named_bar_sync(3, 256);  // both warpgroups: every MMA of the tile complete
-    const bool any_chunk = (sm.tile_chunks[0] | sm.tile_chunks[1]) != 0;  // else TMEM is stale
+    tc_fence_after();
 
     // ---- dK (warpgroup 0) / dV (warpgroup 1) epilogue: the tile's key rows
     bool live_row;
@@ -814,6 +834,102 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   }
 }
 
+// ------------------------------------------------------------------ dQ drain
+// Warpgroup 3: per published chunk (in order), once its gradient MMAs are done, read dQ^T
+// (lanes = d, 64 query columns) from TMEM -- which frees the region for the next chunk's
+// dP^T -- then stage dQ[q][d] (fp32) 32 queries at a time in the region's 16 KB buffer and
+// bulk reduce-add it into the fp32 dQ accumulator.  Off the softmax warps' path, so a
+// region is free ~G + 500 cycles after its chunk was published.
+__device__ void drain_warps(Smem& sm, const Params& P, uint32_t tmem, const CUtensorMap* tmdq) {
+  const int quad = warp_id() & 3, lane = lane_id();
+  const int row = quad * 32 + lane;          // d of dQ^T == TMEM lane
+  const int dt = (int)threadIdx.x - 384;     // 0..127
+  const uint32_t lb = (uint32_t)(quad * 32) << 16;
+  constexpr uint32_t kBarDrain = 4;
+  uint32_t ntile = 0;
+  for (uint32_t n = 0;; ++n) {
+    const uint32_t sl = n % kDrainRing;
+    mbar_wait(smem_u32(&sm.dmfull[sl]), (n / kDrainRing) & 1);
+    const DrainMeta dm = sm.dring[sl];
+    mbar_arrive(smem_u32(&sm.dmfree[sl]));
+    const int kind = dm.kbp & 0xff;
+    const uint32_t b = (uint32_t)(dm.kbp >> 8) & 1u, pre = (uint32_t)(dm.kbp >> 9) & 1u;
+    if (kind == kDone) break;
+    if (kind == kEnd) {  // the previous entries' reduces have read their buffers
+      if (dt == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(smem_u32(&sm.tdrained));
+      }
+      ++ntile;
+      continue;
+    }
+    mbar_wait(smem_u32(&sm.gdone[b]), pre);  // dQ^T complete
+    if (dt == 0) MT_TL(6, dm.seq);
+    tc_fence_after();
+    uint32_t r0[32], r1[32];
+    const uint32_t R = tmem + lb + kColR + 128 * b + 64;
+    tmem_ld32(R, r0);
+    tmem_ld32(R + 32, r1);
+    tmem_ld_wait();
+    tc_fence_before();
+    mbar_arrive(smem_u32(&sm.dqfree[b]));
+    if (dt == 0) MT_TL(7, dm.seq);
+    if (!(P.dbg & 1) && P.dq_red) {
+      // 4 x 4 transposes inside each lane quad: lane (d = 4a + i) ends up with query q0 + i
+      // at d = 4a .. 4a + 3, one 16-B vector reduction per 4 queries (no SMEM traffic)
+      const int qi = lane & 3;
+      float* base = P.dq + ((size_t)dm.j * 64 * P.plan.Hq + dm.h) * 128 + (row & ~3);
+      const size_t qs = (size_t)P.plan.Hq * 128;
+#pragma unroll
+      for (int q0 = 0; q0 < 64; q0 += 4) {
+        const uint32_t* x = q0 < 32 ? &r0[q0] : &r1[q0 - 32];
+        float y[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          // round r: read lane (quad base | (qi + r) & 3), which sends its x[(src - r) & 3]
+          const int si = (qi - r) & 3;  // what THIS lane sends in round r
+          const uint32_t send = si == 0 ? x[0] : si == 1 ? x[1] : si == 2 ? x[2] : x[3];
+          const uint32_t got = r == 0 ? send
+                                      : __shfl_sync(0xffffffffu, send, (lane & ~3) | ((qi + r) & 3));
+          y[(qi + r) & 3] = __uint_as_float(got);
+        }
+        float* dst = base + (size_t)(q0 + qi) * qs;
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(y[0]),
+                     "f"(y[1]), "f"(y[2]), "f"(y[3])
+                     : "memory");
+      }
+    } else if (!(P.dbg & 1)) {
+      const uint32_t buf = smem_u32(sm.pd[b]);  // its dQ^T MMA (the reader) is complete
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        if (hf == 1) {  // the first half's reduce must have read the buffer
+          if (dt == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          named_bar_sync(kBarDrain, 128);
+        }
+        const uint32_t(&rv)[32] = hf ? r1 : r0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(buf + (uint32_t)(c * 128 + row) * 4),
+                       "f"(__uint_as_float(rv[c]))
+                       : "memory");
+        fence_proxy_async_smem();
+        named_bar_sync(kBarDrain, 128);
+        if (dt == 0) {
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+              " [%0, {%1, %2, %3}], [%4];" ::"l"(tmdq),
+              "r"(0), "r"(dm.h), "r"(dm.j * 64 + hf * 32), "r"(buf)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      if (dt == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    if (dt == 0) mbar_arrive(smem_u32(&sm.dqdone[b]));
+  }
+  (void)ntile;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmdo,
@@ -834,11 +950,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&sm.kvfull), 1);
     mbar_init(smem_u32(&sm.kvempty), 1);
     mbar_init(smem_u32(&sm.tfree), 1);
+    mbar_init(smem_u32(&sm.tdrained), 1);
+    for (int i = 0; i < kDrainRing; ++i) {
+      mbar_init(smem_u32(&sm.dmfull[i]), 1);
+      mbar_init(smem_u32(&sm.dmfree[i]), 128);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.sfull[b]), 2);
-      mbar_init(smem_u32(&sm.dsfull[b]), 128);
+      mbar_init(smem_u32(&sm.dsfull[b]), 256);
       mbar_init(smem_u32(&sm.gdone[b]), 1);
       mbar_init(smem_u32(&sm.dqfree[b]), 128);
+      mbar_init(smem_u32(&sm.dqdone[b]), 1);
     }
     fence_barrier_init();
   }
@@ -868,14 +990,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t c = 0;; ++c) {
         const uint32_t st = c % kStages;
         mbar_wait(smem_u32(&sm.full[st]), (c / kStages) & 1);
+#ifndef MT_TL_ISSUER2
         if (lane_id() == 0) MT_TL(1, c);
+#endif
         if (sm.meta[st].kind == kDone) break;
       }
     }
 #endif
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+  } else if (warp < 12) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 184;" ::: "memory");
     softmax_bwd(sm, P, tmem, &tmdq, &tmdk, &tmdv);
+    if (threadIdx.x % 128 == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
+    drain_warps(sm, P, tmem, &tmdq);
     if (threadIdx.x % 128 == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
@@ -924,6 +1052,7 @@ __global__ void f32_to_bf16_kernel(const float* x, __nv_bfloat16* y, int64_t n) 
 
 }  // namespace bwd
 
+static_assert(sizeof(bwd::Smem) <= 232448, "backward SMEM exceeds 227 KB");
 size_t bwd_smem_bytes() { return sizeof(bwd::Smem); }  // the dynamic base is 1024-aligned
 
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
@@ -971,6 +1100,8 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.static_tiles = static_tiles;
   static const int dbg = getenv("MT_BWD_DBG") ? atoi(getenv("MT_BWD_DBG")) : 0;
   P.dbg = dbg;
+  static const int dq_red = getenv("MT_BWD_DQ_RED") ? atoi(getenv("MT_BWD_DQ_RED")) : 0;
+  P.dq_red = dq_red;
   // q heads per block-pass tile: 4 by default (MT_BWD_HPT overrides), the largest divisor
   // of the GQA group size not above it; block-CSR mode keeps one head per tile.  Measured
   // (profiles/r01_bwd_hpt_ab.json): the K/V load and dK/dV epilogue of a tile are shared by
@@ -991,13 +1122,11 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
       make_tmap_bf16_3d(&tmv, v, 128, plan.Hkv, S_loc, 64, 1, 64))
     return fail(MT_ECUDA, "cuTensorMapEncodeTiled failed");
   const size_t smem = bwd_smem_bytes();
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_bwd) failed");
-    attr_done = true;
-  }
+  // set on every launch: the attribute applies to the current device only (a process may
+  // drive several GPUs), and the call is cheap next to the launch
+  if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_bwd) failed");
   // block (slash) part
   cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);  // one tile counter per launch
   P.mode = kModeBlock;
@@ -1012,7 +1141,11 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.tile_counter = plan.scratch + 3;
   P.mode = kModeBar;
   P.hpt = 1;
-  P.bar_part_len = nloc < 1024 ? (nloc > 0 ? nloc : 1) : 1024;
+  // query blocks per bar-tile part: 1024 (MT_BWD_BAR_PART overrides, so tests reach the
+  // multi-part path at sizes the oracle checks in full)
+  static const int part_env = getenv("MT_BWD_BAR_PART") ? atoi(getenv("MT_BWD_BAR_PART")) : 1024;
+  const int part_len = part_env > 0 ? part_env : 1024;
+  P.bar_part_len = nloc < part_len ? (nloc > 0 ? nloc : 1) : part_len;
   P.bar_parts = (nloc + P.bar_part_len - 1) / P.bar_part_len;
   P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128) * P.bar_parts;
   grid = num_sms;
