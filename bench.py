@@ -92,6 +92,13 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+def workload_name(args, W: int) -> str:
+    cfg = {4096: "C1", 65536: "C2", 131072: "C3", 524288: "C4", 1048576: "C5"}.get(args.seq, "custom")
+    ring = "flat" if not args.inner or args.inner == W else f"{W // args.inner}x{args.inner}"
+    return (f"{cfg}-shape layer at W={W}: S={args.seq}, Hq={args.hq}, Hkv={args.hkv}, d=128, "
+            f"p_v=p_s={args.p}, {ring} ring")
+
+
 # ------------------------------------------------------------------ layout helpers
 def stripe_rows(S: int, W: int, r: int) -> np.ndarray:
     """Global token of each local row of rank r (64-token block striping)."""
@@ -105,56 +112,110 @@ def bits_to_torch(bits: np.ndarray, dev):
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def oracle_sample(q, k, v, dO, p: float, S: int, Hq: int, Hkv: int, n_blocks: int = 384):
-    """Time the CPU oracle on a bounded sample of the workload; returns a dict.
+def blas_threads() -> int | None:
+    try:
+        from threadpoolctl import threadpool_info
+        np.ones((64, 64)) @ np.ones((64, 64))  # load the BLAS so it is reported
+        n = [x["num_threads"] for x in threadpool_info() if x.get("user_api") == "blas"]
+        return int(max(n)) if n else None
+    except Exception:
+        return None
 
-    Sample: the full Alg. 1 index of q head 0 (VS-IDX v1, C fast path) and the
-    fp64 forward + backward of `n_blocks` query blocks of head 0 spread over the
-    sequence.  Extrapolated to the whole job by head count (index) and by the
-    activated-pair count (attention).
+
+class OracleSampler:
+    """The CPU oracle (oracle/, test infrastructure) timed on a bounded sample of the
+    workload -- the `cpu_baseline` of our arm and every step of `--impl reference`
+    (identical code and sample size, so the two legs agree within noise).
+
+    Setup (untimed): the oracle's own Alg. 1 index of every q head (C helper, VS-IDX v1)
+    and the true activated-pair total, counted by oracle.attention.count_pairs.
+    One sampled step (timed): the full Alg. 1 index of ONE q head (head i mod Hq on step
+    i) and the fp64 forward + backward of `n_blocks` query blocks of that head spread over
+    the sequence.  Extrapolation to the whole job: index time x Hq, attention time x
+    (total activated pairs / sampled pairs).  So `value` is a projection of tokens/s for
+    the full workload; `sample_seconds` is what a step really took.
     """
+
+    def __init__(self, q, k, v, dO, p: float, S: int, Hq: int, Hkv: int, n_blocks: int = 48):
+        from oracle import attention as OA
+        from oracle import vsidx
+        from synth.generator import bf16_bits_to_f32
+        self.q, self.k, self.v, self.dO = q, k, v, dO
+        self.p, self.S, self.Hq, self.Hkv, self.nb_sample = p, S, Hq, Hkv, n_blocks
+        self.grp = Hq // Hkv
+        t0 = time.perf_counter()
+        self.iv, self.is_ = vsidx.build_vs_index(bf16_bits_to_f32(q), bf16_bits_to_f32(k), p, p)
+        self.setup_index_s = time.perf_counter() - t0
+        self.pairs = OA.count_pairs(self.iv, self.is_, S)
+        self.total_pairs = int(self.pairs.sum())
+        self.step_i = 0
+
+    def step(self) -> dict:
+        from oracle import attention as OA
+        from oracle import sparseformat as SF
+        from oracle import vsidx
+        from synth.generator import bf16_bits_to_f32
+        S, h = self.S, self.step_i % self.Hq
+        self.step_i += 1
+        g_kv = h // self.grp
+        f64 = lambda x: bf16_bits_to_f32(x).astype(np.float64)
+        t_start = time.perf_counter()
+        q_win = np.ascontiguousarray(bf16_bits_to_f32(self.q[S - 64:, h]))
+        kk = np.ascontiguousarray(bf16_bits_to_f32(self.k[:, g_kv]))
+        t0 = time.perf_counter()
+        iv, is_ = vsidx.vs_index_head(q_win, kk, self.p, self.p)
+        t_idx = time.perf_counter() - t0
+        assert np.array_equal(iv, self.iv[h]) and np.array_equal(is_, self.is_[h])
+        nb = S // 64
+        gs = np.unique(np.linspace(0, nb - 1, self.nb_sample).astype(int))
+        qh, kh, vh, dh = (f64(x[:, c:c + 1]) for x, c in
+                          ((self.q, h), (self.k, g_kv), (self.v, g_kv), (self.dO, h)))
+        O = np.zeros_like(qh)
+        L = np.zeros((1, S))
+        pairs = 0
+        t0 = time.perf_counter()
+        for g in gs:
+            B, C = SF.sparseformat_block(iv, is_, int(g))
+            rows = slice(g * 64, g * 64 + 64)
+            O[rows, 0], L[0, rows] = OA.forward_block(qh, kh, vh, 0, int(g), B, C)
+            OA.backward_block(qh, kh, vh, O, L, dh, 0, int(g), B, C)
+            pairs += int(OA.count_pairs([iv], [is_], S, rows=[int(g)])[0])
+        t_attn = time.perf_counter() - t0
+        t_job = t_idx * self.Hq + t_attn * self.total_pairs / max(pairs, 1)
+        return {"value": S / t_job, "unit": UNIT, "kind": "oracle",
+                "cores": len(os.sched_getaffinity(0)), "blas_threads": blas_threads(),
+                "sample": (f"q head {h}: Alg. 1 index in full ({t_idx:.2f} s, x{self.Hq} heads) + "
+                           f"fp64 fwd+bwd of {len(gs)} of {nb} query blocks ({t_attn:.2f} s, "
+                           f"{pairs} of {self.total_pairs} activated pairs, all heads counted); "
+                           f"projected to the whole {S}-token job"),
+                "sample_seconds": time.perf_counter() - t_start,
+                "projected_seconds_per_step": t_job}
+
+
+def oracle_c1_full() -> dict:
+    """The oracle on BASELINE config C1 (4K tokens, 8 q / 1 kv heads) IN FULL: Alg. 1 index
+    of every head, fp64 sparse forward and backward of every row."""
     from oracle import attention as OA
-    from oracle import sparseformat as SF
     from oracle import vsidx
-    from paper_2510_18830_b200 import stats
-    from synth.generator import bf16_bits_to_f32
-    grp = Hq // Hkv
-    qf = bf16_bits_to_f32(q[:, :1])
-    kf = bf16_bits_to_f32(k[:, :1])
+    from synth.generator import bf16_bits_to_f32, make_grad_out, make_qkv
+    S, Hq, Hkv = 4096, 8, 1
+    q, k, v = make_qkv(S, Hq, Hkv, seed=0)
+    dO = make_grad_out(S, Hq, seed=0)
+    f64 = lambda x: bf16_bits_to_f32(x).astype(np.float64)
     t0 = time.perf_counter()
-    iv, is_ = vsidx.vs_index_head(np.ascontiguousarray(qf[S - 64:, 0]), np.ascontiguousarray(kf[:, 0]), p, p)
-    t_idx = time.perf_counter() - t0
-    nb = S // 64
-    gs = np.unique(np.linspace(0, nb - 1, n_blocks).astype(int))
-    q64 = qf.astype(np.float64)
-    k64 = kf.astype(np.float64)
-    v64 = bf16_bits_to_f32(v[:, :1]).astype(np.float64)
-    d64 = bf16_bits_to_f32(dO[:, :1]).astype(np.float64)
-    O = np.zeros_like(q64)
-    L = np.zeros((1, S))
-    pairs = 0
-    t0 = time.perf_counter()
-    for g in gs:
-        B, C = SF.sparseformat_block(iv, is_, int(g))
-        rows = slice(g * 64, g * 64 + 64)
-        O[rows, 0], L[0, rows] = OA.forward_block(q64, k64, v64, 0, int(g), B, C)
-        OA.backward_block(q64, k64, v64, O, L, d64, 0, int(g), B, C)
-        pairs += int(len(B) * 4096 - (2016 if (len(B) and B[-1] == g) else 0) + 64 * len(C))
-    t_attn = time.perf_counter() - t0
-    tot_pairs = int(stats.pairs_per_head([iv], [is_], S)[0]) * Hq
-    t_job = t_idx * Hq + t_attn * tot_pairs / max(pairs, 1)
-    return {"value": S / t_job, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-            "sample": (f"Alg.1 index of 1/{Hq} q heads ({t_idx:.1f} s) + fp64 fwd+bwd of {len(gs)} of "
-                       f"{nb} query blocks of head 0 ({t_attn:.1f} s, {pairs} of {tot_pairs} pairs); "
-                       f"extrapolated by heads and activated pairs"),
-            "seconds": t_idx + t_attn}
+    iv, is_ = vsidx.build_vs_index(bf16_bits_to_f32(q), bf16_bits_to_f32(k), 0.9, 0.9)
+    O, L = OA.sparse_attention_forward(f64(q), f64(k), f64(v), iv, is_)
+    OA.sparse_attention_backward(f64(q), f64(k), f64(v), O, L, f64(dO), iv, is_)
+    t = time.perf_counter() - t0
+    return {"workload": "C1: S=4096, Hq=8, Hkv=1, p=0.9, index + fwd + bwd in full",
+            "seconds": round(t, 3), "tokens_per_s": S / t}
 
 
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2510_18830_b200 import ops, stats
+    from paper_2510_18830_b200 import _lib, ops, stats
     from synth.generator import make_grad_out, make_qkv
 
     W = int(os.environ.get("WORLD_SIZE", "1"))
@@ -208,19 +269,33 @@ def run_ours(args):
     pairs = int(stats.pairs_per_head(iv, is_, S).sum())
     dens = pairs / (Hq * stats.causal_pairs(S))
 
+    # L2 rule (B200_PROFILING.md): inputs larger than L2 between timed steps, else an L2
+    # flush between steps (outside the per-step CUDA-event windows)
+    L2_BYTES = 126 * 2 ** 20
+    in_bytes = sum(x.numel() * x.element_size() for x in (qd, kd, vd, dOd))
+    flush = None if in_bytes > 2 * L2_BYTES else torch.empty(4 * L2_BYTES, dtype=torch.uint8, device=dev)
+    lib = _lib.lib()
     clocks = Clocks(local)
     barrier()
     torch.cuda.synchronize()
+    n_launch0, n_lib0 = lib.mt_launch_count(), lib.mt_library_call_count()
     t0, t1 = ev(), ev()
     marks = []
     t0.record(stream)
     for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1)
         step(qd, kd, vd, dOd, marks)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    n_launch = lib.mt_launch_count() - n_launch0
+    n_lib = lib.mt_library_call_count() - n_lib0
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
+    if flush is None:
+        ms = t0.elapsed_time(t1)
+    else:  # sum of the steps' own windows (index start -> backward end), flushes excluded
+        ms = float(sum(m[0].elapsed_time(m[3]) for m in marks))
     ph = np.array([[m[0].elapsed_time(m[1]), m[1].elapsed_time(m[2]), m[2].elapsed_time(m[3])]
                    for m in marks]).mean(axis=0)
     t_max = torch.tensor([ms], device=dev)
@@ -352,20 +427,31 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded RoPE vertical-slash generator, DESIGN.md §3)",
-            "config": {"workload": f"{ {4096: 'C1', 65536: 'C2', 131072: 'C3', 524288: 'C4', 1048576: 'C5'}.get(S, 'custom') }-shape layer at W={W}: S={S}, Hq={Hq}, Hkv={Hkv}, d=128, "
-                                   f"p_v=p_s={p}, {'flat' if not args.inner or args.inner == W else f'{W // args.inner}x{args.inner}'} ring",
+            "config": {"workload": workload_name(args, W),
                        "seq_len": S, "global_batch": 1, "parallelism": f"cp{W}",
                        "density": round(dens, 4), "activated_pairs": pairs,
-                       "l2": "inputs larger than L2 (Q alone 2 GiB)",
+                       "l2": (f"inputs larger than L2: Q/K/V/dO {in_bytes / 2 ** 30:.2f} GiB per rank "
+                              f"vs 126 MB L2" if flush is None else
+                              f"L2 flushed between steps (inputs {in_bytes / 2 ** 20:.1f} MiB per rank "
+                              f"fit the 126 MB L2); per-step CUDA-event windows summed"),
                        **({"emulated_inter_node": {"gbps": float(os.environ["MT_EMU_INTER_GBPS"]),
                                                    "ranks_per_node": int(os.environ.get("MT_EMU_NODE", args.inner or W))}}
                           if os.environ.get("MT_EMU_INTER_GBPS") else {})},
             "roofline": roof, "e2e": e2e, "clocks": clk,
             **({"ring": ring} if ring else {}),
-            "gpu_launches": args.steps * (17 if W == 1 else 16 + 7 * W)}
+            # counted by libmtsa.so over the timed region (max over ranks is not needed: every
+            # rank launches the same kernels); CUB sorts are library calls, counted apart
+            "gpu_launches": int(n_launch),
+            "gpu_launches_detail": {"own_kernels_per_step": n_launch / args.steps,
+                                    "cub_radix_sort_calls_per_step": n_lib / args.steps}}
     if rank == 0 and W == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = {kk: vv for kk, vv in oracle_sample(q, k, v, dO, p, S, Hq, Hkv).items()
-                                if kk != "seconds"}
+        smp = OracleSampler(q, k, v, dO, p, S, Hq, Hkv)
+        runs = [smp.step() for _ in range(3)]
+        cb = dict(runs[-1])
+        cb["value"] = float(np.median([r["value"] for r in runs]))
+        cb["sample"] = (f"median of 3 sampled steps (q heads 0-2), each: " + runs[-1]["sample"])
+        cb["c1_full"] = oracle_c1_full()
+        line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
@@ -375,6 +461,9 @@ def run_ours(args):
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The CPU oracle as the reference arm (tier framing): each of the W + K steps is one
+    OracleSampler step (the same code and sample size as our arm's cpu_baseline) of the
+    same workload; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -382,23 +471,26 @@ def run_reference(args):
     S, Hq, Hkv, p = args.seq, args.hq, args.hkv, args.p
     q, k, v = make_qkv(S, Hq, Hkv, seed=args.seed)
     dO = make_grad_out(S, Hq, seed=args.seed)
-    vals = []
-    last = None
-    for i in range(args.warmup + args.steps):
-        r = oracle_sample(q, k, v, dO, p, S, Hq, Hkv, n_blocks=48)
-        if i >= args.warmup:
-            vals.append(r["value"])
-        last = r
-    val = float(np.median(vals))
+    smp = OracleSampler(q, k, v, dO, p, S, Hq, Hkv)
+    runs = [smp.step() for _ in range(args.warmup + args.steps)][args.warmup:]
+    val = float(np.median([r["value"] for r in runs]))
+    wall = [r["sample_seconds"] for r in runs]
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": S / val * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (attention), f32/u64 (index)",
+            "warmup": args.warmup,
+            # each step really took sample_seconds; the projected time of a full step is
+            # reported beside it (value is the projection's tokens/s)
+            "ms_per_step": float(np.mean(wall)) * 1e3,
+            "projected_ms_per_full_step": S / val * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64 (attention), f32/u64 (index)",
             "data": "synthetic (seeded RoPE vertical-slash generator, DESIGN.md §3)",
-            "config": {"workload": f"C4-shape layer: S={S}, Hq={Hq}, Hkv={Hkv}, d=128, p_v=p_s={p}",
-                       "seq_len": S, "global_batch": 1, "parallelism": "cpu"},
+            "config": {"workload": workload_name(args, args.gpus), "seq_len": S, "global_batch": 1,
+                       "parallelism": f"cp{args.gpus} (the oracle runs on rank 0's host cores)"},
             "impl": "reference",
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
-                             "sample": last["sample"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": runs[-1]["cores"],
+                             "blas_threads": runs[-1]["blas_threads"], "kind": "oracle",
+                             "sample": f"median of {len(runs)} sampled steps, each: " + runs[-1]["sample"],
+                             "setup_index_seconds": round(smp.setup_index_s, 2)},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

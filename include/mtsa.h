@@ -57,6 +57,13 @@ typedef enum {
 /* Thread-local description of the last non-MT_OK status returned on this thread. */
 const char* mt_last_error(void);
 
+/* Process-wide counters (for benchmarks; thread-safe, monotone):
+ *   mt_launch_count       kernels this library has enqueued (its own sm_100a kernels);
+ *   mt_library_call_count CUB radix-sort calls it has enqueued (each launches several
+ *                         CUB kernels compiled into this library).                   */
+unsigned long long mt_launch_count(void);
+unsigned long long mt_library_call_count(void);
+
 /* Problem shape.  seq_len is the GLOBAL sequence length S. */
 typedef struct {
   int64_t seq_len;

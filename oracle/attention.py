@@ -160,15 +160,17 @@ def sparse_attention_backward(q, k, v, O, LSE, dO, i_v, i_s, block: int = BLOCK)
     return dQ, dK, dV
 
 
-def count_pairs(i_v, i_s, S: int, block: int = BLOCK):
-    """Activated (n, m) pairs per head = sum_n |K_n| (the FLOP unit)."""
+def count_pairs(i_v, i_s, S: int, block: int = BLOCK, rows=None):
+    """Activated (n, m) pairs per head = sum_n |K_n| (the FLOP unit),
+    over all query blocks or only the query blocks listed in `rows`."""
+    from .sparseformat import sparseformat_block
     out = []
     for h in range(len(i_v)):
-        B, C = sparseformat(i_v[h], i_s[h], S, block)
         tot = 0
-        for g in range(S // block):
-            nblk = len(B[g])
-            diag = 1 if (len(B[g]) and B[g][-1] == g) else 0
-            tot += (nblk - diag) * block * block + diag * block * (block + 1) // 2 + block * len(C[g])
+        for g in (range(S // block) if rows is None else rows):
+            B, C = sparseformat_block(i_v[h], i_s[h], g, block)
+            nblk = len(B)
+            diag = 1 if (len(B) and B[-1] == g) else 0
+            tot += (nblk - diag) * block * block + diag * block * (block + 1) // 2 + block * len(C)
         out.append(tot)
     return np.array(out, np.int64)

@@ -103,13 +103,17 @@ _SIGS: dict[str, list] = {
     "mt_vs_format_count": [P, P, P, P, P, P, P, SZ, P],
     "mt_vs_format_fill": [P, P, P, P, P, I64, P, I64, I64, I64, P, SZ, P],
     "mt_unstripe": [I64, I64, I, I, P, P, P],
+    "mt_launch_count": [],
+    "mt_library_call_count": [],
 }
 _RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
             "mt_build_vs_index_workspace_bytes": ctypes.c_size_t,
             "mt_sparse_attn_bwd_workspace_bytes": ctypes.c_size_t,
             "mt_attn_step_workspace_bytes": ctypes.c_size_t,
             "mt_ring_attn_workspace_bytes": ctypes.c_size_t,
-            "mt_vs_format_workspace_bytes": ctypes.c_size_t}
+            "mt_vs_format_workspace_bytes": ctypes.c_size_t,
+            "mt_launch_count": ctypes.c_ulonglong,
+            "mt_library_call_count": ctypes.c_ulonglong}
 
 
 def declared_symbols() -> list[str]:

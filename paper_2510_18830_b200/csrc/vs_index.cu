@@ -494,6 +494,7 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
   const dim3 grid((unsigned)((S_loc + kThreads - 1) / kThreads), Hq);
   stage1_launch(grid, g, w.qwin, static_cast<const __nv_bfloat16*>(k_loc), w.t, w.M, st);
+  count_launches(1);  // fill_f32
   MT_TRY(check_launch("vs stage1"));
   if (coll) MT_TRY(coll->allreduce_max(w.M, (size_t)Hq * 64, st));
   stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
@@ -515,6 +516,7 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
     if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysV, w.sortV, (int)(Hq * S), 0,
                                        kScoreBits + kv.ib + kv.hb, st) != cudaSuccess)
       return fail(MT_ECUDA, "radix sort (verticals) failed");
+    count_library_calls(1);
   } else {
     for (int h = 0; h < Hq; ++h) {  // per head: a device-wide sort
       tb = w.cub_bytes;
@@ -522,6 +524,7 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
                                          w.sortV + (size_t)h * S, (int)S, 0, kScoreBits + kv.ib,
                                          st) != cudaSuccess)
         return fail(MT_ECUDA, "radix sort (verticals) failed");
+      count_library_calls(1);
     }
   }
   tb = w.cub_bytes;
@@ -529,12 +532,15 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
     if (cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb), 0,
                                        kScoreBits + kp.ib + kp.hb, st) != cudaSuccess)
       return fail(MT_ECUDA, "radix sort (slashes) failed");
+    count_library_calls(1);
   } else {
     seg_offsets<<<1, 64, 0, st>>>(w.segP, Hq, nb);
+    count_launches(1);
     if (cub::DeviceSegmentedRadixSort::SortKeys(w.cub_tmp, tb, w.keysP, w.sortP, (int)(Hq * nb),
                                                 Hq, w.segP, w.segP + 1, 0, kScoreBits + kp.ib,
                                                 st) != cudaSuccess)
       return fail(MT_ECUDA, "segmented sort (slashes) failed");
+    count_library_calls(1);
   }
   cudaMemsetAsync(w.bitsV, 0, (size_t)Hq * ((S + 31) / 32) * 4, st);
   cudaMemsetAsync(w.bitsP, 0, (size_t)Hq * ((nb + 31) / 32) * 4, st);
@@ -614,5 +620,6 @@ extern "C" mt_status mt_vs_column_scores(const mt_shape* sh, const void* q, cons
   stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
   stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, w.keysV, w.keysP, col_scores,
                                            slash_scores, key_layout(S, Hq), key_layout(S / 64, Hq));
+  count_launches(3);  // fill_f32, stage 1, stage 2 (+ stage 3 in check_launch)
   return check_launch("mt_vs_column_scores");
 }

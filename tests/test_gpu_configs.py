@@ -63,12 +63,14 @@ def test_c2_64k_full_parity(cuda_lib):
     assert e_l <= TOL_LSE and max(errs.values()) <= TOL, (errs, e_l)
 
 
-class _Lazy64:
-    def __init__(self, bits):
-        self.bits, self.shape = bits, bits.shape
+class _Fixed:
+    """Stand-in for the oracle's O / LSE arrays holding one query block's rows."""
+
+    def __init__(self, val):
+        self.val = val
 
     def __getitem__(self, key):
-        return bf16_bits_to_f32(self.bits[key]).astype(np.float64)
+        return self.val
 
 
 def test_c3_128k_bar_columns_and_sink(cuda_lib):
@@ -85,46 +87,39 @@ def test_c3_128k_bar_columns_and_sink(cuda_lib):
     torch.cuda.synchronize()
     o, lse = o.float().cpu().numpy(), lse.cpu().numpy()
     dk, dv = dk.float().cpu().numpy(), dv.float().cpu().numpy()
-    qf, kf, vf, df = (_Lazy64(x) for x in (q, k, v, dO))
-    # sampled key columns of kv group 0: sinks, head 0's first bar group, key block 1
+    # kv group 0 as a one-head problem for the oracle (its q heads one at a time)
+    k0, v0 = f64(k[:, 0:1]), f64(v[:, 0:1])
+    # sampled key columns: sinks, head 0's first bar group (128 columns), key block 1
     cols = np.unique(np.r_[np.arange(4), np.asarray(riv[0])[:128], np.arange(64, 128)])
-    colset = set(cols.tolist())
+    pos = {int(c): i for i, c in enumerate(cols)}
+    colblk = set((cols // 64).tolist())
     rdk = np.zeros((len(cols), 128))
     rdv = np.zeros((len(cols), 128))
-    pos = {c: i for i, c in enumerate(cols)}
     got_o, ref_o, got_l, ref_l = [], [], [], []
     rng = np.random.default_rng(3)
     sample_g = set(rng.choice(nb, 6, replace=False).tolist()) | {0, nb - 1}
     for h in range(grp):                       # q heads of kv group 0
+        qh, dOh = f64(q[:, h:h + 1]), f64(dO[:, h:h + 1])
         for g in range(nb):
             B, C = sparseformat_block(riv[h], ris[h], g)
             rows = slice(g * 64, g * 64 + 64)
-            Og, Lg = OA.forward_block(qf, kf, vf, h, g, B, C)
+            Og, Lg = OA.forward_block(qh, k0, v0, 0, g, B, C)
             if g in sample_g:
                 got_o.append(o[rows, h]); ref_o.append(Og)
                 got_l.append(lse[h, rows]); ref_l.append(Lg)
-            # keys of this block among the sampled columns (the contribution of a key
-            # needs only its scores and the row's LSE / D, so a key subset is exact)
-            Bs = np.array([kb for kb in B if any((kb * 64 + x) in colset for x in range(64))], np.int64)
-            Cs = np.array([m for m in C if m in colset], np.int64)
+            # the contribution of a key needs only its scores and the row's LSE / D, so
+            # the oracle's block backward on the sampled key subset is exact for them
+            Bs = np.array([kb for kb in B if int(kb) in colblk], np.int64)
+            Cs = np.array([m for m in C if int(m) in pos], np.int64)
             if not len(Bs) and not len(Cs):
                 continue
-            Orow = {(g * 64, h): Og}
-            Lrow = {(h, g * 64): Lg}
-
-            class _O:
-                def __getitem__(self, key):
-                    return Orow[(key[0].start, key[1])]
-
-            class _L:
-                def __getitem__(self, key):
-                    return Lrow[(key[0], key[1].start)]
-
-            _, keys, dkb, dvb = OA.backward_block(qf, kf, vf, _O(), _L(), df, h, g, Bs, Cs)
-            for x, m in enumerate(keys):
-                if m in pos:
-                    rdk[pos[m]] += dkb[x]
-                    rdv[pos[m]] += dvb[x]
+            # backward_block reads O[rows, h, :] and LSE[h, rows] of this block only
+            _, keys, dkb, dvb = OA.backward_block(qh, k0, v0, _Fixed(Og), _Fixed(Lg), dOh, 0, g,
+                                                  Bs, Cs)
+            for xk, m in enumerate(keys):
+                if int(m) in pos:
+                    rdk[pos[int(m)]] += dkb[xk]
+                    rdv[pos[int(m)]] += dvb[xk]
     e = {"dk": normwise_err(dk[cols, 0][:, None], rdk[:, None], 1),
          "dv": normwise_err(dv[cols, 0][:, None], rdv[:, None], 1),
          "dk_sink": normwise_err(dk[:4, 0][:, None], rdk[:4][:, None], 1),

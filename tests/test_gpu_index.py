@@ -99,3 +99,31 @@ def test_index_sort_paths_agree(cuda_lib, tmp_path, S, Hq, Hkv):
     assert len(got) == len(ref.files)
     for i, x in enumerate(got):
         assert np.array_equal(x, ref[f"arr_{i}"]), i
+
+
+def test_column_scores_bitexact_extreme_values(cuda_lib):
+    # VS-IDX I1 is a fused multiply-add fold (reading R11): the GPU's __fmaf_rn and the
+    # oracle's exact sums must agree on EVERY bf16 input, including products below fp32's
+    # subnormal range (2^-149) and subnormal partial sums, where a separately rounded
+    # product would differ.  Planted: 20% of the keys scaled by 2^-120, 20% of the window
+    # queries by 2^-40 (products ~2^-160), plus bf16 subnormals.
+    from synth.generator import f32_to_bf16_bits
+    S, Hq, Hkv = 4096, 4, 2
+    q, k, _ = make_qkv(S, Hq, Hkv, seed=17)
+    r = np.random.default_rng(18)
+    qf, kf = bf16_bits_to_f32(q).copy(), bf16_bits_to_f32(k).copy()
+    kf[r.random(kf.shape) < 0.2] *= np.float32(2.0 ** -120)
+    qf[r.random(qf.shape) < 0.2] *= np.float32(2.0 ** -40)
+    kf[r.random(kf.shape) < 0.01] = np.float32(2.0 ** -130)   # bf16 subnormal
+    q, k = f32_to_bf16_bits(qf), f32_to_bf16_bits(kf)
+    col, sl = ops.vs_column_scores(to_dev_bf16(q), to_dev_bf16(k))
+    torch.cuda.synchronize()
+    ref_c, ref_s = _oracle_scores(q, k)
+    assert np.array_equal(col.cpu().numpy().view(np.uint64), ref_c)
+    assert np.array_equal(sl.cpu().numpy().view(np.uint64), ref_s)
+    idx = ops.build_vs_index(to_dev_bf16(q), to_dev_bf16(k), 0.9, 0.9)
+    torch.cuda.synchronize()
+    iv, is_ = idx.to_lists()
+    riv, ris = vsidx.build_vs_index(bf16_bits_to_f32(q), bf16_bits_to_f32(k), 0.9, 0.9)
+    for h in range(Hq):
+        assert np.array_equal(iv[h], riv[h]) and np.array_equal(is_[h], ris[h]), h

@@ -155,6 +155,12 @@ def test_count_pairs_matches_mask():
     cnt = A.count_pairs(iv, is_, S)
     for h in range(2):
         assert cnt[h] == SF.union_mask(iv[h], is_[h], S).sum()
+    # restricted to some query blocks: the mask rows of those blocks
+    blocks = [0, 2, 3]
+    sub = A.count_pairs(iv, is_, S, rows=blocks)
+    for h in range(2):
+        m = SF.union_mask(iv[h], is_[h], S)
+        assert sub[h] == sum(m[g * 64:(g + 1) * 64].sum() for g in blocks)
 
 
 def test_gqa_mapping_equals_repeat_interleaved_mha():
