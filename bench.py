@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as one CUDA graph (auto: single GPU and S <= 128K, where "
+                         "the step is launch-bound)")
     return ap.parse_args()
 
 
@@ -296,9 +299,42 @@ def run_ours(args):
         ms = t0.elapsed_time(t1)
     else:  # sum of the steps' own windows (index start -> backward end), flushes excluded
         ms = float(sum(m[0].elapsed_time(m[3]) for m in marks))
+    eager_ms = ms
+    # ---- CUDA-graph replay of the whole step (index + fwd + bwd: ~17 own kernels and the
+    # CUB sorts, launch-bound at small S).  Captured once after the eager warm-up; each
+    # timed replay recomputes everything from the same device inputs.
+    graph_info = None
+    use_graph = args.graph == "on" or (args.graph == "auto" and W == 1 and S <= 131072)
+    if use_graph and W == 1:
+        g_stream = torch.cuda.Stream(device=dev)
+        g_stream.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(g_stream):
+            step(qd, kd, vd, dOd)  # allocations of the step's outputs happen before capture
+            with torch.cuda.graph(graph, stream=g_stream):
+                step(qd, kd, vd, dOd)
+        stream.wait_stream(g_stream)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        n_launch0 = lib.mt_launch_count()
+        gms = []
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            a_, b_ = ev(), ev()
+            a_.record(stream)
+            graph.replay()
+            b_.record(stream)
+            gms.append((a_, b_))
+        torch.cuda.synchronize()
+        ms = float(sum(a_.elapsed_time(b_) for a_, b_ in gms))
+        graph_info = {"replayed_ms_per_step": ms / args.steps, "eager_ms_per_step": eager_ms / args.steps,
+                      "note": "value = CUDA-graph replay of the step; phase_ms and roofline from the eager "
+                              "pass (per-phase CUDA events)"}
     ph = np.array([[m[0].elapsed_time(m[1]), m[1].elapsed_time(m[2]), m[2].elapsed_time(m[3])]
                    for m in marks]).mean(axis=0)
-    t_max = torch.tensor([ms], device=dev)
+    t_max = torch.tensor([ms], device=dev)  # eager or graph-replay total
     if W > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
@@ -438,6 +474,7 @@ def run_ours(args):
                                                    "ranks_per_node": int(os.environ.get("MT_EMU_NODE", args.inner or W))}}
                           if os.environ.get("MT_EMU_INTER_GBPS") else {})},
             "roofline": roof, "e2e": e2e, "clocks": clk,
+            **({"cuda_graph": graph_info} if graph_info else {}),
             **({"ring": ring} if ring else {}),
             # counted by libmtsa.so over the timed region (max over ranks is not needed: every
             # rank launches the same kernels); CUB sorts are library calls, counted apart
