@@ -142,12 +142,20 @@ size_t mt_build_vs_index_workspace_bytes(const mt_shape* shape, int world);
  * against all causal keys, softmax in specified fixed point, column
  * sums (token level) and 64x64-pooled block-diagonal sums, exact
  * integer top-p budgets, argtopk with ties to the smaller index,
- * forced column 0 and offset 0.  The result is bit-identical to the CPU oracle
- * and independent of `world`.
+ * forced column 0 and offset 0.  The window scores are a fold of fused
+ * multiply-adds (the bf16 x bf16 product is not rounded on its own, reading R11),
+ * so the result is bit-identical to the CPU oracle for EVERY bf16 input
+ * (subnormals, products below 2^-149 and huge values included; NaN/Inf inputs
+ * give unspecified lists) and independent of `world`.
  *   comm == NULL : single GPU; q [S][Hq][128], k [S][Hkv][128].
  *   comm != NULL : q/k are this rank's block-striped local slices
  *                  [S/W][.][128]; every rank receives the same global lists.
  * out: caller-allocated, v_stride >= S, s_stride >= S/64 (MT_ECAPACITY).
+ * Caller-supplied indices (any call taking an mt_vs_index) must hold lists like
+ * this function's: strictly ascending, columns in [0, S), offsets in [0, S/64),
+ * offset 0 present; strides below (S, S/64) are MT_ESHAPE.  Out-of-range entries
+ * are dropped by the plan builder (no out-of-bounds writes), other violations
+ * give unspecified attention results.
  * Errors: MT_ESHAPE, MT_EWINDOW (S < 64 or S % 64), MT_ECONFIG (p outside
  * (0, 1]), MT_ELAYOUT, MT_EWORKSPACE, MT_EUNSUPPORTED, MT_ECUDA, MT_ENCCL. */
 mt_status mt_build_vs_index(mt_comm* comm, const mt_shape* shape, const mt_vs_params* params,
@@ -258,6 +266,22 @@ mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* shape, const void* q_l
                            const float* lse_loc, const void* dO_loc, const mt_vs_index* idx,
                            void* dq_loc, void* dk_loc, void* dv_loc, void* ws, size_t ws_bytes,
                            mt_stream_t stream);
+
+/* Copy-engine transport for the flat forward ring.  Collective: every
+ * rank of `comm` calls it with the workspace it will pass to mt_ring_attn_fwd / _bwd
+ * (ws_bytes >= the ring workspace + mt_ring_flags_bytes(); the last 256 bytes are reserved
+ * flag words and must not be touched between ring calls).  The ring neighbours'
+ * workspaces are then mapped through CUDA IPC, and the forward ring moves each step's KV
+ * chunk with cudaMemcpyAsync into the next rank's receive slot (copy engines over NVLink:
+ * no SM, so the transfer overlaps the persistent attention kernel), ordered by stream
+ * memory operations (cuStreamWaitValue32 / WriteValue32) on monotone step counters.  Where
+ * IPC or peer access is unavailable on any rank, the call succeeds and the ring keeps NCCL
+ * send/recv (mt_comm_copy_engine reports which).  Registering again (e.g. after the
+ * workspace moved) replaces the mappings; ring calls with another workspace use NCCL.
+ * Synchronizes `stream`.  Errors: MT_ESHAPE, MT_EWORKSPACE, MT_ECUDA, MT_ENCCL. */
+size_t mt_ring_flags_bytes(void);
+mt_status mt_comm_register_workspace(mt_comm* comm, void* ws, size_t ws_bytes, mt_stream_t stream);
+int mt_comm_copy_engine(mt_comm* comm);
 
 /* Host-only: the ring schedule — out[t * world + x] = origin of the KV chunk
  * rank x holds at step t, for a ring of `world` ranks with `inner` ranks per

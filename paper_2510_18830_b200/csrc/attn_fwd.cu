@@ -98,7 +98,7 @@ struct Smem {
   uint8_t q[kTileQ2];   // [d-atom c][128 rows: head 0's 64 queries, head 1's][128 B]
   ChunkMeta meta[kKSt];
   VMeta vmeta[kVM];
-  SMeta smeta[2];
+  SMeta smeta[3];
   alignas(16) float m[128];         // row stabilisers of the tile (log2 domain)
   alignas(16) float lsum[2][128];   // per warpgroup: row sums of its chunks
   int stage_rows[192];
@@ -110,7 +110,7 @@ struct Smem {
   uint32_t sbits[2][kSbitsWords];  // the tile heads' slash bitmaps (producer warp only)
   int ovf[2];  // per tile parity: some row of the tile overflowed its stabiliser
   uint64_t kfull[kKSt], kempty[kKSt], vfull[kVSt], vempty[kVSt];
-  uint64_t sfull[2], sfree[2], pfull[2], obar[2];
+  uint64_t sfull[3], sfree[3], pfull[3], obar[2];
   uint64_t edone;  // the softmax warps finished a tile's epilogue (obar's phase is theirs)
   uint64_t vmfull[kVM], vmfree[kVM];
   uint64_t qfull, qempty, mready;
@@ -140,8 +140,26 @@ struct Params {
   int single;         // 1: one head per tile (block-CSR mode), rows 64-127 dead
 };
 
-// TMEM: O [0, 128), S / P buffers [128, 256) [256, 384)
+// TMEM: O [0, 128), three S / P buffers at [128 + 128 b, 256 + 128 b): chunk k of a tile
+// uses buffer k % 3 and softmax warpgroup k % 2, so S(k + 1), S(k + 2) run on the tensor
+// core while warpgroup k % 2 works on chunk k.
+constexpr int kNB = 3;
 constexpr uint32_t kColO = 0, kColS = 128;
+
+// per-buffer event counters packed in one word (10 bits each: only parities are used)
+__device__ __forceinline__ uint32_t cnt_get(uint32_t c, uint32_t b) { return (c >> (10 * b)) & 1023u; }
+__device__ __forceinline__ uint32_t cnt_inc(uint32_t c, uint32_t b) {
+  return (c & ~(1023u << (10 * b))) | (((cnt_get(c, b) + 1u) & 1023u) << (10 * b));
+}
+// buffer of softmax warpgroup w's next event when a tile has closed after n chunks
+__device__ __forceinline__ uint32_t end_buffer(uint32_t n, uint32_t w) {
+  return (n + ((n & 1u) != w ? 1u : 0u)) % kNB;
+}
+// events a tile of n chunks puts on buffer b: its chunks k = b (mod 3) and END(s)
+__device__ __forceinline__ uint32_t tile_events(uint32_t n, uint32_t b) {
+  const uint32_t chunks = n > b ? (n - 1u - b) / kNB + 1u : 0u;
+  return chunks + (end_buffer(n, 0) == b ? 1u : 0u) + (end_buffer(n, 1) == b ? 1u : 0u);
+}
 
 // tile -> (first head h0, second head h1 or -1, local query block j)
 __device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h0, int& h1, int& j) {
@@ -562,15 +580,16 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const uint64_t dv0 = make_sdesc(smem_u32(sm.v[0]), 16384, 1024);
   uint32_t c = 0, dc = 0, oc = 0, qf_phase = 0;  // K slots, data chunks S-issued, O-issued
   uint32_t nt = 0;                               // tiles closed (obar commits)
-  uint32_t pu0 = 0, pu1 = 0;                     // P publications consumed per buffer
-  uint32_t su0 = 0, su1 = 0;                     // events published per buffer (sfree phases)
-  // smeta[b] may be rewritten once warpgroup b has read the previous event's copy
+  bool o_started = false;
+  uint32_t pcnt = 0;  // per buffer: P publications consumed (pfull phases)
+  uint32_t ecnt = 0;  // per buffer: events published (sfree phases)
+  // smeta[b] may be rewritten once the warpgroup that read the previous event took its copy
   auto wait_sfree = [&](uint32_t b) {
     MT_CRUMB(0, 40 + (int)b);
-    if (b == 0) { if (su0 > 0) mbar_wait(smem_u32(&sm.sfree[0]), (su0 - 1) & 1); ++su0; }
-    else        { if (su1 > 0) mbar_wait(smem_u32(&sm.sfree[1]), (su1 - 1) & 1); ++su1; }
+    const uint32_t n = cnt_get(ecnt, b);
+    if (n > 0) mbar_wait(smem_u32(&sm.sfree[b]), (n - 1) & 1);
+    ecnt = cnt_inc(ecnt, b);
   };
-  bool o_started = false;
   int kind_ring[4] = {0, 0, 0, 0};
   uint32_t buf_ring[4] = {0, 0, 0, 0};
   // O += P V for the oldest data chunk not yet accumulated (oc)
@@ -582,8 +601,8 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     MT_CRUMB(0, 30 + (int)b);
     if (leader) MT_TL(7, oc);
     if (kind_ring[oc & 3] == kBar) fence_proxy_async_smem();
-    if (b == 0) { mbar_wait(smem_u32(&sm.pfull[0]), pu0 & 1); ++pu0; }
-    else        { mbar_wait(smem_u32(&sm.pfull[1]), pu1 & 1); ++pu1; }
+    mbar_wait(smem_u32(&sm.pfull[b]), cnt_get(pcnt, b) & 1);
+    pcnt = cnt_inc(pcnt, b);
     tc_fence_after();
     const uint64_t dv = sdesc_add(dv0, vs * kTileKV);
     const uint32_t pb = tmem + kColS + 128 * b;  // P: keys 2c, 2c+1 packed in column c
@@ -598,12 +617,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     o_started = true;
     ++oc;
   };
-  auto publish = [&](int kind, int tile) {  // END / DONE to both softmax warpgroups
-    for (uint32_t b = 0; b < 2; ++b) {
+  // END / DONE to both softmax warpgroups, each on the buffer its next chunk would use
+  auto publish = [&](int kind, int tile, uint32_t n) {
+    for (uint32_t w = 0; w < 2; ++w) {
+      const uint32_t b = end_buffer(n, w);
       wait_sfree(b);
       if (leader) {
         sm.smeta[b].kind = kind;
         sm.smeta[b].tile = tile;
+        sm.smeta[b].n = (int)n;  // lets both warpgroups account every buffer's events
         mbar_arrive(smem_u32(&sm.sfull[b]));
         mbar_arrive(smem_u32(&sm.sfull[b]));
       }
@@ -614,7 +636,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint32_t ks = c % kKSt;
       mbar_wait(smem_u32(&sm.kfull[ks]), (c / kKSt) & 1);
       if (sm.meta[ks].kind == kDone) {
-        publish(kDone, -1);
+        publish(kDone, -1, 0);
         break;
       }
     }
@@ -645,12 +667,12 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         if (nt > 0) mbar_wait(smem_u32(&sm.edone), (nt - 1) & 1);
         if (leader) mma_commit(smem_u32(&sm.obar[0]));  // the tile's O complete
         ++nt;
-        publish(kEnd, end_tile);
+        publish(kEnd, end_tile, k);
         break;
       }
       if (leader) MT_TL(6, dc);
-      if (dc - oc >= 2) issue_o();  // O(k-2) before S(k) overwrites its P buffer
-      const uint32_t b = k & 1;
+      if (dc - oc >= (uint32_t)kNB) issue_o();  // O(k-3) before S(k) overwrites its P buffer
+      const uint32_t b = k % kNB;
       wait_sfree(b);
       if (leader) {
         sm.smeta[b].seq = (int)dc;
@@ -686,6 +708,21 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^t on the FMA / ALU pipes (a quarter of the exponentials, so the MUFU pipe -- 16 ex2
+// per clock per SM, the forward's bound at 128 x 128 chunks -- is not the only source):
+// t = j + f with j = rint(t) through the 1.5 * 2^23 shift, f in [-0.5, 0.5], 2^f by a cubic
+// (max relative error 1.0e-4, fitted on [-0.5, 0.5]; P is rounded to bf16 anyway), 2^j
+// added to the exponent field.  t is clamped at -125 (2^-125 is a zero weight for bf16).
+__device__ __forceinline__ float ex2_poly(float t) {
+  t = fmaxf(t, -125.f);
+  const float r = t + 12582912.f;
+  const float f = t - (r - 12582912.f);
+  float p = fmaf(0.05500765f, f, 0.24220801f);
+  p = fmaf(p, f, 0.69328274f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+}
+
 // Live keys (bit c = key 32 cg + c) of this thread's query row in one 32-key group.
 __device__ __forceinline__ uint32_t live_bits(const SMeta& cm, int x, int i, int cg) {
   if (cm.kind == kBlk) {
@@ -715,24 +752,32 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
   const uint32_t lb = ((uint32_t)(quad * 32) << 16);
   const int Hq = P.plan.Hq;
   const int64_t S_loc = (int64_t)P.nloc * 64;
-  const uint32_t sfull = smem_u32(&sm.sfull[wg]), pfull = smem_u32(&sm.pfull[wg]);
   const uint32_t mready = smem_u32(&sm.mready);
-  const uint32_t Sb = tmem + lb + kColS + 128 * wg;
   const float sc = P.scale_log2;
-  uint32_t su = 0, mr_phase = 0, ntile = 0;
+  // base: events published on each buffer before the current tile (both warpgroups'); the
+  // buffer-b event of chunk k is number base[b] + k / 3, END's follows the tile's chunks
+  uint32_t base = 0, mr_phase = 0, ntile = 0;
 
   for (;;) {
     float m = -INFINITY, l = 0.f;
     bool m_synced = false, ovf = false;
     int tile = -1;
-    for (;;) {
-      if (row == 0) MT_CRUMB(3 + wg, 1000000 + (int)su);
-      mbar_wait(sfull, su & 1);
-      ++su;
-      const SMeta cm = sm.smeta[wg];
-      mbar_arrive(smem_u32(&sm.sfree[wg]));  // the copy is taken: smeta[wg] reusable
+    for (uint32_t k = (uint32_t)wg;; k += 2) {  // this warpgroup's chunks of the tile
+      const uint32_t b = k % kNB;
+      if (row == 0) MT_CRUMB(3 + wg, 1000000 + (int)k);
+      // the k-th chunk index is an END when the tile closed before it: END's event number
+      // on b is base[b] + (chunks of the tile on b) = base[b] + k / 3 as well
+      mbar_wait(smem_u32(&sm.sfull[b]), (cnt_get(base, b) + k / kNB) & 1);
+      const SMeta cm = sm.smeta[b];
+      mbar_arrive(smem_u32(&sm.sfree[b]));  // the copy is taken: smeta[b] reusable
+      const uint32_t Sb = tmem + lb + kColS + 128 * b;
+      const uint32_t pfull = smem_u32(&sm.pfull[b]);
       if (cm.kind == kEnd || cm.kind == kDone) {
         tile = cm.kind == kEnd ? cm.tile : -1;
+        const uint32_t n = (uint32_t)cm.n;
+#pragma unroll
+        for (uint32_t bb = 0; bb < (uint32_t)kNB; ++bb)
+          base = (base & ~(1023u << (10 * bb))) | (((cnt_get(base, bb) + tile_events(n, bb)) & 1023u) << (10 * bb));
         break;
       }
       if (row == 0) MT_TL(4, cm.seq);
@@ -778,7 +823,8 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
           for (int cc = 0; cc < 32; cc += 2) {
             const float t0 = fmaf(__uint_as_float(sv[cc]), sc, -m);
             const float t1 = fmaf(__uint_as_float(sv[cc + 1]), sc, -m);
-            const float p0 = ex2(t0), p1 = ex2(t1);
+            const float p0 = ex2(t0);
+            const float p1 = (cc & 2) ? ex2_poly(t1) : ex2(t1);
             emax = fmaxf(emax, fmaxf(t0, t1));
             la += p0;
             lb2 += p1;
@@ -925,12 +971,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&sm.vfull[s]), 1);
       mbar_init(smem_u32(&sm.vempty[s]), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       mbar_init(smem_u32(&sm.sfull[b]), 2);
-      mbar_init(smem_u32(&sm.sfree[b]), 128);  // smeta[b] read by softmax warpgroup b
-      mbar_init(smem_u32(&sm.pfull[b]), 128);  // buffer b belongs to softmax warpgroup b
-      mbar_init(smem_u32(&sm.obar[b]), 1);
+      mbar_init(smem_u32(&sm.sfree[b]), 128);  // smeta[b] read by the chunk's warpgroup
+      mbar_init(smem_u32(&sm.pfull[b]), 128);  // P of the chunk in buffer b written
     }
+    for (int b = 0; b < 2; ++b) mbar_init(smem_u32(&sm.obar[b]), 1);
     mbar_init(smem_u32(&sm.qfull), 1);
     mbar_init(smem_u32(&sm.qempty), 1);
     mbar_init(smem_u32(&sm.mready), 128);

@@ -10,7 +10,9 @@
 // the single-GPU result.
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
 #include <thread>
+#include <vector>
 
 #include "comm.cuh"
 #include "vsidx.cuh"
@@ -200,6 +202,7 @@ extern "C" mt_status mt_comm_destroy(mt_comm* c) {
   if (!c) return MT_OK;
   prof_free(c);
 #ifdef MT_HAVE_NCCL
+  mt::ce_release(c);
   if (c->nccl3) ncclCommDestroy(c->nccl3);
   if (c->nccl2) ncclCommDestroy(c->nccl2);
   if (c->nccl) ncclCommDestroy(c->nccl);
@@ -238,3 +241,166 @@ mt_status mt_build_vs_index_dist(mt_comm* comm, const mt_shape* sh, const mt_vs_
   return fail(MT_EUNSUPPORTED, "built without NCCL");
 #endif
 }
+
+// ------------------------------------------------------------------ copy-engine ring
+#ifdef MT_HAVE_NCCL
+#include <cudaTypedefs.h>
+
+namespace mt {
+namespace {
+struct CeHandle {
+  cudaIpcMemHandle_t h;
+  uint64_t off;    // workspace offset inside its allocation
+  uint64_t bytes;  // registered workspace bytes
+  int32_t dev;
+  int32_t pad;
+};
+
+PFN_cuMemGetAddressRange_v3020 get_range() {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &p, 3020, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+void ce_release(mt_comm* c) {
+  if (c->ce_next_map) cudaIpcCloseMemHandle(c->ce_next_map);
+  if (c->ce_prev_map && c->ce_prev_map != c->ce_next_map) cudaIpcCloseMemHandle(c->ce_prev_map);
+  c->ce_next_map = c->ce_prev_map = nullptr;
+  c->ce_next_ws = c->ce_prev_ws = nullptr;
+  c->ce_ws = nullptr;
+  c->ce_ok = false;
+}
+
+CeStreamValueFn ce_wait_fn() {
+  static CeStreamValueFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<CeStreamValueFn>(p);
+  });
+  return fn;
+}
+
+CeStreamValueFn ce_write_fn() {
+  static CeStreamValueFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<CeStreamValueFn>(p);
+  });
+  return fn;
+}
+}  // namespace mt
+#endif
+
+extern "C" size_t mt_ring_flags_bytes(void) { return 256; }
+
+extern "C" mt_status mt_comm_register_workspace(mt_comm* c, void* ws, size_t ws_bytes,
+                                                mt_stream_t stream) {
+#ifdef MT_HAVE_NCCL
+  if (!c || !ws) return fail(MT_ESHAPE, "NULL argument");
+  if (ws_bytes < 4096) return fail(MT_EWORKSPACE, "workspace too small to register");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  mt::ce_release(c);
+  const int W = c->world, r = c->rank;
+  if (W < 2) return MT_OK;
+  // my handle, gathered from every rank over NCCL (the exchange uses the first W * 96
+  // bytes of the workspace as scratch; the flag words at its end are zeroed first)
+  CeHandle mine{};
+  bool ok = true;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  auto range = mt::get_range();
+  if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(ws)) != CUDA_SUCCESS ||
+      cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) != cudaSuccess)
+    ok = false;
+  cudaGetLastError();
+  mine.off = ok ? (uint64_t)(reinterpret_cast<uintptr_t>(ws) - (uintptr_t)base) : 0;
+  mine.bytes = ok ? ws_bytes : 0;  // 0: this rank cannot share (everyone falls back)
+  cudaGetDevice(&mine.dev);
+  uint8_t* scratch = static_cast<uint8_t*>(ws);
+  const size_t hb = sizeof(CeHandle);
+  if (cudaMemsetAsync(static_cast<uint8_t*>(ws) + ws_bytes - 256, 0, 256, st) != cudaSuccess ||
+      cudaMemcpyAsync(scratch + (size_t)W * hb, &mine, hb, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail(MT_ECUDA, "register: staging failed");
+  MT_TRY(nccl_check(ncclAllGather(scratch + (size_t)W * hb, scratch, hb, ncclUint8, c->nccl, st),
+                    "register all-gather"));
+  std::vector<CeHandle> all(W);
+  if (cudaMemcpyAsync(all.data(), scratch, (size_t)W * hb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return fail(MT_ECUDA, "register: handle copy failed");
+  for (int i = 0; i < W; ++i) ok = ok && all[i].bytes > 0;
+  const int nx = (r + 1) % W, pv = (r - 1 + W) % W;
+  if (ok) {
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, mine.dev, all[nx].dev);
+    ok = can != 0;
+    cudaDeviceCanAccessPeer(&can, mine.dev, all[pv].dev);
+    ok = ok && can != 0;
+  }
+  if (ok) {
+    if (cudaIpcOpenMemHandle(&c->ce_next_map, all[nx].h, cudaIpcMemLazyEnablePeerAccess) !=
+        cudaSuccess) {
+      c->ce_next_map = nullptr;
+      ok = false;
+    }
+  }
+  if (ok) {
+    if (pv == nx) {
+      c->ce_prev_map = c->ce_next_map;
+    } else if (cudaIpcOpenMemHandle(&c->ce_prev_map, all[pv].h, cudaIpcMemLazyEnablePeerAccess) !=
+               cudaSuccess) {
+      c->ce_prev_map = nullptr;
+      ok = false;
+    }
+  }
+  cudaGetLastError();
+  // every rank must agree: an all-reduce(min) of the local verdicts; it also orders every
+  // rank's flag zeroing before any rank's first remote flag write
+  int32_t* flag = reinterpret_cast<int32_t*>(scratch);
+  const int32_t okv = ok ? 1 : 0;
+  if (cudaMemcpyAsync(flag, &okv, 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail(MT_ECUDA, "register: verdict copy failed");
+  MT_TRY(nccl_check(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, c->nccl, st), "register verdict"));
+  int32_t all_ok = 0;
+  if (cudaMemcpyAsync(&all_ok, flag, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return fail(MT_ECUDA, "register: verdict readback failed");
+  if (!all_ok) {
+    mt::ce_release(c);
+    return MT_OK;  // the ring keeps its NCCL transport
+  }
+  c->ce_ws = ws;
+  c->ce_bytes = ws_bytes;
+  c->ce_next_ws = static_cast<uint8_t*>(c->ce_next_map) + all[nx].off;
+  c->ce_next_bytes = all[nx].bytes;
+  c->ce_prev_ws = static_cast<uint8_t*>(c->ce_prev_map) + all[pv].off;
+  c->ce_prev_bytes = all[pv].bytes;
+  c->ce_calls = 0;
+  c->ce_ok = true;
+  return MT_OK;
+#else
+  (void)c; (void)ws; (void)ws_bytes; (void)stream;
+  return fail(MT_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+extern "C" int mt_comm_copy_engine(mt_comm* c) { return (c && c->ce_ok) ? 1 : 0; }

@@ -43,9 +43,29 @@ struct mt_comm {
   // step (env MT_RING_RESERVE_SMS / MT_RING_RESERVE_SMS_BWD; 0 = off).
   int reserve_sms = 0;
   int reserve_sms_bwd = 0;
+  // Copy-engine KV ring (flat forward; mt_comm_register_workspace).  The ring neighbours'
+  // registered workspaces are mapped through CUDA IPC; a step's KV chunk is written into
+  // the next rank's receive slot by cudaMemcpyAsync on comm_stream (copy engines over
+  // NVLink: no SM, so the transfer overlaps the persistent attention kernel), ordered by
+  // stream memory operations on monotone 32-bit counters in the workspaces' flag words.
+  void* ce_ws = nullptr;          // my registered workspace
+  size_t ce_bytes = 0;
+  void* ce_next_map = nullptr;    // IPC mapping of rank r+1's allocation (base)
+  uint8_t* ce_next_ws = nullptr;  // rank r+1's registered workspace, in this address space
+  size_t ce_next_bytes = 0;
+  void* ce_prev_map = nullptr;    // same for rank r-1
+  uint8_t* ce_prev_ws = nullptr;
+  size_t ce_prev_bytes = 0;
+  uint32_t ce_calls = 0;          // forward ring calls since registration (identical on all ranks)
+  bool ce_ok = false;
 };
 
+#include <cuda.h>
 namespace mt {
+// cuStreamWaitValue32 / cuStreamWriteValue32 (driver API, fetched by entry point)
+typedef CUresult (*CeStreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+// Release the copy-engine ring's IPC mappings (mt_comm_register_workspace).
+void ce_release(mt_comm* c);
 // Emulated wire time of `bytes` arriving at rank c->rank from rank `from` (no-op
 // unless emulation is on and the two ranks sit on different emulated nodes).
 void emu_inbound(mt_comm* c, int from, size_t bytes, cudaStream_t st);

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "comm.cuh"
+#include <cudaTypedefs.h>
 #include "plan.cuh"
 
 namespace mt {
@@ -242,6 +243,91 @@ struct KVRing {
 }  // namespace
 }  // namespace mt
 
+#ifdef MT_HAVE_NCCL
+namespace mt {
+CeStreamValueFn ce_wait_fn();
+CeStreamValueFn ce_write_fn();
+namespace {
+// Flat forward ring over the copy engines (mt_comm_register_workspace).  Counters (uint32,
+// monotone since registration; waits compare the signed difference, so they wrap safely):
+//   ready  (my flag word 0, written by rank r-1): KV transfers received;
+//   done   (my flag word 16, written by rank r+1): compute steps rank r+1 has finished.
+// In call e (calls since registration) at step t:
+//   send (t < W-1): comm stream waits ready >= e(W-1) + t (the chunk I hold arrived; t >= 1),
+//                   and done >= eW + t (rank r+1 finished its steps < t, so its receive slot
+//                   t % 2 -- last read at step t-1 or in an earlier call -- is free);
+//                   copies K and V into rank r+1's slot t % 2 (cudaMemcpyAsync: copy engines,
+//                   no SM), then writes rank r+1's ready = e(W-1) + t + 1;
+//   compute:        waits ready >= e(W-1) + t (t >= 1), runs step t on slot (t-1) % 2, then
+//                   writes rank r-1's done = eW + t + 1.
+mt_status ring_fwd_ce(mt_comm* c, const std::vector<std::vector<int>>& sched, const VSPlan& plan,
+                      int r, int nloc, int64_t S_loc, int Hkv, const void* q_loc, const void* k_loc,
+                      const void* v_loc, void* o_loc, float* o_acc, float* lse_loc,
+                      uint8_t* const* kv, uint8_t* ws, cudaStream_t stream) {
+  auto wait = ce_wait_fn();
+  auto write = ce_write_fn();
+  if (!wait || !write) return fail(MT_EUNSUPPORTED, "stream memory operations unavailable");
+  const int W = c->world;
+  const uint32_t e = c->ce_calls++;
+  const size_t half = (size_t)S_loc * Hkv * 128 * sizeof(__nv_bfloat16);
+  uint32_t* my_flags = reinterpret_cast<uint32_t*>(ws + c->ce_bytes - 256);
+  uint32_t* next_ready = reinterpret_cast<uint32_t*>(c->ce_next_ws + c->ce_next_bytes - 256);
+  uint32_t* prev_done = reinterpret_cast<uint32_t*>(c->ce_prev_ws + c->ce_prev_bytes - 256) + 16;
+  const CUdeviceptr d_ready = reinterpret_cast<CUdeviceptr>(my_flags);
+  const CUdeviceptr d_done = reinterpret_cast<CUdeviceptr>(my_flags + 16);
+  const uint32_t rbase = e * (uint32_t)(W - 1), cbase = e * (uint32_t)W;
+  cudaStream_t cs = c->comm_stream;
+  // the caller's chunk is complete once the compute stream reaches this point
+  cudaEventRecord(c->ev_ready, stream);
+  cudaStreamWaitEvent(cs, c->ev_ready, 0);
+  const __nv_bfloat16* curK = static_cast<const __nv_bfloat16*>(k_loc);
+  const __nv_bfloat16* curV = static_cast<const __nv_bfloat16*>(v_loc);
+  cudaEvent_t ev_sent;  // the send of step t read the chunk compute step t reads
+  cudaEventCreateWithFlags(&ev_sent, cudaEventDisableTiming);
+  for (int t = 0; t < W; ++t) {
+    if (t >= 1) {
+      curK = reinterpret_cast<const __nv_bfloat16*>(kv[(t - 1) & 1]);
+      curV = curK + half / sizeof(__nv_bfloat16);
+    }
+    if (t < W - 1) {  // ---- send the chunk held at step t to rank r+1's slot t % 2
+      if (t >= 1 && wait(cs, d_ready, rbase + (uint32_t)t, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(MT_ECUDA, "cuStreamWaitValue32 (ready)");
+      if (wait(cs, d_done, cbase + (uint32_t)t, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(MT_ECUDA, "cuStreamWaitValue32 (done)");
+      uint8_t* dst = c->ce_next_ws + (kv[t & 1] - ws);
+      prof_mark(c, 0, t, RingProfile::kInnerB, cs);
+      if (cudaMemcpyAsync(dst, curK, half, cudaMemcpyDeviceToDevice, cs) != cudaSuccess ||
+          cudaMemcpyAsync(dst + half, curV, half, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+        return fail(MT_ECUDA, "ring copy to the next rank failed");
+      prof_mark(c, 0, t, RingProfile::kInnerE, cs);
+      if (write(cs, reinterpret_cast<CUdeviceptr>(next_ready), rbase + (uint32_t)t + 1u,
+                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return fail(MT_ECUDA, "cuStreamWriteValue32 (ready)");
+      cudaEventRecord(ev_sent, cs);
+    }
+    // ---- compute step t
+    if (t >= 1 && wait(stream, d_ready, rbase + (uint32_t)t, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(MT_ECUDA, "cuStreamWaitValue32 (compute)");
+    prof_mark(c, 0, t, RingProfile::kCompB, stream);
+    MT_TRY(attn_fwd_step(plan, r, sched[t][r], nloc, q_loc, curK, curV, o_loc, o_acc, lse_loc,
+                         t == 0, t == W - 1, device_num_sms(), stream));
+    prof_mark(c, 0, t, RingProfile::kCompE, stream);
+    // my slot (t-1) % 2 is free once compute step t and its forwarding copy are done
+    if (t < W - 1) cudaStreamWaitEvent(stream, ev_sent, 0);
+    if (write(stream, reinterpret_cast<CUdeviceptr>(prev_done), cbase + (uint32_t)t + 1u,
+              CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(MT_ECUDA, "cuStreamWriteValue32 (done)");
+  }
+  cudaEventDestroy(ev_sent);
+  // the comm stream's last copy read the chunk of step W-2; later calls reuse the buffers
+  cudaEventRecord(c->ev_done, cs);
+  cudaStreamWaitEvent(stream, c->ev_done, 0);
+  return check_launch("mt_ring_attn_fwd (copy engines)");
+}
+}  // namespace
+}  // namespace mt
+#endif
+
 extern "C" mt_status mt_ring_attn_fwd(mt_comm* comm, const mt_shape* sh, const void* q_loc,
                                       const void* k_loc, const void* v_loc,
                                       const mt_vs_index* idx, void* o_loc, float* lse_loc,
@@ -262,8 +348,12 @@ extern "C" mt_status mt_ring_attn_fwd(mt_comm* comm, const mt_shape* sh, const v
                        idx->v_idx, idx->v_stride, idx->s_cnt, idx->s_off, (int)idx->s_stride,
                        w.plan, stream));
   const auto sched = ring_schedule(W, comm->inner);
-  KVRing ring(comm, S_loc, sh->n_kv_heads, k_loc, v_loc, w.kv);
   if (comm->prof) comm->prof->steps[0] = 0;
+  if (comm->ce_ok && ws == comm->ce_ws && ws_bytes == comm->ce_bytes && comm->inner == W &&
+      comm->emu_gbps <= 0.0)
+    return ring_fwd_ce(comm, sched, plan, r, nloc, S_loc, sh->n_kv_heads, q_loc, k_loc, v_loc,
+                       o_loc, w.o_acc, lse_loc, w.kv, static_cast<uint8_t*>(ws), stream);
+  KVRing ring(comm, S_loc, sh->n_kv_heads, k_loc, v_loc, w.kv);
   for (int t = 0; t < W; ++t) {
     MT_TRY(ring.post(t, stream));
     prof_mark(comm, 0, t, RingProfile::kCompB, stream);

@@ -107,4 +107,7 @@ def test_block_csr_of_vs_index_equals_vs_path(cuda_lib):
     o2, lse2 = ops.sparse_attn_fwd(qd, kd, vd, idx)
     torch.cuda.synchronize()
     assert normwise_err(got[0], o2.float().cpu().numpy().astype(np.float64), 1) <= 1e-2
-    assert np.max(np.abs(got[1] - lse2.cpu().numpy())) <= 1e-4
+    # the two paths group keys into chunks differently, and the forward evaluates a quarter
+    # of the exponentials with a cubic (relative error <= 1.02e-4, attn_fwd.cu ex2_poly), so
+    # their row sums agree to ~1e-4 relative, not bitwise
+    assert np.max(np.abs(got[1] - lse2.cpu().numpy())) <= 5e-4
