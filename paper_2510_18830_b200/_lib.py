@@ -104,6 +104,9 @@ _SIGS: dict[str, list] = {
     "mt_vs_format_fill": [P, P, P, P, P, I64, P, I64, I64, I64, P, SZ, P],
     "mt_unstripe": [I64, I64, I, I, P, P, P],
     "mt_launch_count": [],
+    "mt_ring_flags_bytes": [],
+    "mt_comm_register_workspace": [P, P, SZ, P],
+    "mt_comm_copy_engine": [P],
     "mt_library_call_count": [],
 }
 _RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
@@ -113,6 +116,7 @@ _RESTYPE = {"mt_sparse_attn_fwd_workspace_bytes": ctypes.c_size_t,
             "mt_ring_attn_workspace_bytes": ctypes.c_size_t,
             "mt_vs_format_workspace_bytes": ctypes.c_size_t,
             "mt_launch_count": ctypes.c_ulonglong,
+            "mt_ring_flags_bytes": ctypes.c_size_t,
             "mt_library_call_count": ctypes.c_ulonglong}
 
 

@@ -207,6 +207,25 @@ class Comm:
 
     def __init__(self, handle, world: int, rank: int, inner: int):
         self.handle, self.world, self.rank, self.inner = handle, world, rank, inner
+        self.ring_ws = None  # the ring calls' own workspace (registered for the copy engines)
+
+    def ring_workspace(self, nbytes: int) -> torch.Tensor:
+        """The ring calls' workspace: at least `nbytes` plus the reserved flag words at its
+        end (mt_ring_flags_bytes).  Grown collectively (every rank asks for the same size
+        at the same call), and (re)registered with mt_comm_register_workspace so the flat
+        forward ring moves KV chunks with the copy engines (MT_RING_CE=0 keeps NCCL)."""
+        import os
+        L = _lib.lib()
+        need = nbytes + int(L.mt_ring_flags_bytes())
+        if self.ring_ws is None or self.ring_ws.numel() < need:
+            self.ring_ws = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device="cuda")
+            if os.environ.get("MT_RING_CE", "1") != "0":
+                _lib.check(L.mt_comm_register_workspace(self.handle, _ptr(self.ring_ws),
+                                                        self.ring_ws.numel(), _stream()))
+        return self.ring_ws
+
+    def copy_engine(self) -> bool:
+        return bool(_lib.lib().mt_comm_copy_engine(self.handle))
 
     @staticmethod
     def create(world: int, rank: int, inner: int | None = None, group=None) -> "Comm":
@@ -406,7 +425,8 @@ def ring_schedule(world: int, inner: int | None = None):
 def ring_attn_fwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, idx: VSIndex):
     sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1])
     L = _lib.lib()
-    ws = workspace(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 0))
+    ws = comm.ring_workspace(max(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 0),
+                                 L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 1)))
     o = torch.empty_like(q_loc)
     lse = torch.empty(q_loc.shape[1], q_loc.shape[0], dtype=torch.float32, device=q_loc.device)
     ci = idx.c_struct()
@@ -418,7 +438,8 @@ def ring_attn_fwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, idx: VSIndex):
 def ring_attn_bwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, o_loc, lse_loc, dO_loc, idx: VSIndex):
     sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1])
     L = _lib.lib()
-    ws = workspace(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 1))
+    ws = comm.ring_workspace(max(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 0),
+                                 L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 1)))
     dq, dk, dv = torch.empty_like(q_loc), torch.empty_like(k_loc), torch.empty_like(v_loc)
     ci = idx.c_struct()
     _lib.check(L.mt_ring_attn_bwd(comm.handle, ctypes.byref(sh), _ptr(q_loc), _ptr(k_loc), _ptr(v_loc),

@@ -66,11 +66,18 @@ def main():
 
     ws_plain = ops.workspace
     ops.workspace = lambda n, device=None: guarded(max(n, 1))
+    # the ring's own workspace guarded too; it is not registered, so this re-run takes the
+    # NCCL send/recv transport while the plain run above used the copy engines (when
+    # available): the comparison below cross-checks the two transports
+    ce_used = comm.copy_engine()
+    ring_ws_plain = comm.ring_ws
+    comm.ring_ws = guarded(ring_ws_plain.numel())
     qg, kg, vg, dg = (gcopy(x) for x in (ql, kl, vl, dl))
     og, lg = ops.ring_attn_fwd(comm, S, qg, kg, vg, idx)
     dqg, dkg, dvg = ops.ring_attn_bwd(comm, S, qg, kg, vg, og, lg, dg, idx)
     torch.cuda.synchronize()
     ops.workspace = ws_plain
+    comm.ring_ws = ring_ws_plain
     intact = all(bool((b[:G] == 0xFF).all()) and bool((b[G + n:] == 0xFF).all()) for b, n in guards)
     unchanged = all(torch.equal(x, y) for x, y in ((qg, ql), (kg, kl), (vg, vl), (dg, dl)))
     close = all(bool((x.float() - y.float()).abs().max() <= 1e-2 * y.float().abs().max())
@@ -109,7 +116,7 @@ def main():
                 "dv": nerr(unstripe(gv, ref[2].shape), ref[2])}
         ok["fwd"] = bool(errs["o"] <= 2e-2 and errs["lse"] <= 1e-3)
         ok["bwd"] = bool(max(errs["dq"], errs["dk"], errs["dv"]) <= 2e-2)
-        print(json.dumps({"world": W, "inner": a.inner or W, "ok": ok,
+        print(json.dumps({"world": W, "inner": a.inner or W, "copy_engine_ring": bool(ce_used), "ok": ok,
                           "errs": {k_: float(v_) for k_, v_ in errs.items()}}), flush=True)
     flag = torch.tensor([1 if all(ok.values()) else 0], device=dev)
     dist.broadcast(flag, 0)
