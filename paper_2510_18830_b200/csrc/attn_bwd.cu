@@ -51,11 +51,18 @@ namespace mt {
 
 namespace bwd {
 
-constexpr int kStages = 4;      // Q / dO / LSE / D stages
+#ifndef MT_BWD_STAGES
+#define MT_BWD_STAGES 4
+#endif
+// Q / dO / LSE / D stages.  4: each softmax warpgroup's 16 KB buffer stages dQ in two
+// halves.  3 (-DMT_BWD_STAGES=3) gives each a 32 KB buffer and ONE bulk reduce-add per
+// chunk, but measured slower (296 vs 278 ms at 512K: the loads starve with 3 stages).
+constexpr int kStages = MT_BWD_STAGES;
 constexpr int kThreads = 384;   // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
 constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
 constexpr uint32_t kTileP = 128 * 64 * 2;    // 16 KB (128 keys x 64 queries)
+constexpr uint32_t kTilePD = (kStages <= 3) ? 2 * kTileP : kTileP;  // per-warpgroup buffer
 
 enum : int { kModeBlock = 0, kModeBar = 1 };
 enum : int { kChunk = 0, kEnd = 1, kDone = 2 };
@@ -85,7 +92,7 @@ struct Smem {
   // per softmax warpgroup: dS^T (16 KB, the B operand of dQ^T); once the gradient
   // MMAs are done the same 16 KB stages its dQ tile, 32 queries [32][128] fp32 at
   // a time, for the bulk reduce-adds (P^T lives in TMEM)
-  uint8_t pd[2][kTileP];
+  uint8_t pd[2][kTilePD];
   alignas(16) float lse[kStages][64];
   alignas(16) float dd[kStages][64];
   ChunkMeta meta[kStages];
@@ -438,7 +445,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint32_t st = bg ? pst1 : pst0;
       const uint64_t dqm = sdesc_add(dQmn0, st * kTileQ);
       const uint64_t dom = sdesc_add(dOmn0, st * kTileQ);
-      const uint64_t dstm = sdesc_add(dDSTmn0, bg * kTileP);
+      const uint64_t dstm = sdesc_add(dDSTmn0, bg * kTilePD);
       const uint32_t R = tmem + kColR + 128 * bg;
       if (leader) {
 #pragma unroll
@@ -556,6 +563,7 @@ __device__ __forceinline__ void softmax_half(const uint32_t (&sv)[32], const uin
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int q = c + u;
+      // (ex2_poly for a quarter of these measured no gain here: MUFU is not this kernel's bound)
       p[u] = ex2(fmaf(__uint_as_float(sv[q]), scale_log2, la[u]));
       ds[u] = p[u] * fmaf(__uint_as_float(dpv[q]), inv_sqrt_d, da[u]);
       if (kMasked) {
@@ -627,6 +635,29 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       for (int c = 0; c < 32; ++c) red_add_f32(dst + (c + 32) * qs, __uint_as_float(r1[c]));
       return;
     }
+    if (kTilePD >= 2 * kTileP) {
+      // stage dQ[q][d] (fp32, all 64 queries, 32 KB) in this warpgroup's buffer and issue
+      // ONE bulk tensor reduce-add; its read is waited for before the buffer is rewritten
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const uint32_t(&rv)[32] = hf ? r1 : r0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(pdbuf + (uint32_t)((hf * 32 + c) * 128 + row) * 4),
+                       "f"(__uint_as_float(rv[c]))
+                       : "memory");
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(wg_bar, 128);
+      if (row == 0) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+            " [%0, {%1, %2, %3}], [%4];" ::"l"(tmdq),
+            "r"(0), "r"(h), "r"(j * 64), "r"(pdbuf)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {
     // stage dQ[q][d] (fp32) in this warpgroup's 16 KB buffer, 32 queries at a time,
     // each half one bulk tensor reduce-add into the fp32 dQ accumulator
 #pragma unroll
@@ -651,6 +682,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
             : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
+    }
     }
 #if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
     if (row == 0) MT_TL(7, seq);
@@ -983,7 +1015,7 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.hpt = (plan.bptr || plan.tptr) ? 1 : hpt;
   const uint64_t S_loc = (uint64_t)nloc * 64;
   CUtensorMap tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv;
-  if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, 32) ||
+  if (make_tmap_f32_3d(&tmdq, dq, 128, plan.Hq, S_loc, 128, 1, kTilePD >= 2 * kTileP ? 64 : 32) ||
       make_tmap_f32_3d(&tmdk, dk, 128, plan.Hkv, S_loc, 32, 1, 128, true) ||
       make_tmap_f32_3d(&tmdv, dv, 128, plan.Hkv, S_loc, 32, 1, 128, true) ||
       make_tmap_bf16_3d(&tmq, q, 128, plan.Hq, S_loc, 64, 1, 64) ||
