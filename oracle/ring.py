@@ -7,7 +7,8 @@ message into the receiver's buffer at the end of the step (the async
 send/recv + wait of Alg. 2 becomes a per-step barrier).  fp64 throughout.
 
 Forward (Alg. 2, readings R12-R16):
-  - block-striped layout: global block b -> rank b mod W (P:277);
+  - block-striped layout: global block b -> rank b mod W; or the zigzag
+    layout of the "Ours w/ ZigZag" ablation (P:64, P:345; sparseformat.zigzag_perm);
   - Q and O stay on their rank, K/V circulate (P:64);
   - flat ring: step t, rank r computes with the chunk it holds, then sends it to
     r+1 and receives from r-1 (so it holds origin (r - t) mod W);
@@ -27,15 +28,15 @@ from __future__ import annotations
 import numpy as np
 
 from .attention import NEG_INF, _softmax_rows, merge_out_and_lse
-from .sparseformat import BLOCK, convert_index, sparseformat, stripe_perm
+from .sparseformat import BLOCK, convert_index, layout_perm, sparseformat
 
 
-def _local_plans(i_v, i_s, S, W, block):
+def _local_plans(i_v, i_s, S, W, block, layout="striped"):
     """plans[h][r][s][j] = (local blocks, local bar rows) via convert_index."""
     plans = []
     for h in range(len(i_v)):
         B, C = sparseformat(i_v[h], i_s[h], S, block)
-        plans.append([convert_index(B, C, S, W, r, block) for r in range(W)])
+        plans.append([convert_index(B, C, S, W, r, block, layout) for r in range(W)])
     return plans
 
 
@@ -93,13 +94,15 @@ def schedule(W: int, inner: int | None = None):
     return steps
 
 
-def ring_forward(q, k, v, i_v, i_s, W: int, inner: int | None = None, block: int = BLOCK):
+def ring_forward(q, k, v, i_v, i_s, W: int, inner: int | None = None, block: int = BLOCK,
+                 layout: str = "striped"):
     """Sparse ring forward over W ranks; returns (O, LSE) in GLOBAL token order
-    plus the per-(step, rank) origin log."""
+    plus the per-(step, rank) origin log.  layout: "striped" (the method) or
+    "zigzag" (the "Ours w/ ZigZag" ablation, P:345)."""
     S, Hq, d = q.shape
     grp = Hq // k.shape[1]
-    perm = stripe_perm(S, W, block)
-    plans = _local_plans(i_v, i_s, S, W, block)
+    perm = layout_perm(S, W, layout, block)
+    plans = _local_plans(i_v, i_s, S, W, block, layout)
     sched = schedule(W, inner)
     qs = [q[perm[r]] for r in range(W)]
     ks = [k[perm[r]] for r in range(W)]
@@ -123,14 +126,14 @@ def ring_forward(q, k, v, i_v, i_s, W: int, inner: int | None = None, block: int
 
 
 def ring_backward(q, k, v, O, LSE, dO, i_v, i_s, W: int, inner: int | None = None,
-                  block: int = BLOCK):
+                  block: int = BLOCK, layout: str = "striped"):
     """Sparse ring backward (reading R17); inputs/outputs in GLOBAL token order."""
     S, Hq, d = q.shape
     Hkv = k.shape[1]
     grp = Hq // Hkv
     G = W if inner is None else inner
-    perm = stripe_perm(S, W, block)
-    plans = _local_plans(i_v, i_s, S, W, block)
+    perm = layout_perm(S, W, layout, block)
+    plans = _local_plans(i_v, i_s, S, W, block, layout)
     sched = schedule(W, inner)
     loc = lambda x, r: x[perm[r]]
     qs, dOs, Os = [loc(q, r) for r in range(W)], [loc(dO, r) for r in range(W)], [loc(O, r) for r in range(W)]

@@ -9,12 +9,16 @@ Reading (DESIGN.md §2.1 I9-I10, readings R3, R4, R8, R12, R15):
        C_g = sort_asc{ m in i_v : floor(m/64) < g, (g - floor(m/64)) not in i_s }
        (a vertical inside a selected slash block is already computed there;
         verticals in block g itself are covered by the forced offset 0).
-  I10  block-striped layout: global block b lives on rank b mod W
-       at local block b // W.  For rank r, local query block j (g = jW + r),
-       and KV origin s:
-         B_g^(s) = { (kb - s) / W : kb in B_g, kb = s (mod W) }
-         C_g^(s) = { ((floor(m/64) - s) / W) * 64 + m mod 64 :
-                     m in C_g, floor(m/64) = s (mod W) }
+  I10  a layout maps global block b to (owner(b), local block lb(b)):
+         block-striped (P:276-277): owner = b mod W, lb = b // W;
+         zigzag (Fig. 1): the sequence is cut into 2W equal
+           chunks, rank w holds chunks w and 2W-1-w (in that order); with chunk
+           length c blocks, owner(b) = k if k < W else 2W-1-k for k = b // c, and
+           lb = b mod c (+ c for the second chunk).
+       For rank r, local query block j (global g), and KV origin s:
+         B_g^(s) = { lb(kb) : kb in B_g, owner(kb) = s }
+         C_g^(s) = { lb(floor(m/64)) * 64 + m mod 64 : m in C_g, owner(floor(m/64)) = s }
+       (slash offsets stay defined on global positions)
 The key set of global query n in block g is
   K_n = { m : floor(m/64) in B_g, m <= n }  U  C_g.
 """
@@ -91,26 +95,66 @@ def stripe_perm(S: int, W: int, block: int = BLOCK):
     return np.stack([((j // block) * W + r) * block + j % block for r in range(W)])
 
 
-def convert_index(B, C, S: int, W: int, r: int, block: int = BLOCK):
+def zigzag_perm(S: int, W: int):
+    """Zigzag layout ("ZigZag folds the query dimension", Fig. 1):
+    2W equal chunks, rank r holds chunk r then chunk 2W-1-r.
+
+    Returns int64 [W][S/W] with the global token of every local row.
+    """
+    if S % (2 * W):
+        raise ValueError("S must be a multiple of 2 W (zigzag layout)")
+    c = S // (2 * W)
+    return np.stack([np.r_[np.arange(r * c, r * c + c), np.arange((2 * W - 1 - r) * c, (2 * W - r) * c)]
+                     for r in range(W)]).astype(np.int64)
+
+
+LAYOUTS = ("striped", "zigzag")
+
+
+def layout_perm(S: int, W: int, layout: str = "striped", block: int = BLOCK):
+    """[W][S/W] global token of each local row, for a block-aligned layout."""
+    if layout == "striped":
+        return stripe_perm(S, W, block)
+    if layout == "zigzag":
+        if S % (2 * W * block):
+            raise ValueError("zigzag with 64-token blocks needs S a multiple of 2 W 64")
+        return zigzag_perm(S, W)
+    raise ValueError(f"unknown layout {layout!r}")
+
+
+def block_owner(S: int, W: int, layout: str = "striped", block: int = BLOCK):
+    """(owner[b], lb[b]) for every global block b, read off layout_perm."""
+    perm = layout_perm(S, W, layout, block)
+    nb = S // block
+    owner = np.empty(nb, np.int64)
+    lb = np.empty(nb, np.int64)
+    for r in range(W):
+        gb = perm[r][::block] // block
+        owner[gb] = r
+        lb[gb] = np.arange(gb.size)
+    return owner, lb
+
+
+def convert_index(B, C, S: int, W: int, r: int, block: int = BLOCK, layout: str = "striped"):
     """I10 for rank r: per origin s, per local query block j: (blocks, bars) local.
 
     Returns plan[s][j] = (local key blocks array, local bar rows array), both
     sorted ascending, indices into origin s's local K/V chunk.
     """
-    nb = S // block
-    nloc = nb // W
+    perm = layout_perm(S, W, layout, block)
+    owner, lblk = block_owner(S, W, layout, block)
+    nloc = S // block // W
     plan = []
     for s in range(W):
         per_j = []
         for j in range(nloc):
-            g = j * W + r
-            kb = B[g]
-            kb = kb[(kb % W) == s]
-            lb = (kb - s) // W
-            cm = C[g]
+            g = int(perm[r][j * block]) // block
+            kb = np.asarray(B[g], np.int64)
+            lb = lblk[kb[owner[kb] == s]]
+            cm = np.asarray(C[g], np.int64)
             cb = cm // block
-            sel = (cb % W) == s
-            lc = ((cb[sel] - s) // W) * block + cm[sel] % block
+            sel = owner[cb] == s
+            lc = lblk[cb[sel]] * block + cm[sel] % block
             per_j.append((np.sort(lb), np.sort(lc)))
         plan.append(per_j)
     return plan

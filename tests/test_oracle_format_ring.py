@@ -142,3 +142,73 @@ def test_hierarchical_equals_flat_both_factorizations():
     flat = R.ring_forward(q, k, v, iv, is_, 8, None)[0]
     for inner in (4, 2):
         assert np.max(np.abs(R.ring_forward(q, k, v, iv, is_, 8, inner)[0] - flat)) < 1e-12
+
+
+# ------------------------------------------------------------------ zigzag layout (f1)
+@pytest.mark.parametrize("case", GOLD["layout_zigzag"])
+def test_zigzag_golden(case):
+    perm = SF.zigzag_perm(case["S"], case["W"])
+    assert [sorted(p.tolist()) for p in perm] == case["rank_tokens"]
+
+
+def test_zigzag_bijection_two_runs_identity_at_w1():
+    for S, W in ((1024, 2), (1024, 4), (2048, 8)):
+        p = SF.zigzag_perm(S, W)
+        assert sorted(p.ravel().tolist()) == list(range(S))
+        for r in range(W):  # exactly two contiguous ascending runs of S / 2W tokens
+            d = np.diff(p[r])
+            assert (d > 0).all() and int((d != 1).sum()) == (1 if r < W - 1 else 0)
+    assert SF.zigzag_perm(256, 1)[0].tolist() == list(range(256))
+    with pytest.raises(ValueError):
+        SF.layout_perm(64 * 6, 2, "zigzag")   # chunks must be whole 64-token blocks
+
+
+def test_zigzag_causal_balance_exact():
+    # P:64 "Under causal full attention, both variants maintain balanced workload";
+    # per-rank planned work is EXACTLY equal for zigzag (chunk w and its
+    # mirror 2W-1-w together hold (2W-1)c^2 + c(c+1) causal pairs, independent of w),
+    # unlike block striping (test_dense_causal_balanced_across_ranks).
+    for S, W in ((1024, 2), (1024, 4), (2048, 8)):
+        B, C = SF.sparseformat(np.arange(S), np.arange(S // 64), S)
+        tot = []
+        for rank in range(W):
+            plan = SF.convert_index(B, C, S, W, rank, layout="zigzag")
+            tot.append(sum(len(lb) for s in range(W) for lb, _ in plan[s]))
+        assert len(set(tot)) == 1, tot
+        c = S // 64 // (2 * W)
+        assert tot[0] == (2 * W - 1) * c * c + c * (c + 1)
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_convert_index_coverage_zigzag(W):
+    # the union over (rank, origin) of the local plans, mapped back through
+    # the layout, is exactly the global index mask (no gaps, no duplicates)
+    S = 1024
+    r = np.random.default_rng(30 + W)
+    iv = np.unique(np.r_[0, r.choice(S, 25, replace=False)])
+    is_ = np.unique(np.r_[0, r.choice(S // 64, 4, replace=False)])
+    B, C = SF.sparseformat(iv, is_, S)
+    perm = SF.zigzag_perm(S, W)
+    got = np.zeros((S, S), np.int64)
+    for rank in range(W):
+        plan = SF.convert_index(B, C, S, W, rank, layout="zigzag")
+        for s in range(W):
+            for j, (lb, lc) in enumerate(plan[s]):
+                keys = np.concatenate([np.arange(b * 64, b * 64 + 64) for b in lb] + [lc]).astype(int)
+                for n in perm[rank][j * 64:(j + 1) * 64]:
+                    gk = perm[s][keys]
+                    got[n, gk[gk <= n]] += 1
+    assert np.array_equal(got, SF.union_mask(iv, is_, S).astype(np.int64))
+
+
+@pytest.mark.parametrize("W,inner", [(2, None), (4, None), (4, 2)])
+def test_ring_zigzag_equals_single_device(W, inner):
+    q, k, v, iv, is_ = _problem(S=1024, seed=50 + W)
+    dO = np.random.default_rng(7).standard_normal(q.shape)
+    O, L = A.sparse_attention_forward(q, k, v, iv, is_)
+    Or, Lr, _ = R.ring_forward(q, k, v, iv, is_, W, inner, layout="zigzag")
+    assert np.max(np.abs(Or - O)) < 1e-12 and np.max(np.abs(Lr - L)) < 1e-12
+    ref = A.sparse_attention_backward(q, k, v, O, L, dO, iv, is_)
+    got = R.ring_backward(q, k, v, O, L, dO, iv, is_, W, inner, layout="zigzag")
+    for a, b in zip(got, ref):
+        assert np.max(np.abs(a - b)) < 1e-11
