@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--hkv", type=int, default=2)
     ap.add_argument("--p", type=float, default=0.9)
     ap.add_argument("--inner", type=int, default=0, help="hierarchical inner ring size (0 = flat)")
+    ap.add_argument("--layout", default="striped", choices=["striped", "zigzag"],
+                    help="sequence layout of the ranks: the method's 64-token block striping, or "
+                         "the zigzag layout of the 'Ours w/ ZigZag' ablation (P:345)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -98,8 +101,9 @@ class Clocks:
 def workload_name(args, W: int) -> str:
     cfg = {4096: "C1", 65536: "C2", 131072: "C3", 524288: "C4", 1048576: "C5"}.get(args.seq, "custom")
     ring = "flat" if not args.inner or args.inner == W else f"{W // args.inner}x{args.inner}"
+    lay = "" if args.layout == "striped" else f", {args.layout} layout"
     return (f"{cfg}-shape layer at W={W}: S={args.seq}, Hq={args.hq}, Hkv={args.hkv}, d=128, "
-            f"p_v=p_s={args.p}, {ring} ring")
+            f"p_v=p_s={args.p}, {ring} ring{lay}")
 
 
 # ------------------------------------------------------------------ layout helpers
@@ -107,6 +111,13 @@ def stripe_rows(S: int, W: int, r: int) -> np.ndarray:
     """Global token of each local row of rank r (64-token block striping)."""
     j = np.arange(S // W)
     return ((j // 64) * W + r) * 64 + j % 64
+
+
+def zigzag_rows(S: int, W: int, r: int) -> np.ndarray:
+    """Global token of each local row of rank r in the zigzag layout (Fig. 1):
+    2W chunks, rank r holds chunk r then chunk 2W-1-r."""
+    c = S // (2 * W)
+    return np.r_[np.arange(r * c, r * c + c), np.arange((2 * W - 1 - r) * c, (2 * W - r) * c)]
 
 
 def bits_to_torch(bits: np.ndarray, dev):
@@ -235,7 +246,8 @@ def run_ours(args):
     S, Hq, Hkv, p = args.seq, args.hq, args.hkv, args.p
     q, k, v = make_qkv(S, Hq, Hkv, seed=args.seed)
     dO = make_grad_out(S, Hq, seed=args.seed)
-    rows = stripe_rows(S, W, rank) if W > 1 else np.arange(S)
+    lay = args.layout
+    rows = (stripe_rows if lay == "striped" else zigzag_rows)(S, W, rank) if W > 1 else np.arange(S)
     hq_, hk_, hv_, hdo = (np.ascontiguousarray(x[rows]) for x in (q, k, v, dO))
     qd, kd, vd, dOd = (bits_to_torch(x, dev) for x in (hq_, hk_, hv_, hdo))
     stream = torch.cuda.current_stream()
@@ -245,17 +257,17 @@ def run_ours(args):
     def step(qx, kx, vx, dox, marks=None):
         e = [ev() for _ in range(4)] if marks is not None else None
         if e: e[0].record(stream)
-        idx = ops.build_vs_index(qx, kx, p, p, comm=comm, seq_len=S)
+        idx = ops.build_vs_index(qx, kx, p, p, comm=comm, seq_len=S, layout=lay)
         if e: e[1].record(stream)
         if comm is None:
             o, lse = ops.sparse_attn_fwd(qx, kx, vx, idx)
         else:
-            o, lse = ops.ring_attn_fwd(comm, S, qx, kx, vx, idx)
+            o, lse = ops.ring_attn_fwd(comm, S, qx, kx, vx, idx, layout=lay)
         if e: e[2].record(stream)
         if comm is None:
             g = ops.sparse_attn_bwd(qx, kx, vx, o, lse, dox, idx)
         else:
-            g = ops.ring_attn_bwd(comm, S, qx, kx, vx, o, lse, dox, idx)
+            g = ops.ring_attn_bwd(comm, S, qx, kx, vx, o, lse, dox, idx, layout=lay)
         if e:
             e[3].record(stream)
             marks.append(e)

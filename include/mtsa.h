@@ -46,7 +46,7 @@ typedef enum {
   MT_ESHAPE = 1,       /* null pointer / bad dimension */
   MT_EWINDOW = 2,      /* S < 64 or S % 64 != 0 (window = last 64 queries) */
   MT_ECONFIG = 3,      /* p_v or p_s outside (0, 1] */
-  MT_ELAYOUT = 4,      /* S % (64 * W) != 0 for the block-striped layout */
+  MT_ELAYOUT = 4,      /* S not divisible for the layout (64 W striped, 128 W zigzag) */
   MT_ECAPACITY = 5,    /* an output buffer is too small */
   MT_EWORKSPACE = 6,   /* workspace too small */
   MT_EUNSUPPORTED = 7, /* d != 128, block != 64, non-sm_100 device */
@@ -64,13 +64,25 @@ const char* mt_last_error(void);
 unsigned long long mt_launch_count(void);
 unsigned long long mt_library_call_count(void);
 
-/* Problem shape.  seq_len is the GLOBAL sequence length S. */
+/* Sequence-to-rank layouts of the ring (Fig. 1), at 64-token
+ * block granularity; a rank's local blocks are always in ascending global order.
+ *   MT_LAYOUT_STRIPED  the method: global block b -> rank b mod W, local
+ *                      block b / W.  Needs S % (64 W) == 0.
+ *   MT_LAYOUT_ZIGZAG   the "Ours w/ ZigZag" ablation: the sequence
+ *                      is cut into 2W equal chunks, rank r holds chunk r then chunk
+ *                      2W-1-r.  Needs S % (128 W) == 0.
+ * With world == 1 both are the identity. */
+enum { MT_LAYOUT_STRIPED = 0, MT_LAYOUT_ZIGZAG = 1 };
+
+/* Problem shape.  seq_len is the GLOBAL sequence length S.  A zero-initialised
+ * `layout` is the block-striped layout. */
 typedef struct {
   int64_t seq_len;
   int32_t n_q_heads;  /* Hq */
   int32_t n_kv_heads; /* Hkv; q head h uses kv head h / (Hq / Hkv) */
   int32_t head_dim;   /* d, must be 128 */
   int32_t block;      /* B = stripe = slash block = window rows, must be 64 */
+  int32_t layout;     /* MT_LAYOUT_STRIPED or MT_LAYOUT_ZIGZAG (multi-rank calls) */
 } mt_shape;
 
 /* Online top-p targets of Alg. 1 ("p_v, p_s", read as reals in (0, 1]). */
@@ -161,6 +173,20 @@ size_t mt_build_vs_index_workspace_bytes(const mt_shape* shape, int world);
 mt_status mt_build_vs_index(mt_comm* comm, const mt_shape* shape, const mt_vs_params* params,
                             const void* q, const void* k, mt_vs_index* out, void* ws,
                             size_t ws_bytes, mt_stream_t stream);
+
+/* f3 upstream fusion (P:339 RoPE/YaRN, Appendix A): the index of
+ * the ROTATED q / k built from PRE-RoPE inputs, with the RoPE pass folded into it.  q, k
+ * are pre-RoPE (layout, world and shapes as mt_build_vs_index); on return q_out / k_out
+ * hold RoPE(q) / RoPE(k) at the tokens' global positions (theta[64] and mscale as
+ * mt_rope_inv_freq; the same bf16 bits as mt_rope) and `out` holds exactly the lists
+ * mt_build_vs_index gives for (q_out, k_out).  The window queries are rotated while
+ * staged, k is rotated in registers by the index's first stage (each key row read once
+ * for both), q by one extra pass.  q_out may alias q; k_out must not alias k (MT_ESHAPE).
+ * Same workspace as mt_build_vs_index.  Errors: as mt_build_vs_index. */
+mt_status mt_rope_vs_index(mt_comm* comm, const mt_shape* shape, const mt_vs_params* params,
+                           const double* theta, float mscale, const void* q, const void* k,
+                           void* q_out, void* k_out, mt_vs_index* out, void* ws,
+                           size_t ws_bytes, mt_stream_t stream);
 
 /* Test hook (single GPU): the exact intermediate scores of Alg. 1 —
  * col_scores [Hq][S] = sum_v(A_hat) per token column (uint64 fixed point,
@@ -409,6 +435,15 @@ mt_status mt_stripe(int64_t seq_len, int64_t row_bytes, int world, int rank,
                     const void* global, void* local, mt_stream_t stream);
 mt_status mt_unstripe(int64_t seq_len, int64_t row_bytes, int world, int rank,
                       const void* local, void* global, mt_stream_t stream);
+
+/* The same copies for either layout (MT_LAYOUT_STRIPED as mt_stripe / mt_unstripe, or
+ * MT_LAYOUT_ZIGZAG: local row j of rank r <-> global token of chunk r (j < S/2W) or
+ * chunk 2W-1-r; Fig. 1).  Errors as above, plus MT_ESHAPE for an
+ * unknown layout and MT_ELAYOUT when zigzag and S % (128 W) != 0. */
+mt_status mt_layout_to_local(int layout, int64_t seq_len, int64_t row_bytes, int world,
+                             int rank, const void* global, void* local, mt_stream_t stream);
+mt_status mt_layout_to_global(int layout, int64_t seq_len, int64_t row_bytes, int world,
+                              int rank, const void* local, void* global, mt_stream_t stream);
 
 /* ------------------------------------------------------------------ tests */
 /* Hardware self-test hook (not part of the attention API): one 128-row tcgen05

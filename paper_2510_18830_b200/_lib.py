@@ -27,7 +27,7 @@ class MTError(RuntimeError):
 class Shape(ctypes.Structure):
     _fields_ = [("seq_len", ctypes.c_int64), ("n_q_heads", ctypes.c_int32),
                 ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
-                ("block", ctypes.c_int32)]
+                ("block", ctypes.c_int32), ("layout", ctypes.c_int32)]
 
 
 class VSParams(ctypes.Structure):
@@ -73,6 +73,7 @@ _SIGS: dict[str, list] = {
     "mt_attn_fwd_step": [P, I, I, I, I, I, P, P, P, P, P, P, P, P, SZ, P],
     "mt_build_vs_index_workspace_bytes": [P, I],
     "mt_build_vs_index": [P, P, P, P, P, P, P, SZ, P],
+    "mt_rope_vs_index": [P, P, P, P, ctypes.c_float, P, P, P, P, P, P, SZ, P],
     "mt_vs_column_scores": [P, P, P, P, P, P, SZ, P],
     "mt_comm_unique_id": [P],
     "mt_comm_create": [P, I, I, I, P],
@@ -103,6 +104,8 @@ _SIGS: dict[str, list] = {
     "mt_vs_format_count": [P, P, P, P, P, P, P, SZ, P],
     "mt_vs_format_fill": [P, P, P, P, P, I64, P, I64, I64, I64, P, SZ, P],
     "mt_unstripe": [I64, I64, I, I, P, P, P],
+    "mt_layout_to_local": [I, I64, I64, I, I, P, P, P],
+    "mt_layout_to_global": [I, I64, I64, I, I, P, P, P],
     "mt_launch_count": [],
     "mt_ring_flags_bytes": [],
     "mt_comm_register_workspace": [P, P, SZ, P],

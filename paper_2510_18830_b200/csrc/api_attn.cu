@@ -9,7 +9,8 @@
 namespace mt {
 
 size_t vs_plan_bytes(int64_t S, int Hq, int W);
-mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const int32_t* v_cnt,
+mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, int layout,
+                        const int32_t* v_cnt,
                         const int32_t* v_idx, int64_t v_stride, const int32_t* s_cnt,
                         const int32_t* s_off, int s_stride, void* ws, cudaStream_t st);
 mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* q,
@@ -62,6 +63,11 @@ mt_status check_shape(const mt_shape* sh, int W) {
     return fail(MT_ELAYOUT, "seq_len %lld is not a multiple of 64 * world (%d)",
                 (long long)sh->seq_len, W);
   if (sh->seq_len / 64 > (1LL << 24)) return fail(MT_ESHAPE, "seq_len too large");
+  if (sh->layout != MT_LAYOUT_STRIPED && sh->layout != MT_LAYOUT_ZIGZAG)
+    return fail(MT_ESHAPE, "unknown layout %d", sh->layout);
+  if (sh->layout == MT_LAYOUT_ZIGZAG && W > 1 && sh->seq_len % (128LL * W))
+    return fail(MT_ELAYOUT, "zigzag: seq_len %lld is not a multiple of 128 * world (%d)",
+                (long long)sh->seq_len, W);
   return MT_OK;
 }
 
@@ -106,7 +112,8 @@ extern "C" mt_status mt_attn_fwd_step(const mt_shape* sh, int world, int rank, i
     return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   MT_TRY(check_device());
   VSPlan plan;
-  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, world, idx->v_cnt,
+  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, world, sh->layout,
+                       idx->v_cnt,
                        idx->v_idx, idx->v_stride, idx->s_cnt, idx->s_off, (int)idx->s_stride, ws,
                        stream));
   const int nloc = (int)(sh->seq_len / 64 / world);
@@ -130,6 +137,8 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
                               cudaStream_t st);
 mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st);
+mt_status f32_to_bf16_x3(const float* x0, void* y0, int64_t n0, const float* x1, void* y1,
+                         int64_t n1, const float* x2, void* y2, int64_t n2, cudaStream_t st);
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -189,17 +198,16 @@ extern "C" mt_status mt_sparse_attn_bwd(const mt_shape* sh, const void* q, const
   const int64_t S = sh->seq_len;
   const int Hq = sh->n_q_heads, Hkv = sh->n_kv_heads;
   VSPlan plan;
-  MT_TRY(vs_plan_build(&plan, S, Hq, Hkv, 1, idx->v_cnt, idx->v_idx, idx->v_stride, idx->s_cnt,
+  MT_TRY(vs_plan_build(&plan, S, Hq, Hkv, 1, 0, idx->v_cnt, idx->v_idx, idx->v_stride, idx->s_cnt,
                        idx->s_off, (int)idx->s_stride, w.plan, stream));
   MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream));
-  cudaMemsetAsync(w.dq, 0, (size_t)S * Hq * 128 * 4, stream);
-  cudaMemsetAsync(w.dk, 0, (size_t)S * Hkv * 128 * 4, stream);
-  cudaMemsetAsync(w.dv, 0, (size_t)S * Hkv * 128 * 4, stream);
+  // dq, dk, dv are adjacent in the workspace (carve_bwd): one memset clears all three
+  cudaMemsetAsync(w.dq, 0, (size_t)((const char*)(w.dv + S * Hkv * 128) - (const char*)w.dq),
+                  stream);
   MT_TRY(attn_bwd_step(plan, 0, 0, (int)(S / 64), q, k, v, dO, lse, w.D, w.dq, w.dk, w.dv,
                        device_num_sms(), stream));
-  MT_TRY(f32_to_bf16(w.dq, dq, S * Hq * 128, stream));
-  MT_TRY(f32_to_bf16(w.dk, dk, S * Hkv * 128, stream));
-  return f32_to_bf16(w.dv, dv, S * Hkv * 128, stream);
+  return f32_to_bf16_x3(w.dq, dq, S * Hq * 128, w.dk, dk, S * Hkv * 128, w.dv, dv, S * Hkv * 128,
+                        stream);
 }
 
 extern "C" mt_status mt_attn_bwd_preprocess(const mt_shape* sh, int world, const void* o_loc,
@@ -228,7 +236,8 @@ extern "C" mt_status mt_attn_bwd_step(const mt_shape* sh, int world, int rank, i
   if (!ws || ws_bytes < need) return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   MT_TRY(check_device());
   VSPlan plan;
-  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, world, idx->v_cnt,
+  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, world, sh->layout,
+                       idx->v_cnt,
                        idx->v_idx, idx->v_stride, idx->s_cnt, idx->s_off, (int)idx->s_stride, ws,
                        stream));
   return attn_bwd_step(plan, rank, origin, (int)(sh->seq_len / 64 / world), q_loc, k_chunk,

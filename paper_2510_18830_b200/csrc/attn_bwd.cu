@@ -43,7 +43,7 @@
 
 #include "common.cuh"
 #include "plan.cuh"
-#define MT_TL_ON (P.mode == 0)  // timeline probe: the block (slash) launch only
+#define MT_TL_ON (P.dbg >= 0)  // timeline probe: every tile
 #include "sm100.cuh"
 #include "tmap.cuh"
 
@@ -81,7 +81,7 @@ struct alignas(16) ChunkMeta {
   int stage;       // smem stage holding the chunk's Q / dO / LSE / D
   int tile;        // kEnd: the tile it closes
   int seq;         // producer event index (timeline probe)
-  int pad;
+  int mode;        // kModeBlock / kModeBar: the tile kind this chunk belongs to
 };
 
 struct Smem {
@@ -107,10 +107,12 @@ struct Smem {
 
 struct Params {
   VSPlan plan;
-  int mode;
+  int n_block;              // tiles [0, n_block) are BLOCK tiles, the rest BAR tiles (one launch)
+  int bar_first;            // 1: BAR tiles are numbered first (longest tiles first)
   int r, s, t;              // rank, origin, step residue
   int nloc;                 // local blocks per rank (queries and keys)
-  int n_tiles;              // BLOCK: Hkv * ceil(nloc/2); BAR: upper bound (per-head lists)
+  int n_tiles;              // n_block + upper bound of BAR tiles (per-head lists)
+  int n_bar;                // upper bound of BAR tiles
   float scale_log2;         // log2(e)/sqrt(d)
   float inv_sqrt_d;
   const __nv_bfloat16* k;   // held chunk [S_loc][Hkv][128]
@@ -131,6 +133,7 @@ struct Params {
 
 // ---- tile decoding
 struct Tile {
+  int mode;    // kModeBlock / kModeBar
   bool ok;
   bool skip;   // BAR: part holds no query block after the tile's first column
   int g;       // kv head
@@ -140,19 +143,42 @@ struct Tile {
   int j_lo, j_hi;  // BAR: local query blocks [j_lo, j_hi) of this part
 };
 
-__device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
+// BAR tiles of this launch: sum over q heads of ceil(|origin list| / 128) x parts
+__device__ __forceinline__ int bar_tile_count(const Params& P) {
+  const VSPlan& pl = P.plan;
+  if (P.n_bar == 0) return 0;
+  int n = 0;
+  for (int h = 0; h < pl.Hq; ++h)
+    n += (pl.vptr[h * (pl.W + 1) + P.s + 1] - pl.vptr[h * (pl.W + 1) + P.s] + 127) / 128;
+  return n * P.bar_parts;
+}
+
+// One launch runs both tile kinds (the tail of one overlaps the other): BLOCK tiles
+// [0, n_block) and BAR tiles after them, or BAR tiles first when P.bar_first (their
+// per-tile work is the longest).  nbar = bar_tile_count(P).
+__device__ __forceinline__ Tile decode_tile(const Params& P, int tile, int nbar) {
   Tile T{};
   const VSPlan& pl = P.plan;
   const int W = pl.W;
-  if (P.mode == kModeBlock) {
+  if (tile < 0 || tile >= P.n_block + nbar) return T;
+  int bt;  // BLOCK tile index, or -1
+  if (P.bar_first) {
+    bt = tile >= nbar ? tile - nbar : -1;
+    if (bt < 0) bt = -1 - tile;  // BAR tile -(bt + 1)
+  } else {
+    bt = tile < P.n_block ? tile : -1 - (tile - P.n_block);
+  }
+  if (bt >= 0) {
     const int npairs = (P.nloc + 1) / 2;
-    if (tile < 0 || tile >= (pl.Hq / P.hpt) * npairs) return T;
+    T.mode = kModeBlock;
     T.ok = true;
-    T.h = (tile / npairs) * P.hpt;  // first q head of the tile
+    T.h = (bt / npairs) * P.hpt;  // first q head of the tile
     T.g = T.h / (pl.Hq / pl.Hkv);
-    T.lb0 = 2 * (tile % npairs);  // early key blocks (most work) first
+    T.lb0 = 2 * (bt % npairs);  // early key blocks (most work) first
     return T;
   }
+  tile = -1 - bt;
+  T.mode = kModeBar;
   // BAR: (head, 128-column group, part of the query range).  Parts of at most
   // bar_part_len query blocks keep tile lengths comparable (a group of early
   // columns otherwise walks every later query block); within a head, the parts
@@ -173,7 +199,7 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile) {
       T.j_hi = min(P.nloc, T.j_lo + P.bar_part_len);
       // first rank-local query block after the group's first (smallest) column
       const int bfirst = pl.vcol[(int64_t)h * pl.S + T.e0] >> 6;
-      const int j0 = bfirst + 1 - P.r <= 0 ? 0 : (bfirst + 1 - P.r + W - 1) / W;
+      const int j0 = plan_count_le(pl, P.r, bfirst);
       T.skip = max(T.j_lo, j0) >= T.j_hi;
       return T;
     }
@@ -192,6 +218,8 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
   const int64_t S_loc = (int64_t)P.nloc * 64;
   uint32_t c = 0;  // chunk events (incl. END)
   uint32_t ntile = 0;
+  int cur_mode = kModeBlock;
+  const int nbar = bar_tile_count(P);
   auto emit = [&](int h, int j, uint32_t flags) {
     const uint32_t stage = c % kStages;
     MT_CRUMB(2, 1000000 + (int)c);
@@ -204,6 +232,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       m.h = h;
       m.j = j;
       m.flags = flags;
+      m.mode = cur_mode;
       m.stage = (int)stage;
       const uint32_t bar = smem_u32(&sm.full[stage]);
       mbar_expect_tx(bar, 2 * kTileQ + 512);
@@ -234,8 +263,9 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       if (lane == 0) tile = atomicAdd(P.tile_counter, 1);
       tile = __shfl_sync(0xffffffffu, tile, 0);
     }
-    const Tile T = decode_tile(P, tile);
+    const Tile T = decode_tile(P, tile, nbar);
     if (!T.ok) break;
+    cur_mode = T.mode;
     if (T.skip) continue;
     // ---- K/V tile: wait until every MMA of the previous tile finished and its
     // epilogue (which reads cols[]) is done
@@ -247,7 +277,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     }
     ++ntile;
     const uint32_t kvbar = smem_u32(&sm.kvfull);
-    if (P.mode == kModeBlock) {
+    if (T.mode == kModeBlock) {
       const bool v1 = T.lb0 + 1 < P.nloc;
       if (lane == 0) {
         // a missing second slot re-loads block lb0: every K/V row must be finite
@@ -274,7 +304,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         int m = sm.cols[row];
         if (m < 0) m = m0;  // padding rows duplicate a live row (masked later)
         const int blk = m >> 6;
-        const int64_t lrow = (int64_t)((blk - P.s) / W) * 64 + (m & 63);
+        const int64_t lrow = (int64_t)plan_g2l(pl, blk) * 64 + (m & 63);
         const size_t goff = ((size_t)lrow * pl.Hkv + T.g) * 128 + c16 * 8;
         const uint32_t doff = (c16 >> 3) * 16384 + sw128(row, c16 & 7);
         cp_async_16(kb + doff, P.k + goff);
@@ -286,9 +316,9 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     }
 
     // ---- chunk stream
-    if (P.mode == kModeBlock) {
+    if (T.mode == kModeBlock) {
       const bool v1 = T.lb0 + 1 < P.nloc;
-      const int kb0 = T.lb0 * W + P.s;
+      const int kb0 = plan_l2g(pl, P.s, T.lb0);  // global key block of slot 0
       if (pl.tptr) {
         // block-CSR mode (W = 1): the pair's sorted (gq << 1 | slot) entries; a query
         // block attending both slots has two adjacent entries, emitted once (at the
@@ -320,29 +350,32 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
           carry = __shfl_sync(0xffffffffu, e, 31);
         }
       } else {
-        // query blocks gq = kb0 + x with x on the lattice t + mW (gq = r mod W): slot 0
-        // (key block kb0) is live iff x is a selected offset, slot 1 (kb0 + W) iff x - W
-        // is.  32 lattice points per ballot from the slash bitmap: a scalar walk of the
-        // offset list costs a dependent global load per offset and skips (W-1)/W of them.
+        // local query blocks j >= jfirst (global gq = l2g(r, j) >= kb0; block-striped:
+        // the lattice gq = kb0 + t + mW): slot 0 (key block kb0) is live iff gq - kb0 is a
+        // selected offset, slot 1 (key block kb1) iff gq - kb1 is.  32 query blocks per
+        // ballot from the slash bitmap: a scalar walk of the offset list costs a dependent
+        // global load per offset and skips (W-1)/W of them.
+        const int kb1 = v1 ? plan_l2g(pl, P.s, T.lb0 + 1) : -1;
+        const int jfirst = plan_count_le(pl, P.r, kb0 - 1);
         for (int h = T.h; h < T.h + P.hpt; ++h) {  // the tile's q heads one after another
         const uint32_t* bits = pl.s_bits + (int64_t)h * pl.bits_words;
         auto has = [&](int x) { return x >= 0 && ((bits[x >> 5] >> (x & 31)) & 1u) != 0u; };
-        const int xmax = pl.nb - kb0;  // gq < nb
-        for (int m0 = 0; P.t + m0 * W < xmax; m0 += 32) {
-          const int x = P.t + (m0 + lane) * W;
-          const bool in = x < xmax;
-          const bool a = in && has(x);
-          const bool b = in && v1 && has(x - W);
+        for (int j0 = jfirst; j0 < P.nloc; j0 += 32) {
+          const int j = j0 + lane;
+          const bool in = j < P.nloc;
+          const int gq = plan_l2g(pl, P.r, j);
+          const bool a = in && has(gq - kb0);
+          const bool b = in && v1 && has(gq - kb1);
           const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b);
           uint32_t bal = ba | bb;
           while (bal) {
             const int l = __ffs(bal) - 1;
             bal &= bal - 1;
-            const int xs = P.t + (m0 + l) * W;
+            const int gl = __shfl_sync(0xffffffffu, gq, l);
             uint32_t flags = 0;
-            if ((ba >> l) & 1u) flags |= xs == 0 ? 5u : 1u;      // slot 0 live (+ diagonal)
-            if ((bb >> l) & 1u) flags |= xs == W ? 10u : 2u;     // slot 1 live (+ diagonal)
-            emit(h, (kb0 + xs - P.r) / W, flags);
+            if ((ba >> l) & 1u) flags |= gl == kb0 ? 5u : 1u;  // slot 0 live (+ diagonal)
+            if ((bb >> l) & 1u) flags |= gl == kb1 ? 10u : 2u;  // slot 1 live (+ diagonal)
+            emit(h, j0 + l, flags);
           }
         }
         }
@@ -351,8 +384,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     } else {
       const int bfirst = sm.cols[0] >> 6;
       // first rank-local query block with global block > bfirst
-      int j0 = (bfirst + 1 - P.r + W - 1) / W;
-      if (bfirst + 1 - P.r <= 0) j0 = 0;
+      const int j0 = plan_count_le(pl, P.r, bfirst);
       // walk this part's query blocks from the last one down: the resident bar tiles
       // of a head start together and share each Q/dO/dQ block while it is in L2
       for (int j = T.j_hi - 1; j >= max(j0, T.j_lo); --j) emit(T.h, j, 0u);
@@ -421,7 +453,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     MT_CRUMB(0, 2);
     mbar_wait(smem_u32(&sm.kvfull), ntile & 1);
     ++ntile;
-    if (P.mode == kModeBar) fence_proxy_async_smem();
+    fence_proxy_async_smem();  // BAR tiles: K/V rows arrived by cp.async (generic proxy)
     tc_fence_after();
     // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and its
     // warpgroup's TMEM region is drained; the gradient MMAs of chunk g as soon as its
@@ -537,6 +569,11 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
 __device__ __forceinline__ void red_add_f32(float* addr, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_f32x4(float* addr, const uint32_t* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(__uint_as_float(v[0])),
+               "f"(__uint_as_float(v[1])), "f"(__uint_as_float(v[2])), "f"(__uint_as_float(v[3]))
+               : "memory");
+}
 
 
 __device__ __forceinline__ float ex2(float x) {
@@ -598,6 +635,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
   uint32_t su = 0, gw = 0;  // sfull events, gdone waits
   uint32_t ntile = 0;
+  const int nbar = bar_tile_count(P);
   bool staging_busy = false;  // a bulk reduce may still be reading this warpgroup's buffer
 
   auto wait_staging = [&]() {  // warpgroup-uniform
@@ -703,21 +741,21 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         tile = cm.kind == kEnd ? cm.tile : -1;
         break;
       }
-      if (P.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
+      if (cm.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
 #ifndef MT_TL_WARPS
       if (row == 0) MT_TL(4, cm.seq);
 #endif
       tc_fence_after();
       // which of the 64 queries see this key row
       uint64_t vis;
-      if (P.mode == kModeBlock) {
+      if (cm.mode == kModeBlock) {
         const bool live = (cm.flags >> slot) & 1u;
         const bool diag = (cm.flags >> (2 + slot)) & 1u;
         vis = live ? (diag ? (~0ull << kk) : ~0ull) : 0ull;  // causal: query i >= key kk
       } else {
         bool live = my_col >= 0;
         if (live) {
-          const int gq = cm.j * W + P.r;
+          const int gq = plan_l2g(pl, P.r, cm.j);
           const int blk = my_col >> 6;
           live = blk < gq && !plan_has_slash(pl, cm.h, gq - blk);
         }
@@ -776,7 +814,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       had_chunk = true;
     }
     if (tile < 0) break;  // DONE
-    const Tile T = decode_tile(P, tile);
+    const Tile T = decode_tile(P, tile, nbar);
     wait_staging();  // the epilogue stages dK/dV in the same buffer
     tc_fence_after();
     if (row == 0) sm.tile_chunks[wg] = had_chunk ? 1 : 0;
@@ -787,16 +825,16 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
     // ---- dK (warpgroup 0) / dV (warpgroup 1) epilogue: the tile's key rows
     bool live_row;
     int64_t lrow;
-    if (P.mode == kModeBlock) {
+    if (T.mode == kModeBlock) {
       live_row = any_chunk && !(slot == 1 && T.lb0 + 1 >= P.nloc);
       lrow = (int64_t)(T.lb0 + slot) * 64 + kk;
     } else {
       const int m = sm.cols[row];
       live_row = any_chunk && m >= 0;
-      lrow = live_row ? (int64_t)(((m >> 6) - P.s) / W) * 64 + (m & 63) : 0;
+      lrow = live_row ? (int64_t)plan_g2l(pl, m >> 6) * 64 + (m & 63) : 0;
     }
     const uint32_t col = wg == 0 ? kColDK : kColDV;
-    if (P.mode == kModeBlock) {
+    if (T.mode == kModeBlock) {
       // rows lb0*64 .. +127 are contiguous: stage [128 rows][32 d] fp32 (SW128) in this
       // warpgroup's P/dS buffer, two column groups per round, and bulk reduce-add them
       // (rows past the chunk end are clipped by the tensor map; they hold zeros anyway)
@@ -835,7 +873,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         tmem_ld_wait();
         if (!live_row) continue;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) red_add_f32(dst + c0 + c, __uint_as_float(a[c]));
+        for (int c = 0; c < 32; c += 4) red_add_f32x4(dst + c0 + c, a + c);
       }
     }
     tc_fence_before();
@@ -878,10 +916,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmq);
     tma_prefetch_desc(&tmdo);
-    if (P.mode == kModeBlock) {
-      tma_prefetch_desc(&tmk);
-      tma_prefetch_desc(&tmv);
-    }
+    tma_prefetch_desc(&tmk);
+    tma_prefetch_desc(&tmv);
   }
   tc_fence_before();
   __syncthreads();
@@ -895,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
     }
 #ifdef MT_TIMELINE
-    else if (warp == 3 && blockIdx.x == 0 && P.mode == kModeBlock) {
+    else if (warp == 3 && blockIdx.x == 0) {
       // observer: stamps each stage's "full" completion (load latency = event 1 - event 0)
       for (uint32_t c = 0;; ++c) {
         const uint32_t st = c % kStages;
@@ -941,8 +977,20 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* o, const __nv_bfloat1
   }
 }
 
-__global__ void f32_to_bf16_kernel(const float* x, __nv_bfloat16* y, int64_t n) {
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+struct Cvt3 {  // three fp32 -> bf16 conversions in one launch (dQ, dK, dV)
+  const float* x[3];
+  __nv_bfloat16* y[3];
+  int64_t n[3];
+  int64_t b1, b2;  // first block of segment 1 / 2
+};
+
+__global__ void f32_to_bf16_kernel(Cvt3 c) {
+  const int seg = blockIdx.x < c.b1 ? 0 : (blockIdx.x < c.b2 ? 1 : 2);
+  const int64_t blk = (int64_t)blockIdx.x - (seg == 0 ? 0 : (seg == 1 ? c.b1 : c.b2));
+  const float* x = c.x[seg];
+  __nv_bfloat16* y = c.y[seg];
+  const int64_t n = c.n[seg];
+  const int64_t i = (blk * blockDim.x + threadIdx.x) * 4;
   if (i + 3 < n) {
     const float4 v = *reinterpret_cast<const float4*>(x + i);
     uint2 o;
@@ -970,11 +1018,24 @@ mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S
   return check_launch("bwd_preprocess");
 }
 
-mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st) {
+// y_i = bf16(x_i) for the three (x, y, n) pairs, one launch
+mt_status f32_to_bf16_x3(const float* x0, void* y0, int64_t n0, const float* x1, void* y1,
+                         int64_t n1, const float* x2, void* y2, int64_t n2, cudaStream_t st) {
   const int64_t threads = 256, per = threads * 4;
-  bwd::f32_to_bf16_kernel<<<(unsigned)((n + per - 1) / per), (unsigned)threads, 0, st>>>(
-      x, static_cast<__nv_bfloat16*>(y), n);
+  bwd::Cvt3 c{{x0, x1, x2},
+              {static_cast<__nv_bfloat16*>(y0), static_cast<__nv_bfloat16*>(y1),
+               static_cast<__nv_bfloat16*>(y2)},
+              {n0, n1, n2}, 0, 0};
+  const int64_t g0 = (n0 + per - 1) / per, g1 = (n1 + per - 1) / per, g2 = (n2 + per - 1) / per;
+  c.b1 = g0;
+  c.b2 = g0 + g1;
+  if (g0 + g1 + g2 > 0)
+    bwd::f32_to_bf16_kernel<<<(unsigned)(g0 + g1 + g2), (unsigned)threads, 0, st>>>(c);
   return check_launch("f32_to_bf16");
+}
+
+mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st) {
+  return f32_to_bf16_x3(x, y, n, nullptr, nullptr, 0, nullptr, nullptr, 0, st);
 }
 
 // One ring step of the backward: block part then bar part, accumulating into
@@ -1029,30 +1090,39 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_bwd) failed");
-  // block (slash) part
-  cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);  // one tile counter per launch
-  P.mode = kModeBlock;
+  // one launch: BLOCK (slash) tiles and BAR (vertical) tiles share the dynamic tile counter
+  cudaMemsetAsync(P.tile_counter, 0, sizeof(int), st);
   const int npairs = (nloc + 1) / 2;
-  P.n_tiles = (plan.Hq / P.hpt) * npairs;
-  int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
-  if (grid > 0)
-    attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
-  MT_TRY(check_launch("attn_bwd_kernel(block)"));
-  if (plan.bptr) return MT_OK;  // block-CSR mode: no vertical part
-  // bar (vertical) part: tile count bounded by sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128)
-  P.tile_counter = plan.scratch + 3;
-  P.mode = kModeBar;
-  P.hpt = 1;
-  // query blocks per bar-tile part: 1024 (MT_BWD_BAR_PART overrides, so tests reach the
-  // multi-part path at sizes the oracle checks in full)
-  static const int part_env = getenv("MT_BWD_BAR_PART") ? atoi(getenv("MT_BWD_BAR_PART")) : 1024;
-  const int part_len = part_env > 0 ? part_env : 1024;
+  // fewer heads per BLOCK tile when the launch would otherwise hold too few tiles to fill
+  // the SMs (short sequences / many ring ranks); the bar tiles below are counted too
+  while (P.hpt > 1 && (plan.Hq / P.hpt) * npairs < 2 * num_sms) {
+    int h2 = P.hpt - 1;
+    while (grp % h2) --h2;
+    P.hpt = h2;
+  }
+  P.n_block = (plan.Hq / P.hpt) * npairs;
+  // bar (vertical) part (none in block-CSR mode): tile count bounded by
+  // sum_h ceil(|i_v^(s)(h)| / 128) <= Hq * ceil(S/128); the exact count is read on device.
+  // Query blocks per bar-tile part: 1024 (MT_BWD_BAR_PART overrides, so tests reach the
+  // multi-part path at sizes the oracle checks in full); ranges of <= 1024 blocks are cut into
+  // 4 parts of >= 16 blocks so a few long early-column tiles do not make the tail.
+  static const int part_env = getenv("MT_BWD_BAR_PART") ? atoi(getenv("MT_BWD_BAR_PART")) : 0;
+  int part_len = part_env > 0 ? part_env : 1024;
+  if (part_env <= 0 && nloc <= 1024) part_len = nloc / 4 > 16 ? nloc / 4 : 16;
   P.bar_part_len = nloc < part_len ? (nloc > 0 ? nloc : 1) : part_len;
   P.bar_parts = (nloc + P.bar_part_len - 1) / P.bar_part_len;
-  P.n_tiles = plan.Hq * (int)((S_loc + 127) / 128) * P.bar_parts;
-  grid = num_sms;
-  attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
-  return check_launch("attn_bwd_kernel(bar)");
+  P.n_bar = plan.bptr ? 0 : plan.Hq * (int)((S_loc + 127) / 128) * P.bar_parts;
+  P.n_tiles = P.n_block + P.n_bar;
+  // BAR tiles first (longest first) up to 2048 local blocks; beyond that their long query
+  // walks evict the BLOCK tiles' shared Q/dO blocks from L2 (measured at 512K, W = 1:
+  // 298 ms bar-first vs 279 ms block-first; at 4K: 0.095 vs 0.116 ms, 128K: 17.8 vs 18.1).
+  // MT_BWD_BAR_FIRST=0/1 overrides.
+  static const int bar_first_env = getenv("MT_BWD_BAR_FIRST") ? atoi(getenv("MT_BWD_BAR_FIRST")) : -1;
+  P.bar_first = bar_first_env >= 0 ? bar_first_env : (nloc <= 2048 ? 1 : 0);
+  const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
+  if (grid > 0)
+    attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+  return check_launch("attn_bwd_kernel");
 }
 
 }  // namespace mt

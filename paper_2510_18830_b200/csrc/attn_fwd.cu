@@ -58,6 +58,8 @@ constexpr int kSoftmax = 256;
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB
 constexpr uint32_t kTileQ2 = 128 * 128 * 2;  // 32 KB: the head pair's 128 query rows
 constexpr float kOverflow = 64.f;            // log2 headroom above the stabiliser
+constexpr float kUnderflow = -100.f;         // a row whose every live score is this far below
+                                             // its stabiliser (log2) goes to the exact fix-up
 
 // kBarP: a bar chunk of 128 consecutive packed rows of one head (TMA), live rows in `mask`
 enum : int { kBlk = 0, kBar = 1, kEnd = 2, kDone = 3, kBarP = 4 };
@@ -101,6 +103,7 @@ struct Smem {
   SMeta smeta[3];
   alignas(16) float m[128];         // row stabilisers of the tile (log2 domain)
   alignas(16) float lsum[2][128];   // per warpgroup: row sums of its chunks
+  alignas(16) float emx[2][128];    // per warpgroup: largest live exponent of the row
   int stage_rows[192];
   // bar chunks: K-gather requests from the K producer (warp 0) to the gatherer (warp 3)
   struct alignas(16) GatherReq {
@@ -220,7 +223,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     if (tile >= P.n_tiles) break;
     int h0, h1, j;
     tile_coords(P, tile, h0, h1, j);
-    const int g = j * W + P.r;
+    const int g = plan_l2g(pl, P.r, j);  // global query block (plan.cuh layouts)
     const int gkv = h0 / grp;
     if (!first_tile) {
       mbar_wait(smem_u32(&sm.qempty), qe_phase);
@@ -256,8 +259,8 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     {
       // live0 / live1: per slot, bit x = head x of the pair attends that key block
       auto emit_pair = [&](int o0, int o1, uint32_t live0, uint32_t live1) {  // o1 < 0: slot empty
-        const int lb0 = (g - o0 - P.s) / W;
-        const int lb1 = o1 >= 0 ? (g - o1 - P.s) / W : lb0;
+        const int lb0 = plan_g2l(pl, g - o0);
+        const int lb1 = o1 >= 0 ? plan_g2l(pl, g - o1) : lb0;
         uint32_t flags = live0 & 3u;
         if (o1 >= 0) flags |= (live1 & 3u) << 2;
         if (o0 == 0) flags |= 16u;
@@ -309,16 +312,19 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         }
         if (pend >= 0) emit_pair(pend, -1, 1u, 0u);
       }
-      // lattice o = t + mW (o <= g) tested 32 at a time against both bitmaps
-      const int npts = (pl.bptr || g < P.t) ? 0 : (g - P.t) / W + 1;
+      // the origin's key blocks <= g, nearest first: point m is local key block
+      // npts-1-m, offset o(m) = g - l2g(s, npts-1-m) ascending (block-striped: the lattice
+      // o = t + mW); tested 32 at a time against both bitmaps
+      const int npts = pl.bptr ? 0 : plan_count_le(pl, P.s, g);
+      auto o_of = [&](int m) { return g - plan_l2g(pl, P.s, npts - 1 - m); };
       int f0 = -1, f1 = -1;  // each head's first offset
       for (int m0 = 0; m0 < npts && (f0 < 0 || (h1 >= 0 && f1 < 0)); m0 += 32) {
-        const int o = P.t + (m0 + lane) * W;
+        const int o = o_of(m0 + lane);
         const bool in = m0 + lane < npts;
         const uint32_t ba = __ballot_sync(0xffffffffu, in && has(0, o));
         const uint32_t bb = __ballot_sync(0xffffffffu, in && has(1, o));
-        if (f0 < 0 && ba) f0 = P.t + (m0 + __ffs(ba) - 1) * W;
-        if (f1 < 0 && bb) f1 = P.t + (m0 + __ffs(bb) - 1) * W;
+        if (f0 < 0 && ba) f0 = o_of(m0 + __ffs(ba) - 1);
+        if (f1 < 0 && bb) f1 = o_of(m0 + __ffs(bb) - 1);
       }
       int skip0 = -1, skip1 = -1;
       if (f0 >= 0 && f1 >= 0 && f0 != f1) {
@@ -328,13 +334,13 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
       }
       int pending = -1;
       for (int m0 = 0; m0 < npts; m0 += 32) {
-        const int o = P.t + (m0 + lane) * W;
+        const int o = o_of(m0 + lane);
         const bool in = m0 + lane < npts && o != skip0 && o != skip1;
         uint32_t bal = __ballot_sync(0xffffffffu, in && (has(0, o) || has(1, o)));
         while (bal) {
           const int l = __ffs(bal) - 1;
           bal &= bal - 1;
-          const int ov = P.t + (m0 + l) * W;
+          const int ov = __shfl_sync(0xffffffffu, o, l);
           if (pending < 0) {
             pending = ov;
           } else {
@@ -445,7 +451,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
             if (blk < g) {
               more = true;
               keep = !covered(g - blk);
-              lrow = ((blk - P.s) / W) * 64 + (m & 63);
+              lrow = plan_g2l(pl, blk) * 64 + (m & 63);
             }
           }
           const uint32_t bal = __ballot_sync(0xffffffffu, keep);
@@ -744,7 +750,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
   uint32_t base = 0, mr_phase = 0, ntile = 0;
 
   for (;;) {
-    float m = -INFINITY, l = 0.f;
+    float m = -INFINITY, l = 0.f, tile_emax = -INFINITY;
     bool m_synced = false, ovf = false;
     int tile = -1;
     for (uint32_t k = (uint32_t)wg;; k += 2) {  // this warpgroup's chunks of the tile
@@ -769,7 +775,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
       tc_fence_after();
       if (!m_synced) {
         if (wg == 0) {  // chunk 0: exact max of the row's live scores
-          float mx = -INFINITY;
+          float mx = -INFINITY, mx_all = -INFINITY;
 #pragma unroll 1
           for (int cg = 0; cg < 4; ++cg) {
             uint32_t sv[32];
@@ -777,9 +783,16 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
             tmem_ld_wait();
             const uint32_t lv = live_bits(cm, x, qi, cg);
 #pragma unroll
-            for (int cc = 0; cc < 32; ++cc)
-              if ((lv >> cc) & 1u) mx = fmaxf(mx, __uint_as_float(sv[cc]) * sc);
+            for (int cc = 0; cc < 32; ++cc) {
+              const float v = __uint_as_float(sv[cc]) * sc;
+              mx_all = fmaxf(mx_all, v);
+              if ((lv >> cc) & 1u) mx = fmaxf(mx, v);
+            }
           }
+          // a row with no live key in chunk 0 (ring steps: its head has no slash block of
+          // this origin, only bars) takes the chunk's largest score against the same kv
+          // head's keys as its scale; the overflow / underflow checks keep it exact
+          if (mx == -INFINITY) mx = mx_all;
           sm.m[row] = mx;
           m = mx;
           mbar_arrive(mready);
@@ -835,6 +848,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
         tmem_st16(Sb + 16 * cg, pk);
       }
       ovf |= emax > kOverflow || (any_live && m == -INFINITY);
+      tile_emax = fmaxf(tile_emax, emax);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(pfull);
@@ -867,6 +881,12 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
     if (row == 0) MT_CRUMB(3 + wg, 6000000 + (int)ntile);
     tc_fence_after();
     sm.lsum[wg][row] = l;
+    sm.emx[wg][row] = tile_emax;
+    named_bar_sync(3, kSoftmax);
+    {  // underflow: the row has live keys but all of them sit far below the stabiliser
+      const float e = fmaxf(sm.emx[0][row], sm.emx[1][row]);
+      if (e > -INFINITY && e < kUnderflow) sm.ovf[ntile & 1] = 1;
+    }
     named_bar_sync(3, kSoftmax);
     if (row == 0) MT_CRUMB(5 + wg, 7000000 + (int)ntile);
     const bool tile_ovf = sm.ovf[ntile & 1] != 0;
@@ -1036,8 +1056,8 @@ __device__ __forceinline__ void for_each_key(const Params& P, int h, int g, int 
   for (int x = 0; x < ns; ++x) {
     const int o = offs[x];
     if (o > g) break;
-    if ((o % W) != P.t) continue;
-    const int lb = (g - o - P.s) / W;
+    if (plan_owner(pl, g - o) != P.s) continue;
+    const int lb = plan_g2l(pl, g - o);
     const int lim = (o == 0) ? i : 63;  // diagonal block: causal
     for (int kk = 0; kk <= lim; ++kk) fn(lb * 64 + kk);
   }
@@ -1048,7 +1068,7 @@ __device__ __forceinline__ void for_each_key(const Params& P, int h, int g, int 
     const int blk = m >> 6;
     if (blk >= g) break;
     if (plan_has_slash(pl, h, g - blk)) continue;
-    fn(((blk - P.s) / W) * 64 + (m & 63));
+    fn(plan_g2l(pl, blk) * 64 + (m & 63));
   }
 }
 __global__ void __launch_bounds__(256) attn_fwd_fixup(const __grid_constant__ Params P,
@@ -1063,7 +1083,7 @@ __global__ void __launch_bounds__(256) attn_fwd_fixup(const __grid_constant__ Pa
     tile_coords(P, P.fix_list[f >> 1], h0, h1, j);
     const int h = (f & 1) ? h1 : h0;
     if (h < 0) continue;
-    const int g = j * pl.W + P.r, gkv = h / grp;
+    const int g = plan_l2g(pl, P.r, j), gkv = h / grp;
     for (int i = w; i < 64; i += 8) {
       const int64_t tok = (int64_t)j * 64 + i;
       float qv[4];
@@ -1135,7 +1155,7 @@ __global__ void pack_bars_kernel(VSPlan pl, int s, const __nv_bfloat16* __restri
     uint4 val = make_uint4(0u, 0u, 0u, 0u);
     if (i < n) {
       const int m = vc[i];
-      const int64_t lrow = (int64_t)(((m >> 6) - s) / W) * 64 + (m & 63);
+      const int64_t lrow = (int64_t)plan_g2l(pl, m >> 6) * 64 + (m & 63);
       const __nv_bfloat16* src = (part < 16 ? k : v) + (lrow * pl.Hkv + h / grp) * 128;
       val = reinterpret_cast<const uint4*>(src)[c16];
     }

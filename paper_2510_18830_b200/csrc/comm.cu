@@ -24,8 +24,8 @@ namespace mt {
 struct NcclCollectives final : VSCollectives {
   mt_comm* c;
   explicit NcclCollectives(mt_comm* cm) : c(cm) {}
-  mt_status bcast_window(__nv_bfloat16* qwin, size_t n, cudaStream_t st) override {
-    return nccl_check(ncclBroadcast(qwin, qwin, n * 2, ncclUint8, c->world - 1, c->nccl, st),
+  mt_status bcast_window(__nv_bfloat16* qwin, size_t n, int root, cudaStream_t st) override {
+    return nccl_check(ncclBroadcast(qwin, qwin, n * 2, ncclUint8, root, c->nccl, st),
                       "ncclBroadcast(window)");
   }
   mt_status allreduce_max(float* M, size_t n, cudaStream_t st) override {
@@ -218,7 +218,8 @@ extern "C" mt_status mt_comm_destroy(mt_comm* c) {
 
 mt_status mt_build_vs_index_dist(mt_comm* comm, const mt_shape* sh, const mt_vs_params* prm,
                                  const void* q, const void* k, mt_vs_index* out, void* ws,
-                                 size_t ws_bytes, mt_stream_t st) {
+                                 size_t ws_bytes, mt_stream_t st, const mt::RopeArgs* rope,
+                                 void* q_out, void* k_out) {
 #ifdef MT_HAVE_NCCL
   const int W = comm->world;
   MT_TRY(check_shape(sh, W));
@@ -233,11 +234,13 @@ mt_status mt_build_vs_index_dist(mt_comm* comm, const mt_shape* sh, const mt_vs_
   const size_t need = vsidx_workspace_bytes(sh->seq_len, sh->n_q_heads, W);
   if (!ws || ws_bytes < need) return fail(MT_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   NcclCollectives coll(comm);
-  return vsidx_build(&coll, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, W, comm->rank, prm->p_v,
+  return vsidx_build(&coll, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, W, comm->rank, sh->layout,
+                     prm->p_v,
                      prm->p_s, q, k, out->v_cnt, out->v_idx, out->v_stride, out->s_cnt,
-                     out->s_off, out->s_stride, nullptr, nullptr, ws, st);
+                     out->s_off, out->s_stride, nullptr, nullptr, ws, st, rope, q_out, k_out);
 #else
   (void)comm; (void)sh; (void)prm; (void)q; (void)k; (void)out; (void)ws; (void)ws_bytes; (void)st;
+  (void)rope; (void)q_out; (void)k_out;
   return fail(MT_EUNSUPPORTED, "built without NCCL");
 #endif
 }

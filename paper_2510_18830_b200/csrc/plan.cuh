@@ -13,11 +13,19 @@
 #pragma once
 #include <cstdint>
 
+#ifndef __CUDACC__
+#include <algorithm>
+using std::max;
+using std::min;
+#endif
+
 namespace mt {
 
 struct VSPlan {
   int64_t S;        // global sequence length
-  int Hq, Hkv, W;   // heads, world size (ranks of the block-striped layout)
+  int Hq, Hkv, W;   // heads, world size (ranks of the layout)
+  int layout;       // MT_LAYOUT_STRIPED (0) or MT_LAYOUT_ZIGZAG (1), see layout_* below
+  int zc;           // zigzag: blocks per chunk (nb / 2W)
   int nb;           // global 64-token blocks = S / 64
   int s_stride;     // row stride of s_off (>= nb)
   int bits_words;   // 32-bit words per head in s_bits
@@ -44,8 +52,47 @@ struct VSPlan {
   int pcap;             // packed rows per head (multiple of 128; 0 = no packing)
 };
 
+// ---- sequence layouts (Fig. 1), at 64-token block granularity
+//   striped (the method): global block b on rank b mod W, local block b / W;
+//   zigzag  (the "Ours w/ ZigZag" ablation): 2W chunks of zc blocks, rank r holds
+//           chunk r then chunk 2W-1-r.
+// Both map a rank's local blocks to ascending global blocks.
+__host__ __device__ __forceinline__ int layout_l2g(int layout, int W, int zc, int r, int lb) {
+  if (layout == 0) return lb * W + r;
+  return lb < zc ? r * zc + lb : (2 * W - 1 - r) * zc + (lb - zc);
+}
+__host__ __device__ __forceinline__ int layout_owner(int layout, int W, int zc, int gb) {
+  if (layout == 0) return gb % W;
+  const int k = gb / zc;
+  return k < W ? k : 2 * W - 1 - k;
+}
+__host__ __device__ __forceinline__ int layout_g2l(int layout, int W, int zc, int gb) {
+  if (layout == 0) return gb / W;
+  const int k = gb / zc;
+  return k < W ? gb - k * zc : zc + gb - k * zc;
+}
+// local blocks of rank r whose global block is <= g
+__host__ __device__ __forceinline__ int layout_count_le(int layout, int W, int zc, int r, int g) {
+  if (layout == 0) return g < r ? 0 : (g - r) / W + 1;
+  const int a = min(max(g - r * zc + 1, 0), zc);
+  const int b = min(max(g - (2 * W - 1 - r) * zc + 1, 0), zc);
+  return a + b;
+}
 __device__ __forceinline__ bool plan_has_slash(const VSPlan& p, int h, int o) {
   return (p.s_bits[(int64_t)h * p.bits_words + (o >> 5)] >> (o & 31)) & 1u;
+}
+
+__host__ __device__ __forceinline__ int plan_l2g(const VSPlan& p, int r, int lb) {
+  return layout_l2g(p.layout, p.W, p.zc, r, lb);
+}
+__host__ __device__ __forceinline__ int plan_owner(const VSPlan& p, int gb) {
+  return layout_owner(p.layout, p.W, p.zc, gb);
+}
+__host__ __device__ __forceinline__ int plan_g2l(const VSPlan& p, int gb) {
+  return layout_g2l(p.layout, p.W, p.zc, gb);
+}
+__host__ __device__ __forceinline__ int plan_count_le(const VSPlan& p, int r, int g) {
+  return layout_count_le(p.layout, p.W, p.zc, r, g);
 }
 
 }  // namespace mt

@@ -24,7 +24,8 @@
 namespace mt {
 
 size_t vs_plan_bytes(int64_t S, int Hq, int W);
-mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const int32_t* v_cnt,
+mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, int layout,
+                        const int32_t* v_cnt,
                         const int32_t* v_idx, int64_t v_stride, const int32_t* s_cnt,
                         const int32_t* s_off, int s_stride, void* ws, cudaStream_t st);
 mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* q,
@@ -37,6 +38,8 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
                               cudaStream_t st);
 mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st);
+mt_status f32_to_bf16_x3(const float* x0, void* y0, int64_t n0, const float* x1, void* y1,
+                         int64_t n1, const float* x2, void* y2, int64_t n2, cudaStream_t st);
 mt_status check_shape(const mt_shape* sh, int W);
 mt_status check_index(const mt_vs_index* idx, const mt_shape* sh);
 mt_status check_device();
@@ -344,7 +347,8 @@ extern "C" mt_status mt_ring_attn_fwd(mt_comm* comm, const mt_shape* sh, const v
   const int64_t S_loc = sh->seq_len / W;
   const int nloc = (int)(S_loc / 64);
   VSPlan plan;
-  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, W, idx->v_cnt,
+  MT_TRY(vs_plan_build(&plan, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, W, sh->layout,
+                       idx->v_cnt,
                        idx->v_idx, idx->v_stride, idx->s_cnt, idx->s_off, (int)idx->s_stride,
                        w.plan, stream));
   const auto sched = ring_schedule(W, comm->inner);
@@ -391,7 +395,7 @@ extern "C" mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* sh, const v
   const int Hq = sh->n_q_heads, Hkv = sh->n_kv_heads;
   const int64_t nkv = S_loc * Hkv * 128;  // floats of dK (= of dV)
   VSPlan plan;
-  MT_TRY(vs_plan_build(&plan, sh->seq_len, Hq, Hkv, W, idx->v_cnt, idx->v_idx, idx->v_stride,
+  MT_TRY(vs_plan_build(&plan, sh->seq_len, Hq, Hkv, W, sh->layout, idx->v_cnt, idx->v_idx, idx->v_stride,
                        idx->s_cnt, idx->s_off, (int)idx->s_stride, w.plan, stream));
   MT_TRY(attn_bwd_preprocess(o_loc, dO_loc, w.D, S_loc, Hq, stream));
   cudaMemsetAsync(w.dq, 0, (size_t)S_loc * Hq * 128 * 4, stream);
@@ -454,9 +458,8 @@ extern "C" mt_status mt_ring_attn_bwd(mt_comm* comm, const mt_shape* sh, const v
   cudaEventDestroy(ev_done);
   for (int i = 0; i < 2; ++i) cudaEventDestroy(ev_p[i]);
   MT_TRY(st);
-  MT_TRY(f32_to_bf16(w.dq, dq_loc, S_loc * Hq * 128, stream));
-  MT_TRY(f32_to_bf16(w.dkv_acc, dk_loc, nkv, stream));
-  return f32_to_bf16(w.dkv_acc + nkv, dv_loc, nkv, stream);
+  return f32_to_bf16_x3(w.dq, dq_loc, S_loc * Hq * 128, w.dkv_acc, dk_loc, nkv,
+                        w.dkv_acc + nkv, dv_loc, nkv, stream);
 #else
   (void)comm; (void)sh; (void)q_loc; (void)k_loc; (void)v_loc; (void)o_loc; (void)lse_loc;
   (void)dO_loc; (void)idx; (void)dq_loc; (void)dk_loc; (void)dv_loc; (void)ws; (void)ws_bytes;

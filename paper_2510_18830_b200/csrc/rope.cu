@@ -12,6 +12,8 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "plan.cuh"
+#include "rope.cuh"
 #include "../../include/mtsa.h"
 
 namespace mt {
@@ -23,19 +25,22 @@ struct RopeParams {
   int inverse;
   int64_t rows;  // local tokens
   int H, W, r;
+  int layout, zc;  // rank layout of the rows (plan.cuh)
 };
 
-__global__ void rope_kernel(const __grid_constant__ RopeParams p, __nv_bfloat16* x) {
+__global__ void rope_kernel(const __grid_constant__ RopeParams p, const __nv_bfloat16* src,
+                            __nv_bfloat16* x) {
   const int64_t n_items = p.rows * p.H * 8;
   for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < n_items;
        it += (int64_t)gridDim.x * blockDim.x) {
     const int gi = (int)(it & 7);
     const int64_t th = it >> 3;  // token * H + head
     const int64_t j = th / p.H;
-    const int64_t pos = ((j >> 6) * p.W + p.r) * 64 + (j & 63);  // block-striped global position
+    const int64_t pos = (int64_t)layout_l2g(p.layout, p.W, p.zc, p.r, (int)(j >> 6)) * 64 + (j & 63);
     __nv_bfloat16* v = x + th * 128;
-    uint4 lo = *reinterpret_cast<const uint4*>(v + 8 * gi);
-    uint4 hi = *reinterpret_cast<const uint4*>(v + 64 + 8 * gi);
+    const __nv_bfloat16* vs = src + th * 128;
+    uint4 lo = *reinterpret_cast<const uint4*>(vs + 8 * gi);
+    uint4 hi = *reinterpret_cast<const uint4*>(vs + 64 + 8 * gi);
     __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lo);
     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&hi);
 #pragma unroll
@@ -45,14 +50,11 @@ __global__ void rope_kernel(const __grid_constant__ RopeParams p, __nv_bfloat16*
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int i = 8 * gi + 2 * e + u;
-        double ang = (double)pos * p.theta[i];
-        ang -= floor(ang * 0.15915494309189535) * 6.283185307179586;  // mod 2 pi
         float s, c;
-        sincosf((float)ang, &s, &c);
+        rope_sincos(pos, p.theta[i], &s, &c);  // rope.cuh: shared with the fused index
         if (p.inverse) s = -s;
         const float xl = u ? a.y : a.x, xh = u ? b.y : b.x;
-        ra[u] = p.mscale * (xl * c - xh * s);
-        rb[u] = p.mscale * (xh * c + xl * s);
+        rope_rotate(xl, xh, s, c, p.mscale, &ra[u], &rb[u]);
       }
       l2[e] = __floats2bfloat162_rn(ra[0], ra[1]);
       h2[e] = __floats2bfloat162_rn(rb[0], rb[1]);
@@ -63,6 +65,30 @@ __global__ void rope_kernel(const __grid_constant__ RopeParams p, __nv_bfloat16*
 }
 
 }  // namespace
+
+// x_out = RoPE(x_in) on a rank's token-major [S/W][H][128] bf16 slice in `layout`
+// (in place when x_out == x_in); used by mt_rope and the RoPE-fused index
+mt_status rope_launch(const RopeArgs& ra, int inverse, int64_t seq_len, int world, int rank,
+                      int layout, int n_heads, const void* x_in, void* x_out, cudaStream_t st) {
+  RopeParams p{};
+  for (int i = 0; i < 64; ++i) p.theta[i] = ra.theta[i];
+  p.mscale = ra.mscale;
+  p.inverse = inverse;
+  p.rows = seq_len / world;
+  p.H = n_heads;
+  p.W = world;
+  p.r = rank;
+  p.layout = world > 1 ? layout : 0;
+  p.zc = p.layout ? (int)(seq_len / 64 / (2 * world)) : 0;
+  const int64_t n = p.rows * n_heads * 8;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  rope_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, static_cast<const __nv_bfloat16*>(x_in),
+                                               static_cast<__nv_bfloat16*>(x_out));
+  return check_launch("rope_kernel");
+}
+
 }  // namespace mt
 
 using namespace mt;
@@ -102,18 +128,9 @@ extern "C" mt_status mt_rope(int64_t seq_len, int world, int rank, int n_heads,
     return fail(MT_ESHAPE, "rope: bad arguments");
   if (seq_len < 64 || seq_len % 64) return fail(MT_EWINDOW, "rope: seq_len must be a multiple of 64");
   if (seq_len % (64LL * world)) return fail(MT_ELAYOUT, "rope: seq_len %% (64 world) != 0");
-  RopeParams p{};
-  for (int i = 0; i < 64; ++i) p.theta[i] = theta[i];
-  p.mscale = mscale;
-  p.inverse = inverse;
-  p.rows = seq_len / world;
-  p.H = n_heads;
-  p.W = world;
-  p.r = rank;
-  const int64_t n = p.rows * n_heads * 8;
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  rope_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      p, static_cast<__nv_bfloat16*>(x));
-  return check_launch("rope_kernel");
+  RopeArgs ra{};
+  for (int i = 0; i < 64; ++i) ra.theta[i] = theta[i];
+  ra.mscale = mscale;
+  return rope_launch(ra, inverse, seq_len, world, rank, MT_LAYOUT_STRIPED, n_heads, x, x,
+                     static_cast<cudaStream_t>(stream));
 }

@@ -14,7 +14,8 @@
 namespace mt {
 
 size_t vs_plan_bytes(int64_t S, int Hq, int W);
-mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const int32_t* v_cnt,
+mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, int layout,
+                        const int32_t* v_cnt,
                         const int32_t* v_idx, int64_t v_stride, const int32_t* s_cnt,
                         const int32_t* s_off, int s_stride, void* ws, cudaStream_t st);
 mt_status check_shape(const mt_shape* sh, int W);
@@ -182,7 +183,7 @@ extern "C" mt_status mt_vs_format_count(const mt_shape* sh, const mt_vs_index* i
   const int64_t S = sh->seq_len, nb = S / 64;
   const int Hq = sh->n_q_heads;
   VSPlan pl;
-  MT_TRY(vs_plan_build(&pl, S, Hq, sh->n_kv_heads, 1, idx->v_cnt, idx->v_idx, idx->v_stride,
+  MT_TRY(vs_plan_build(&pl, S, Hq, sh->n_kv_heads, 1, 0, idx->v_cnt, idx->v_idx, idx->v_stride,
                        idx->s_cnt, idx->s_off, (int)idx->s_stride, w.plan, st));
   count_kernel<<<dim3((unsigned)nb, Hq), kThreads, 0, st>>>(pl, w.nblk, w.ncol);
   MT_TRY(check_launch("vs_format count"));
@@ -216,7 +217,7 @@ extern "C" mt_status mt_vs_format_fill(const mt_shape* sh, const mt_vs_index* id
   const int64_t S = sh->seq_len, nb = S / 64;
   const int Hq = sh->n_q_heads;
   VSPlan pl;
-  MT_TRY(vs_plan_build(&pl, S, Hq, sh->n_kv_heads, 1, idx->v_cnt, idx->v_idx, idx->v_stride,
+  MT_TRY(vs_plan_build(&pl, S, Hq, sh->n_kv_heads, 1, 0, idx->v_cnt, idx->v_idx, idx->v_stride,
                        idx->s_cnt, idx->s_off, (int)idx->s_stride, w.plan, st));
   fill_kernel<<<dim3((unsigned)nb, Hq), kThreads, 0, st>>>(pl, blk_ptr, col_ptr, blk_idx, col_idx);
   return check_launch("vs_format fill");

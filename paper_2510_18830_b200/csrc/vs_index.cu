@@ -19,9 +19,13 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "plan.cuh"
+#include "rope.cuh"
 #include "vsidx.cuh"
 
 namespace mt {
+
+int device_num_sms();
 
 namespace vsi {
 
@@ -54,10 +58,11 @@ struct Geo {
   int64_t S;      // global
   int64_t S_loc;  // local keys
   int Hq, Hkv, W, r;
+  int layout, zc;  // sequence layout of the ranks (plan.cuh)
 };
 
 __device__ __forceinline__ int64_t global_col(const Geo& g, int64_t m_loc) {
-  return ((m_loc >> 6) * g.W + g.r) * 64 + (m_loc & 63);
+  return (int64_t)layout_l2g(g.layout, g.W, g.zc, g.r, (int)(m_loc >> 6)) * 64 + (m_loc & 63);
 }
 
 // I3: specified 2^y (y <= 0), every operation one IEEE RN op.
@@ -92,16 +97,27 @@ __device__ __forceinline__ uint64_t shfl_down_u64(uint64_t v, int o) {
 // (32 accumulators) x 32 k values per block in registers, ~80 registers, so three
 // CTAs (24 warps) share an SM to hide the shared-memory broadcast latency
 // (kMinBlocks = 3: 80 registers; 2: 128 registers, no spill; MT_VS_S1_MINB picks).
+//
+// kRope (f3 upstream fusion, mt_rope_vs_index): k holds PRE-RoPE rows; each thread
+// rotates its key row once (rope.cuh, the arithmetic of mt_rope, so the bf16 values are
+// the same bits) into dynamic shared memory, the fold reads it from there, and the first
+// CTA of the kv group (q head h % grp == 0, z == 0) writes the rotated row to k_out.
 constexpr int kRows = 32, kKB = 32;
-template <int kMinBlocks>
+constexpr size_t kRopeSmem = (size_t)16 * kThreads * 16;  // 128 bf16 per key row
+template <int kMinBlocks, bool kRope>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, const __nv_bfloat16* qwin,
                                                              const __nv_bfloat16* k, float* t,
-                                                             float* M) {
+                                                             float* M,
+                                                             const __grid_constant__ RopeArgs ra,
+                                                             __nv_bfloat16* k_out) {
   __shared__ __align__(16) float qs[64][128];
   __shared__ float wmax[kThreads / 32][64];
+  extern __shared__ __align__(16) uint4 krot[];  // kRope: [16][kThreads] rotated rows
   const int h = blockIdx.y;
   const int grp = g.Hq / g.Hkv;
-  for (int e = threadIdx.x; e < 64 * 128; e += kThreads) {
+  // window rows [rlo, rhi) of this CTA: gridDim.z splits the 64 rows at short lengths
+  const int rlo = blockIdx.z * (64 / gridDim.z), rhi = rlo + 64 / gridDim.z;
+  for (int e = threadIdx.x + rlo * 128; e < rhi * 128; e += kThreads) {
     const int i = e >> 7, c = e & 127;
     qs[i][c] = __bfloat162float(qwin[((size_t)i * g.Hq + h) * 128 + c]);
   }
@@ -110,11 +126,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
   const bool in = m < g.S_loc;
   const uint4* src = reinterpret_cast<const uint4*>(k + ((size_t)(in ? m : 0) * g.Hkv + h / grp) * 128);
   const int64_t mg = in ? global_col(g, m) : INT64_MAX;
+  if constexpr (kRope) {
+    uint4* dst = reinterpret_cast<uint4*>(k_out + ((size_t)(in ? m : 0) * g.Hkv + h / grp) * 128);
+    const bool wr = in && h % grp == 0 && blockIdx.z == 0;
+#pragma unroll 1
+    for (int v = 0; v < 8; ++v) {  // pairs (c, c + 64), c = 8v .. 8v + 7
+      uint4 lo = in ? src[v] : make_uint4(0u, 0u, 0u, 0u);
+      uint4 hi = in ? src[v + 8] : make_uint4(0u, 0u, 0u, 0u);
+      __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lo);
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&hi);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 a = __bfloat1622float2(l2[e]), b = __bfloat1622float2(h2[e]);
+        float s0, c0, s1, c1, y[4];
+        rope_sincos(mg, ra.theta[8 * v + 2 * e], &s0, &c0);
+        rope_sincos(mg, ra.theta[8 * v + 2 * e + 1], &s1, &c1);
+        rope_rotate(a.x, b.x, s0, c0, ra.mscale, &y[0], &y[2]);
+        rope_rotate(a.y, b.y, s1, c1, ra.mscale, &y[1], &y[3]);
+        l2[e] = __floats2bfloat162_rn(y[0], y[1]);
+        h2[e] = __floats2bfloat162_rn(y[2], y[3]);
+      }
+      krot[v * kThreads + threadIdx.x] = lo;
+      krot[(v + 8) * kThreads + threadIdx.x] = hi;
+      if (wr) {
+        dst[v] = lo;
+        dst[v + 8] = hi;
+      }
+    }
+  }
   const int64_t n0 = g.S - 64;
   float* th = t + (size_t)h * 64 * g.S_loc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll 1
-  for (int i0 = 0; i0 < 64; i0 += kRows) {
+  for (int i0 = rlo; i0 < rhi; i0 += kRows) {
     float acc[kRows];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) acc[r] = 0.f;
@@ -123,7 +167,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
       float kf[kKB];
 #pragma unroll
       for (int v = 0; v < kKB / 8; ++v) {
-        const uint4 u = in ? src[cb / 8 + v] : make_uint4(0u, 0u, 0u, 0u);
+        uint4 u;
+        if constexpr (kRope)
+          u = krot[(cb / 8 + v) * kThreads + threadIdx.x];  // own row: no barrier needed
+        else
+          u = in ? src[cb / 8 + v] : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -156,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
     }
   }
   __syncthreads();
-  if (threadIdx.x < 64) {
+  if (threadIdx.x >= rlo && threadIdx.x < rhi) {
     float mx = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) mx = fmaxf(mx, wmax[w][threadIdx.x]);
@@ -164,13 +212,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
   }
 }
 
-inline void stage1_launch(dim3 grid, const Geo& g, const __nv_bfloat16* qwin,
-                          const __nv_bfloat16* k, float* t, float* M, cudaStream_t st) {
+inline mt_status stage1_launch(dim3 grid, const Geo& g, const __nv_bfloat16* qwin,
+                               const __nv_bfloat16* k, float* t, float* M, cudaStream_t st,
+                               const RopeArgs* rope = nullptr, __nv_bfloat16* k_out = nullptr) {
   static const int minb = getenv("MT_VS_S1_MINB") ? atoi(getenv("MT_VS_S1_MINB")) : 3;
-  if (minb == 2)
-    stage1_scores<2><<<grid, kThreads, 0, st>>>(g, qwin, k, t, M);
-  else
-    stage1_scores<3><<<grid, kThreads, 0, st>>>(g, qwin, k, t, M);
+  const RopeArgs none{};
+  if (rope) {
+    if (cudaFuncSetAttribute(stage1_scores<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kRopeSmem) != cudaSuccess)
+      return fail(MT_ECUDA, "cudaFuncSetAttribute(stage1 rope) failed");
+    stage1_scores<2, true><<<grid, kThreads, kRopeSmem, st>>>(g, qwin, k, t, M, *rope, k_out);
+  } else if (minb == 2) {
+    stage1_scores<2, false><<<grid, kThreads, 0, st>>>(g, qwin, k, t, M, none, nullptr);
+  } else {
+    stage1_scores<3, false><<<grid, kThreads, 0, st>>>(g, qwin, k, t, M, none, nullptr);
+  }
+  return MT_OK;
+}
+
+// f3: the window queries' RoPE (positions pos0 + i) while staging them: qwin[i][h][:] =
+// RoPE(q[row0 + i][h][:]), the arithmetic of mt_rope (rope.cuh)
+__global__ void rope_window_kernel(const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ qwin,
+                                   int64_t row0, int64_t pos0, int Hq,
+                                   const __grid_constant__ RopeArgs ra) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // (i, h, pair c)
+  if (t >= 64 * Hq * 64) return;
+  const int c = t & 63, ih = t >> 6, hh = ih % Hq, i = ih / Hq;
+  const __nv_bfloat16* src = q + ((size_t)(row0 + i) * Hq + hh) * 128;
+  __nv_bfloat16* dst = qwin + ((size_t)i * Hq + hh) * 128;
+  float s, co, yl, yh;
+  rope_sincos(pos0 + i, ra.theta[c], &s, &co);
+  rope_rotate(__bfloat162float(src[c]), __bfloat162float(src[c + 64]), s, co, ra.mscale, &yl, &yh);
+  dst[c] = __float2bfloat16_rn(yl);
+  dst[c + 64] = __float2bfloat16_rn(yh);
 }
 
 // ---------------------------------------------------------------- stage 2
@@ -184,8 +258,9 @@ __global__ void __launch_bounds__(kThreads) stage2_exp(Geo g, float* t, const fl
   const float Cd = __uint_as_float(kCdBits);
   float* th = t + (size_t)h * 64 * g.S_loc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rlo = blockIdx.z * (64 / gridDim.z), rhi = rlo + 64 / gridDim.z;
 #pragma unroll 4
-  for (int i = 0; i < 64; ++i) {
+  for (int i = rlo; i < rhi; ++i) {
     uint64_t fx = 0;
     if (in) {
       const float tv = th[(size_t)i * g.S_loc + m];
@@ -202,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) stage2_exp(Geo g, float* t, const fl
     if (lane == 0) wsum[warp][i] = fx;
   }
   __syncthreads();
-  if (threadIdx.x < 64) {
+  if (threadIdx.x >= rlo && threadIdx.x < rhi) {
     uint64_t s = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) s += wsum[w][threadIdx.x];
@@ -257,7 +332,7 @@ __global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
     const int64_t lb = (int64_t)blockIdx.x * (kThreads / 64) + threadIdx.x;
     if (lb * 64 < g.S_loc) {
       const uint64_t P = half[2 * threadIdx.x] + half[2 * threadIdx.x + 1];
-      const int64_t kb = lb * g.W + g.r;
+      const int64_t kb = layout_l2g(g.layout, g.W, g.zc, g.r, (int)lb);
       const int64_t nb = g.S / 64;
       const int64_t o = nb - 1 - kb;  // slash offset scored by this block (I6, reading R1)
       const uint64_t hk = kp.hb ? (uint64_t)h << (kScoreBits + kp.ib) : 0ull;
@@ -268,20 +343,14 @@ __global__ void __launch_bounds__(kThreads) stage3_scores(Geo g, const float* t,
 }
 
 // ---------------------------------------------------------------- select
-// One CTA per (head, list): exact top-p budget over sorted keys, then mark
-// the first k indices (plus forced index 0) in a bitmap.
-__global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const uint64_t* sortedP,
-                                                   int64_t nV, int64_t nP, uint64_t pq_v,
-                                                   uint64_t pq_s, uint32_t* bitsV,
-                                                   uint32_t* bitsP, int* kout, int ibV,
-                                                   int ibP) {
-  const int h = blockIdx.x, which = blockIdx.y;
-  const int64_t n = which ? nP : nV;
-  const uint64_t* keys = (which ? sortedP : sortedV) + (size_t)h * n;
-  uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * ((n + 31) / 32);
-  const uint64_t pq = which ? pq_s : pq_v;
+// Per (head, list), block-wide (every thread of the CTA calls these):
+//   topp_count  exact integer top-p budget k over keys sorted by (score desc, index asc)
+//               (I7: smallest k with 2^24 sum_{x<k} score_x >= round(p 2^24) sum score)
+//   mark_bits   the first k indices plus the forced index 0 (reading R7) -> bitmap
+//   compact     ascending compaction of the bitmap -> index list + count (I8)
+// `keys` / `bits` may live in global or shared memory.
+__device__ int64_t topp_count(const uint64_t* keys, int64_t n, uint64_t pq, int ib) {
   const uint64_t smax = (1ull << kScoreBits) - 1;
-  const int ib = which ? ibP : ibV;
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long tot_s;
   __shared__ long long kmin;
@@ -330,28 +399,20 @@ __global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const
     k = kmin;
     if (k == LLONG_MAX) k = n;
   }
+  __syncthreads();  // red / kmin reusable
+  return k;
+}
+
+__device__ __forceinline__ void mark_bits(const uint64_t* keys, int64_t k, int ib, uint32_t* bits) {
   const uint64_t imask = (1ull << ib) - 1;
-  for (int64_t x = tid; x < k; x += nt) {
+  for (int64_t x = threadIdx.x; x < k; x += blockDim.x) {
     const uint64_t idx = keys[x] & imask;
     atomicOr(&bits[idx >> 5], 1u << (idx & 31));
   }
-  if (tid == 0) {
-    atomicOr(&bits[0], 1u);  // forced: column 0 / offset 0 (reading R7)
-    if (kout) kout[h * 2 + which] = (int)k;
-  }
+  if (threadIdx.x == 0) atomicOr(&bits[0], 1u);  // forced: column 0 / offset 0 (reading R7)
 }
 
-// Ascending compaction of a bitmap into an index list.
-__global__ void __launch_bounds__(1024) compact_bits(const uint32_t* bitsV, const uint32_t* bitsP,
-                                                     int64_t nV, int64_t nP, int32_t* v_cnt,
-                                                     int32_t* v_idx, int64_t v_stride,
-                                                     int32_t* s_cnt, int32_t* s_off,
-                                                     int64_t s_stride) {
-  const int h = blockIdx.x, which = blockIdx.y;
-  const int64_t n = which ? nP : nV;
-  const int64_t words = (n + 31) / 32;
-  const uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * words;
-  int32_t* out = which ? s_off + (size_t)h * s_stride : v_idx + (size_t)h * v_stride;
+__device__ void compact(const uint32_t* bits, int64_t words, int32_t* out, int32_t* cnt_out) {
   __shared__ int red[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t per = (words + nt - 1) / nt;
@@ -386,7 +447,155 @@ __global__ void __launch_bounds__(1024) compact_bits(const uint32_t* bitsV, cons
       out[pos++] = (int32_t)(w * 32 + bit);
     }
   }
-  if (tid == nt - 1) (which ? s_cnt : v_cnt)[h] = red[31];
+  if (tid == nt - 1) *cnt_out = red[31];
+}
+
+// One CTA per (head, list): top-p budget over the sorted keys, bitmap marks.
+__global__ void __launch_bounds__(1024) topp_mark(const uint64_t* sortedV, const uint64_t* sortedP,
+                                                   int64_t nV, int64_t nP, uint64_t pq_v,
+                                                   uint64_t pq_s, uint32_t* bitsV,
+                                                   uint32_t* bitsP, int ibV, int ibP) {
+  const int h = blockIdx.x, which = blockIdx.y;
+  const int64_t n = which ? nP : nV;
+  const uint64_t* keys = (which ? sortedP : sortedV) + (size_t)h * n;
+  uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * ((n + 31) / 32);
+  const int ib = which ? ibP : ibV;
+  const int64_t k = topp_count(keys, n, which ? pq_s : pq_v, ib);
+  mark_bits(keys, k, ib, bits);
+}
+
+// Ascending compaction of a bitmap into an index list.
+__global__ void __launch_bounds__(1024) compact_bits(const uint32_t* bitsV, const uint32_t* bitsP,
+                                                     int64_t nV, int64_t nP, int32_t* v_cnt,
+                                                     int32_t* v_idx, int64_t v_stride,
+                                                     int32_t* s_cnt, int32_t* s_off,
+                                                     int64_t s_stride) {
+  const int h = blockIdx.x, which = blockIdx.y;
+  const int64_t n = which ? nP : nV;
+  const int64_t words = (n + 31) / 32;
+  const uint32_t* bits = (which ? bitsP : bitsV) + (size_t)h * words;
+  int32_t* out = which ? s_off + (size_t)h * s_stride : v_idx + (size_t)h * v_stride;
+  compact(bits, words, out, (which ? s_cnt : v_cnt) + h);
+}
+
+// Short sequences (n <= kSmallSel keys per head and list): the whole select in one launch,
+// one CTA per (head, list), keys in registers, no sort.  The top-p set of I7-I8 is the
+// k smallest keys (key order = score desc, index asc) with k the smallest count whose
+// score mass reaches the budget, i.e. every key <= K* where K* is the smallest key value
+// with 2^24 sum_{key <= K*} score >= round(p 2^24) sum score (the mass is a step function
+// of the key value, so K* is a key).  K* is found by a radix search, two key bits per
+// round (three block-wide sums per round); k >= 1 as in the sorted form.  Replaces the
+// device-wide radix sorts (~20 launches), two memsets and two kernels, which dominate
+// the index below ~8K tokens.
+constexpr int kSmallSel = 8192;
+constexpr int kSelThreads = 512;
+constexpr int kSelPer = kSmallSel / kSelThreads;  // keys per thread, in registers
+__global__ void __launch_bounds__(kSelThreads) select_small(const uint64_t* keysV, const uint64_t* keysP,
+                                                      int64_t nV, int64_t nP, uint64_t pq_v,
+                                                      uint64_t pq_s, int ibV, int ibP,
+                                                      int32_t* v_cnt, int32_t* v_idx,
+                                                      int64_t v_stride, int32_t* s_cnt,
+                                                      int32_t* s_off, int64_t s_stride) {
+  __shared__ uint32_t bits[kSmallSel / 32];
+  constexpr int kWarps = kSelThreads / 32;
+  __shared__ unsigned long long part[2][kWarps][3];
+  const int h = blockIdx.x, which = blockIdx.y;
+  const int n = (int)(which ? nP : nV);
+  const int ib = which ? ibP : ibV;
+  const uint64_t pq = which ? pq_s : pq_v;
+  const uint64_t* src = (which ? keysP : keysV) + (size_t)h * n;
+  const int nbits = kScoreBits + ib;
+  const uint64_t lowmask = nbits >= 64 ? ~0ull : (1ull << nbits) - 1;
+  const uint64_t smax = (1ull << kScoreBits) - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t kr[kSelPer];  // key (head bits dropped); ~0 = no key
+#pragma unroll
+  for (int u = 0; u < kSelPer; ++u) {
+    const int x = u * kSelThreads + tid;
+    kr[u] = x < n ? (src[x] & lowmask) : ~0ull;
+  }
+  const int words = (n + 31) / 32;
+  for (int x = tid; x < words; x += kSelThreads) bits[x] = 0u;
+  auto score = [&](uint64_t key) { return smax - ((key >> ib) & smax); };
+  // block-wide sums of (a, b, c); round r uses part[r & 1] (one barrier per round)
+  auto block_sum3 = [&](int r, unsigned long long& a, unsigned long long& b,
+                        unsigned long long& c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      part[r & 1][warp][0] = a;
+      part[r & 1][warp][1] = b;
+      part[r & 1][warp][2] = c;
+    }
+    __syncthreads();
+    a = b = c = 0ull;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      a += part[r & 1][w][0];
+      b += part[r & 1][w][1];
+      c += part[r & 1][w][2];
+    }
+  };
+  // total mass and the smallest key (k >= 1)
+  unsigned long long tot = 0;
+  uint64_t mn = ~0ull;
+#pragma unroll
+  for (int u = 0; u < kSelPer; ++u)
+    if (kr[u] != ~0ull) {
+      tot += score(kr[u]);
+      mn = min(mn, kr[u]);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)mn, o));
+  {
+    unsigned long long dummy = 0;
+    block_sum3(0, tot, dummy, dummy);
+  }
+  __shared__ unsigned long long wmin[kWarps];
+  if (lane == 0) wmin[warp] = mn;
+  __syncthreads();
+  mn = ~0ull;
+  for (int w = 0; w < kWarps; ++w) mn = min(mn, (uint64_t)wmin[w]);
+  uint64_t thr = ~0ull;  // select every key <= thr
+  if (pq < (1ull << 24)) {
+    const unsigned long long rhs = pq * tot;
+    uint64_t prefix = 0;
+    int round = 1;
+    for (int b = ((nbits + 1) & ~1) - 2; b >= 0; b -= 2, ++round) {
+      const uint64_t ones = (1ull << b) - 1;
+      const uint64_t c0 = prefix | ones, c1 = prefix | (1ull << b) | ones,
+                     c2 = prefix | (2ull << b) | ones;
+      unsigned long long s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+      for (int u = 0; u < kSelPer; ++u) {
+        const uint64_t key = kr[u];
+        const unsigned long long sc = key != ~0ull ? score(key) : 0ull;
+        s0 += key <= c0 ? sc : 0ull;
+        s1 += key <= c1 ? sc : 0ull;
+        s2 += key <= c2 ? sc : 0ull;
+      }
+      block_sum3(round, s0, s1, s2);
+      const uint64_t d = (s0 << 24) >= rhs ? 0 : (s1 << 24) >= rhs ? 1 : (s2 << 24) >= rhs ? 2 : 3;
+      prefix |= d << b;
+    }
+    thr = max(prefix, mn);
+  }
+  // marks (plus the forced index 0, reading R7), then ascending compaction
+  const uint64_t imask = (1ull << ib) - 1;
+#pragma unroll
+  for (int u = 0; u < kSelPer; ++u)
+    if (kr[u] != ~0ull && kr[u] <= thr) {
+      const uint32_t idx = (uint32_t)(kr[u] & imask);
+      atomicOr(&bits[idx >> 5], 1u << (idx & 31));
+    }
+  if (tid == 0) atomicOr(&bits[0], 1u);
+  __syncthreads();
+  int32_t* out = which ? s_off + (size_t)h * s_stride : v_idx + (size_t)h * v_stride;
+  compact(bits, words, out, (which ? s_cnt : v_cnt) + h);
 }
 
 __global__ void fill_f32(float* p, float v, int n) {
@@ -470,34 +679,45 @@ static VSIndexWs carve_vsidx(void* base, int64_t S, int Hq, int W) {
 
 size_t vsidx_workspace_bytes(int64_t S, int Hq, int W) { return carve_vsidx(nullptr, S, Hq, W).total; }
 
-mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, int r, float p_v,
-                      float p_s, const void* q_loc, const void* k_loc, int32_t* v_cnt,
+mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, int r, int layout,
+                      float p_v, float p_s, const void* q_loc, const void* k_loc, int32_t* v_cnt,
                       int32_t* v_idx, int64_t v_stride, int32_t* s_cnt, int32_t* s_off,
                       int64_t s_stride, uint64_t* dbg_colV, uint64_t* dbg_blkP, void* ws,
-                      cudaStream_t st) {
+                      cudaStream_t st, const RopeArgs* rope, void* q_out, void* k_out) {
   using namespace vsi;
   VSIndexWs w = carve_vsidx(ws, S, Hq, W);
   const int64_t S_loc = S / W, nb = S / 64, nloc = nb / W;
-  Geo g{S, S_loc, Hq, Hkv, W, r};
-  // window queries (global rows S-64..S-1, held by rank W-1 at its last local block)
+  if (W == 1) layout = 0;
+  Geo g{S, S_loc, Hq, Hkv, W, r, layout, layout ? (int)(nb / (2 * W)) : 0};
+  // window queries (global rows S-64..S-1): the last global block, which is the last local
+  // block of its owner (rank W-1 block-striped, rank 0 zigzag)
+  // (f3, rope != NULL: q / k are pre-RoPE; the window is rotated while staged, then q is
+  // rotated into q_out and k into k_out by stage 1, as mt_rope would)
   const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(q_loc);
-  if (coll) {
-    if (r == W - 1)
+  const int root = coll ? layout_owner(layout, W, g.zc, (int)(nb - 1)) : 0;
+  if (r == root) {
+    if (rope) {
+      rope_window_kernel<<<(64 * Hq * 64 + 255) / 256, 256, 0, st>>>(q, w.qwin, S_loc - 64, S - 64,
+                                                                     Hq, *rope);
+      MT_TRY(check_launch("vs rope window"));
+    } else {
       cudaMemcpyAsync(w.qwin, q + (size_t)(S_loc - 64) * Hq * 128, (size_t)64 * Hq * 128 * 2,
                       cudaMemcpyDeviceToDevice, st);
-    MT_TRY(coll->bcast_window(w.qwin, (size_t)64 * Hq * 128, st));
-  } else {
-    cudaMemcpyAsync(w.qwin, q + (size_t)(S - 64) * Hq * 128, (size_t)64 * Hq * 128 * 2,
-                    cudaMemcpyDeviceToDevice, st);
+    }
   }
+  if (coll) MT_TRY(coll->bcast_window(w.qwin, (size_t)64 * Hq * 128, root, st));
+  if (rope) MT_TRY(rope_launch(*rope, 0, S, W, r, layout, Hq, q_loc, q_out, st));
   fill_f32<<<(Hq * 64 + 255) / 256, 256, 0, st>>>(w.M, -INFINITY, Hq * 64);
   cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
   const dim3 grid((unsigned)((S_loc + kThreads - 1) / kThreads), Hq);
-  stage1_launch(grid, g, w.qwin, static_cast<const __nv_bfloat16*>(k_loc), w.t, w.M, st);
+  // short lengths: split the 64 window rows over 2 CTAs (stages 1-2) to fill the SMs
+  const dim3 grid12(grid.x, grid.y, (int64_t)grid.x * grid.y < 2 * device_num_sms() ? 2 : 1);
+  MT_TRY(stage1_launch(grid12, g, w.qwin, static_cast<const __nv_bfloat16*>(k_loc), w.t, w.M, st,
+                       rope, static_cast<__nv_bfloat16*>(k_out)));
   count_launches(1);  // fill_f32
   MT_TRY(check_launch("vs stage1"));
   if (coll) MT_TRY(coll->allreduce_max(w.M, (size_t)Hq * 64, st));
-  stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
+  stage2_exp<<<grid12, kThreads, 0, st>>>(g, w.t, w.M, w.E);
   MT_TRY(check_launch("vs stage2"));
   if (coll) MT_TRY(coll->allreduce_sum_u64(w.E, (size_t)Hq * 64, st));
   if (dbg_colV) cudaMemsetAsync(dbg_colV, 0, (size_t)Hq * S * 8, st);
@@ -509,6 +729,16 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   if (coll) {
     MT_TRY(coll->allgather_keys(w.keysV_loc, w.keysV, Hq, S_loc, st));
     MT_TRY(coll->allgather_keys(w.keysP_loc, w.keysP, Hq, nloc, st));
+  }
+  const uint64_t pq_v = (uint64_t)llrint((double)p_v * 16777216.0);
+  const uint64_t pq_s = (uint64_t)llrint((double)p_s * 16777216.0);
+  // MT_VS_SELECT_SMALL=0 forces the radix-sort path (tests compare the two)
+  static const bool small_ok = !getenv("MT_VS_SELECT_SMALL") || atoi(getenv("MT_VS_SELECT_SMALL"));
+  if (S <= kSmallSel && small_ok) {
+    select_small<<<dim3(Hq, 2), kSelThreads, 0, st>>>(w.keysV, w.keysP, S, nb, pq_v, pq_s, kv.ib,
+                                                  kp.ib, v_cnt, v_idx, v_stride, s_cnt, s_off,
+                                                  s_stride);
+    return check_launch("vs select_small");
   }
   size_t tb;
   if (kv.hb) {  // one sort of every head's keys (see cub_sort1_bytes)
@@ -544,10 +774,8 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   }
   cudaMemsetAsync(w.bitsV, 0, (size_t)Hq * ((S + 31) / 32) * 4, st);
   cudaMemsetAsync(w.bitsP, 0, (size_t)Hq * ((nb + 31) / 32) * 4, st);
-  const uint64_t pq_v = (uint64_t)llrint((double)p_v * 16777216.0);
-  const uint64_t pq_s = (uint64_t)llrint((double)p_s * 16777216.0);
   topp_mark<<<dim3(Hq, 2), 1024, 0, st>>>(w.sortV, w.sortP, S, nb, pq_v, pq_s, w.bitsV, w.bitsP,
-                                          nullptr, kv.ib, kp.ib);
+                                          kv.ib, kp.ib);
   MT_TRY(check_launch("vs topp"));
   compact_bits<<<dim3(Hq, 2), 1024, 0, st>>>(w.bitsV, w.bitsP, S, nb, v_cnt, v_idx, v_stride,
                                              s_cnt, s_off, s_stride);
@@ -559,10 +787,11 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
 // ---------------------------------------------------------------- C ABI
 using namespace mt;
 
-// distributed variant lives with the NCCL communicator (ring.cu)
+// distributed variant lives with the NCCL communicator (comm.cu)
 mt_status mt_build_vs_index_dist(mt_comm* comm, const mt_shape* sh, const mt_vs_params* prm,
                                  const void* q, const void* k, mt_vs_index* out, void* ws,
-                                 size_t ws_bytes, mt_stream_t st);
+                                 size_t ws_bytes, mt_stream_t st, const RopeArgs* rope,
+                                 void* q_out, void* k_out);
 
 extern "C" size_t mt_build_vs_index_workspace_bytes(const mt_shape* sh, int world) {
   if (!sh || world <= 0) return 0;
@@ -586,16 +815,40 @@ extern "C" mt_status mt_build_vs_index(mt_comm* comm, const mt_shape* sh,
                                        const mt_vs_params* prm, const void* q, const void* k,
                                        mt_vs_index* out, void* ws, size_t ws_bytes,
                                        mt_stream_t st) {
-  if (comm) return mt_build_vs_index_dist(comm, sh, prm, q, k, out, ws, ws_bytes, st);
+  if (comm)
+    return mt_build_vs_index_dist(comm, sh, prm, q, k, out, ws, ws_bytes, st, nullptr, nullptr,
+                                  nullptr);
   MT_TRY(vs_validate(sh, prm, q, k, ws, ws_bytes, 1));
   if (!out || !out->v_cnt || !out->v_idx || !out->s_cnt || !out->s_off)
     return fail(MT_ESHAPE, "output index pointers must be non-NULL");
   if (out->v_stride < sh->seq_len || out->s_stride < sh->seq_len / 64)
     return fail(MT_ECAPACITY, "index capacity: need v_stride >= %lld, s_stride >= %lld",
                 (long long)sh->seq_len, (long long)(sh->seq_len / 64));
-  return vsidx_build(nullptr, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, 1, 0, prm->p_v,
+  return vsidx_build(nullptr, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, 1, 0, 0, prm->p_v,
                      prm->p_s, q, k, out->v_cnt, out->v_idx, out->v_stride, out->s_cnt,
                      out->s_off, out->s_stride, nullptr, nullptr, ws, st);
+}
+
+extern "C" mt_status mt_rope_vs_index(mt_comm* comm, const mt_shape* sh,
+                                      const mt_vs_params* prm, const double* theta, float mscale,
+                                      const void* q, const void* k, void* q_out, void* k_out,
+                                      mt_vs_index* out, void* ws, size_t ws_bytes,
+                                      mt_stream_t st) {
+  if (!theta || !q_out || !k_out) return fail(MT_ESHAPE, "NULL theta / q_out / k_out");
+  if (k_out == k) return fail(MT_ESHAPE, "k_out must not alias k (stage 1 reads k while writing)");
+  RopeArgs ra{};
+  for (int i = 0; i < 64; ++i) ra.theta[i] = theta[i];
+  ra.mscale = mscale;
+  if (comm) return mt_build_vs_index_dist(comm, sh, prm, q, k, out, ws, ws_bytes, st, &ra, q_out, k_out);
+  MT_TRY(vs_validate(sh, prm, q, k, ws, ws_bytes, 1));
+  if (!out || !out->v_cnt || !out->v_idx || !out->s_cnt || !out->s_off)
+    return fail(MT_ESHAPE, "output index pointers must be non-NULL");
+  if (out->v_stride < sh->seq_len || out->s_stride < sh->seq_len / 64)
+    return fail(MT_ECAPACITY, "index capacity: need v_stride >= %lld, s_stride >= %lld",
+                (long long)sh->seq_len, (long long)(sh->seq_len / 64));
+  return vsidx_build(nullptr, sh->seq_len, sh->n_q_heads, sh->n_kv_heads, 1, 0, 0, prm->p_v,
+                     prm->p_s, q, k, out->v_cnt, out->v_idx, out->v_stride, out->s_cnt,
+                     out->s_off, out->s_stride, nullptr, nullptr, ws, st, &ra, q_out, k_out);
 }
 
 extern "C" mt_status mt_vs_column_scores(const mt_shape* sh, const void* q, const void* k,
@@ -610,13 +863,13 @@ extern "C" mt_status mt_vs_column_scores(const mt_shape* sh, const void* q, cons
   VSIndexWs w = carve_vsidx(ws, S, Hq, 1);
   (void)w;
   using namespace vsi;
-  Geo g{S, S, Hq, sh->n_kv_heads, 1, 0};
+  Geo g{S, S, Hq, sh->n_kv_heads, 1, 0, 0, 0};
   cudaMemcpyAsync(w.qwin, static_cast<const __nv_bfloat16*>(q) + (size_t)(S - 64) * Hq * 128,
                   (size_t)64 * Hq * 128 * 2, cudaMemcpyDeviceToDevice, st);
   fill_f32<<<(Hq * 64 + 255) / 256, 256, 0, st>>>(w.M, -INFINITY, Hq * 64);
   cudaMemsetAsync(w.E, 0, (size_t)Hq * 64 * 8, st);
   const dim3 grid((unsigned)((S + kThreads - 1) / kThreads), Hq);
-  stage1_launch(grid, g, w.qwin, static_cast<const __nv_bfloat16*>(k), w.t, w.M, st);
+  MT_TRY(stage1_launch(grid, g, w.qwin, static_cast<const __nv_bfloat16*>(k), w.t, w.M, st));
   stage2_exp<<<grid, kThreads, 0, st>>>(g, w.t, w.M, w.E);
   stage3_scores<<<grid, kThreads, 0, st>>>(g, w.t, w.E, w.keysV, w.keysP, col_scores,
                                            slash_scores, key_layout(S, Hq), key_layout(S / 64, Hq));

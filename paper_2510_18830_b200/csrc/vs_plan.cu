@@ -1,7 +1,8 @@
 // vs_plan.cu — build the kernel-side VSPlan (plan.cuh) from index lists.
 //
 // One CTA per q head.  (1) slash bitmap of i_s[h]; (2) i_v[h] split by KV
-// origin s = floor(m / 64) mod W with order kept (stable compaction), which is
+// origin s = owner(floor(m / 64)) (block-striped: floor(m / 64) mod W; plan.cuh
+// layouts) with order kept (stable compaction), which is
 // the per-origin vertical list of convert_index (Alg. 2, P:845;
 // DESIGN.md I10).
 #include <cstdlib>
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kThreads) vs_plan_kernel(VSPlan p, const int32
     for (int base = 0; base < nv; base += blockDim.x) {
       const int i = base + threadIdx.x;
       int m = (i < nv) ? vin[i] : 0;
-      const int keep = (i < nv) && m >= 0 && m < p.S && (((m >> 6) % p.W) == s);
+      const int keep = (i < nv) && m >= 0 && m < p.S && plan_owner(p, m >> 6) == s;
       int total;
       const int pos = block_exclusive_scan(keep, scan_smem, total);
       if (keep) vout[written + pos] = m;
@@ -110,7 +111,8 @@ size_t vs_plan_bytes(int64_t S, int Hq, int W) {
 }
 
 // Carve the plan out of `ws` and launch the builder.
-mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const int32_t* v_cnt,
+mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, int layout,
+                        const int32_t* v_cnt,
                         const int32_t* v_idx, int64_t v_stride, const int32_t* s_cnt,
                         const int32_t* s_off, int s_stride, void* ws, cudaStream_t st) {
   const int nb = (int)(S / 64);
@@ -132,6 +134,8 @@ mt_status vs_plan_build(VSPlan* out, int64_t S, int Hq, int Hkv, int W, const in
   pl.Hq = Hq;
   pl.Hkv = Hkv;
   pl.W = W;
+  pl.layout = W > 1 ? layout : 0;  // one rank: every layout is the identity
+  pl.zc = pl.layout ? nb / (2 * W) : 0;
   pl.nb = nb;
   pl.s_stride = s_stride;
   pl.bits_words = words;

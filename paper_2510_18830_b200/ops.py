@@ -31,8 +31,11 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return t.data_ptr()
 
 
-def shape(seq_len: int, n_q_heads: int, n_kv_heads: int) -> _lib.Shape:
-    return _lib.Shape(seq_len, n_q_heads, n_kv_heads, HEAD_DIM, BLOCK)
+LAYOUTS = {"striped": 0, "zigzag": 1}  # MT_LAYOUT_STRIPED / MT_LAYOUT_ZIGZAG (include/mtsa.h)
+
+
+def shape(seq_len: int, n_q_heads: int, n_kv_heads: int, layout: str = "striped") -> _lib.Shape:
+    return _lib.Shape(seq_len, n_q_heads, n_kv_heads, HEAD_DIM, BLOCK, LAYOUTS[layout])
 
 
 @dataclass
@@ -48,6 +51,14 @@ class VSIndex:
         nb = seq_len // BLOCK
         z = lambda *s: torch.zeros(*s, dtype=torch.int32, device=device)
         return VSIndex(z(n_q_heads), z(n_q_heads, seq_len), z(n_q_heads), z(n_q_heads, nb))
+
+    @staticmethod
+    def uninit(seq_len: int, n_q_heads: int, device="cuda") -> "VSIndex":
+        """Output buffers for mt_build_vs_index, which writes the counts and every entry
+        below them (entries past a count are never read): no fill kernels."""
+        nb = seq_len // BLOCK
+        e = lambda *s: torch.empty(*s, dtype=torch.int32, device=device)
+        return VSIndex(e(n_q_heads), e(n_q_heads, seq_len), e(n_q_heads), e(n_q_heads, nb))
 
     @staticmethod
     def from_lists(i_v, i_s, seq_len: int, device="cuda") -> "VSIndex":
@@ -122,9 +133,9 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, idx: VSIn
 
 
 def attn_fwd_step(seq_len: int, world: int, rank: int, origin: int, first: bool, last: bool,
-                  q_loc, k_chunk, v_chunk, idx: VSIndex, o, o_acc, lse):
-    """One ring step (mt_attn_fwd_step); tensors are rank-local (striped)."""
-    sh = shape(seq_len, q_loc.shape[1], k_chunk.shape[1])
+                  q_loc, k_chunk, v_chunk, idx: VSIndex, o, o_acc, lse, layout: str = "striped"):
+    """One ring step (mt_attn_fwd_step); tensors are rank-local (in `layout`)."""
+    sh = shape(seq_len, q_loc.shape[1], k_chunk.shape[1], layout)
     L = _lib.lib()
     nbytes = L.mt_sparse_attn_fwd_workspace_bytes(ctypes.byref(sh), world)
     ws = workspace(nbytes)
@@ -139,22 +150,43 @@ class VSParams(ctypes.Structure):
 
 
 def build_vs_index(q: torch.Tensor, k: torch.Tensor, p_v: float, p_s: float, comm=None,
-                   seq_len: int | None = None) -> VSIndex:
+                   seq_len: int | None = None, layout: str = "striped") -> VSIndex:
     """Alg. 1 index on the GPU (mt_build_vs_index).  With `comm`, q/k are the
-    rank-local striped slices and `seq_len` is the global length."""
+    rank-local slices in `layout` and `seq_len` is the global length."""
     S = q.shape[0] if seq_len is None else seq_len
     Hq = q.shape[1]
     world = 1 if comm is None else comm.world
-    sh = shape(S, Hq, k.shape[1])
+    sh = shape(S, Hq, k.shape[1], layout)
     L = _lib.lib()
     ws = workspace(L.mt_build_vs_index_workspace_bytes(ctypes.byref(sh), world))
-    idx = VSIndex.empty(S, Hq, device=q.device)
+    idx = VSIndex.uninit(S, Hq, device=q.device)
     ci = idx.c_struct()
     prm = VSParams(p_v, p_s)
     _lib.check(L.mt_build_vs_index(None if comm is None else comm.handle, ctypes.byref(sh),
                                    ctypes.byref(prm), _ptr(q), _ptr(k), ctypes.byref(ci),
                                    _ptr(ws), ws.numel(), _stream()))
     return idx
+
+
+def rope_vs_index(q: torch.Tensor, k: torch.Tensor, freqs, p_v: float, p_s: float, comm=None,
+                  seq_len: int | None = None, layout: str = "striped"):
+    """f3 fusion (mt_rope_vs_index): from PRE-RoPE q / k, returns (index, RoPE(q), RoPE(k)),
+    the index equal to build_vs_index(RoPE(q), RoPE(k)).  freqs = rope_freqs(...)."""
+    th, ms = freqs
+    S = q.shape[0] if seq_len is None else seq_len
+    Hq = q.shape[1]
+    world = 1 if comm is None else comm.world
+    sh = shape(S, Hq, k.shape[1], layout)
+    L = _lib.lib()
+    ws = workspace(L.mt_build_vs_index_workspace_bytes(ctypes.byref(sh), world))
+    idx = VSIndex.uninit(S, Hq, device=q.device)
+    ci = idx.c_struct()
+    prm = VSParams(p_v, p_s)
+    q_out, k_out = torch.empty_like(q), torch.empty_like(k)
+    _lib.check(L.mt_rope_vs_index(None if comm is None else comm.handle, ctypes.byref(sh),
+                                  ctypes.byref(prm), th, ms, _ptr(q), _ptr(k), _ptr(q_out),
+                                  _ptr(k_out), ctypes.byref(ci), _ptr(ws), ws.numel(), _stream()))
+    return idx, q_out, k_out
 
 
 def vs_column_scores(q: torch.Tensor, k: torch.Tensor):
@@ -184,15 +216,16 @@ def sparse_attn_bwd(q, k, v, o, lse, dO, idx: VSIndex):
     return dq, dk, dv
 
 
-def attn_bwd_preprocess(seq_len: int, world: int, o_loc, dO_loc, D_loc):
-    sh = shape(seq_len, o_loc.shape[1], 1)
+def attn_bwd_preprocess(seq_len: int, world: int, o_loc, dO_loc, D_loc, layout: str = "striped"):
+    sh = shape(seq_len, o_loc.shape[1], 1, layout)
     _lib.check(_lib.lib().mt_attn_bwd_preprocess(ctypes.byref(sh), world, _ptr(o_loc), _ptr(dO_loc),
                                                  _ptr(D_loc), _stream()))
 
 
 def attn_bwd_step(seq_len: int, world: int, rank: int, origin: int, q_loc, k_chunk, v_chunk,
-                  dO_loc, lse_loc, D_loc, idx: VSIndex, dq_acc, dk_acc, dv_acc):
-    sh = shape(seq_len, q_loc.shape[1], k_chunk.shape[1])
+                  dO_loc, lse_loc, D_loc, idx: VSIndex, dq_acc, dk_acc, dv_acc,
+                  layout: str = "striped"):
+    sh = shape(seq_len, q_loc.shape[1], k_chunk.shape[1], layout)
     L = _lib.lib()
     ws = workspace(L.mt_attn_step_workspace_bytes(ctypes.byref(sh), world))
     ci = idx.c_struct()
@@ -397,21 +430,32 @@ def rope_(x: torch.Tensor, freqs, seq_len: int | None = None, world: int = 1, ra
     return x
 
 
-def stripe(x_global: torch.Tensor, world: int, rank: int) -> torch.Tensor:
-    """Rank `rank`'s block-striped share of a token-major tensor (mt_stripe)."""
+def stripe(x_global: torch.Tensor, world: int, rank: int, layout: str = "striped") -> torch.Tensor:
+    """Rank `rank`'s share of a token-major tensor in `layout` (mt_stripe /
+    mt_layout_to_local)."""
     S = x_global.shape[0]
     out = torch.empty((S // world,) + tuple(x_global.shape[1:]), dtype=x_global.dtype,
                       device=x_global.device)
     row = x_global[0].numel() * x_global.element_size()
-    _lib.check(_lib.lib().mt_stripe(S, row, world, rank, _ptr(x_global), _ptr(out), _stream()))
+    if layout == "striped":
+        _lib.check(_lib.lib().mt_stripe(S, row, world, rank, _ptr(x_global), _ptr(out), _stream()))
+    else:
+        _lib.check(_lib.lib().mt_layout_to_local(LAYOUTS[layout], S, row, world, rank, _ptr(x_global),
+                                                 _ptr(out), _stream()))
     return out
 
 
-def unstripe(x_local: torch.Tensor, world: int, rank: int, out: torch.Tensor) -> torch.Tensor:
-    """Scatter rank `rank`'s local rows back into the global tensor `out` (mt_unstripe)."""
+def unstripe(x_local: torch.Tensor, world: int, rank: int, out: torch.Tensor,
+             layout: str = "striped") -> torch.Tensor:
+    """Scatter rank `rank`'s local rows back into the global tensor `out` (mt_unstripe /
+    mt_layout_to_global)."""
     S = out.shape[0]
     row = out[0].numel() * out.element_size()
-    _lib.check(_lib.lib().mt_unstripe(S, row, world, rank, _ptr(x_local), _ptr(out), _stream()))
+    if layout == "striped":
+        _lib.check(_lib.lib().mt_unstripe(S, row, world, rank, _ptr(x_local), _ptr(out), _stream()))
+    else:
+        _lib.check(_lib.lib().mt_layout_to_global(LAYOUTS[layout], S, row, world, rank, _ptr(x_local),
+                                                  _ptr(out), _stream()))
     return out
 
 
@@ -422,8 +466,9 @@ def ring_schedule(world: int, inner: int | None = None):
     return [[out[t * world + x] for x in range(world)] for t in range(world)]
 
 
-def ring_attn_fwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, idx: VSIndex):
-    sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1])
+def ring_attn_fwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, idx: VSIndex,
+                  layout: str = "striped"):
+    sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1], layout)
     L = _lib.lib()
     ws = comm.ring_workspace(max(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 0),
                                  L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 1)))
@@ -435,8 +480,9 @@ def ring_attn_fwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, idx: VSIndex):
     return o, lse
 
 
-def ring_attn_bwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, o_loc, lse_loc, dO_loc, idx: VSIndex):
-    sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1])
+def ring_attn_bwd(comm: Comm, seq_len: int, q_loc, k_loc, v_loc, o_loc, lse_loc, dO_loc, idx: VSIndex,
+                  layout: str = "striped"):
+    sh = shape(seq_len, q_loc.shape[1], k_loc.shape[1], layout)
     L = _lib.lib()
     ws = comm.ring_workspace(max(L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 0),
                                  L.mt_ring_attn_workspace_bytes(ctypes.byref(sh), comm.world, 1)))

@@ -1,7 +1,7 @@
 """torchrun worker: distributed index + flat/hierarchical ring fwd/bwd vs the oracle.
 
 Launched by tests/test_gpu_ring.py (and usable by hand):
-  torchrun --nproc-per-node N tests/dist_ring_worker.py --inner G --seq S
+  torchrun --nproc-per-node N tests/dist_ring_worker.py --inner G --seq S [--layout zigzag]
 Exit code 0 = every check passed (rank 0 prints a JSON summary).
 """
 import argparse
@@ -17,6 +17,7 @@ import torch.distributed as dist
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
+from oracle.sparseformat import layout_perm  # noqa: E402  (the layout's row map, test side)
 from paper_2510_18830_b200 import ops  # noqa: E402
 from synth.generator import bf16_bits_to_f32, make_grad_out, make_qkv  # noqa: E402
 
@@ -26,7 +27,9 @@ def main():
     ap.add_argument("--inner", type=int, default=0)
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--p", type=float, default=0.9)
+    ap.add_argument("--layout", default="striped", choices=["striped", "zigzag"])
     a = ap.parse_args()
+    lay = a.layout
     W, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -35,20 +38,29 @@ def main():
     S, Hq, Hkv = a.seq, 4, 2
     q, k, v = make_qkv(S, Hq, Hkv, seed=31, a=12.0)
     dO = make_grad_out(S, Hq, seed=31)
-    j = np.arange(S // W)
-    rows = ((j // 64) * W + rank) * 64 + j % 64
+    perm = layout_perm(S, W, lay)
+    rows = perm[rank]
     t = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).to(dev)
     ql, kl, vl, dl = (t(x[rows]) for x in (q, k, v, dO))
     ok = {}
     # distributed index == single-GPU index (bit-exact, W-invariant)
-    idx = ops.build_vs_index(ql, kl, a.p, a.p, comm=comm, seq_len=S)
+    idx = ops.build_vs_index(ql, kl, a.p, a.p, comm=comm, seq_len=S, layout=lay)
     idx1 = ops.build_vs_index(t(q), t(k), a.p, a.p)
     iv, is_ = idx.to_lists()
     iv1, is1 = idx1.to_lists()
     ok["index_w_invariant"] = bool(all(np.array_equal(x, y) for x, y in zip(iv + is_, iv1 + is1)))
+    # f3: RoPE-fused distributed index == the single-GPU fused call (lists, rotated slices)
+    fr = ops.rope_freqs(1e6, 32.0, 32768)
+    idx_r, q_r, k_r = ops.rope_vs_index(ql, kl, fr, a.p, a.p, comm=comm, seq_len=S, layout=lay)
+    idx_r1, q_r1, k_r1 = ops.rope_vs_index(t(q), t(k), fr, a.p, a.p)
+    rows_t = torch.from_numpy(rows).to(dev)
+    same_rot = torch.equal(q_r.view(torch.int16), q_r1[rows_t].view(torch.int16)) and \
+        torch.equal(k_r.view(torch.int16), k_r1[rows_t].view(torch.int16))
+    lr, lr1 = idx_r.to_lists(), idx_r1.to_lists()
+    ok["rope_index"] = bool(same_rot and all(np.array_equal(x, y) for x, y in zip(lr[0] + lr[1], lr1[0] + lr1[1])))
     # ring forward / backward
-    o, lse = ops.ring_attn_fwd(comm, S, ql, kl, vl, idx)
-    dq, dk, dv = ops.ring_attn_bwd(comm, S, ql, kl, vl, o, lse, dl, idx)
+    o, lse = ops.ring_attn_fwd(comm, S, ql, kl, vl, idx, layout=lay)
+    dq, dk, dv = ops.ring_attn_bwd(comm, S, ql, kl, vl, o, lse, dl, idx, layout=lay)
     torch.cuda.synchronize()
 
     # guarded re-run (compute-sanitizer substitute, as tests/test_gpu_guard.py): inputs and every workspace
@@ -73,8 +85,8 @@ def main():
     ring_ws_plain = comm.ring_ws
     comm.ring_ws = guarded(ring_ws_plain.numel())
     qg, kg, vg, dg = (gcopy(x) for x in (ql, kl, vl, dl))
-    og, lg = ops.ring_attn_fwd(comm, S, qg, kg, vg, idx)
-    dqg, dkg, dvg = ops.ring_attn_bwd(comm, S, qg, kg, vg, og, lg, dg, idx)
+    og, lg = ops.ring_attn_fwd(comm, S, qg, kg, vg, idx, layout=lay)
+    dqg, dkg, dvg = ops.ring_attn_bwd(comm, S, qg, kg, vg, og, lg, dg, idx, layout=lay)
     torch.cuda.synchronize()
     ops.workspace = ws_plain
     comm.ring_ws = ring_ws_plain
@@ -101,7 +113,7 @@ def main():
         def unstripe(parts, shape, lse_=False):
             out = np.zeros(shape)
             for r in range(W):
-                rr = ((j // 64) * W + r) * 64 + j % 64
+                rr = perm[r]
                 if lse_:
                     out[:, rr] = parts[r]
                 else:
@@ -116,7 +128,8 @@ def main():
                 "dv": nerr(unstripe(gv, ref[2].shape), ref[2])}
         ok["fwd"] = bool(errs["o"] <= 2e-2 and errs["lse"] <= 1e-3)
         ok["bwd"] = bool(max(errs["dq"], errs["dk"], errs["dv"]) <= 2e-2)
-        print(json.dumps({"world": W, "inner": a.inner or W, "copy_engine_ring": bool(ce_used), "ok": ok,
+        print(json.dumps({"world": W, "inner": a.inner or W, "layout": lay,
+                          "copy_engine_ring": bool(ce_used), "ok": ok,
                           "errs": {k_: float(v_) for k_, v_ in errs.items()}}), flush=True)
     flag = torch.tensor([1 if all(ok.values()) else 0], device=dev)
     dist.broadcast(flag, 0)

@@ -11,7 +11,7 @@ import torch
 from oracle import attention as OA
 from oracle import ring as OR
 from oracle import vsidx
-from oracle.sparseformat import stripe_perm
+from oracle.sparseformat import layout_perm
 from paper_2510_18830_b200 import ops
 from synth.generator import bf16_bits_to_f32, make_grad_out, make_qkv
 from tests.gpu_util import f64, normwise_err, random_index, to_dev_bf16
@@ -62,20 +62,22 @@ def test_bwd_random_index_many_bars_gqa(cuda_lib, S):
     _check(q, k, v, dO, iv, is_)
 
 
+@pytest.mark.parametrize("layout", ["striped", "zigzag"])
 @pytest.mark.parametrize("W", [2, 4, 8])
-def test_bwd_ring_steps_emulated(cuda_lib, W):
-    """Every (rank, step) of the backward ring on one GPU vs the oracle ring backward."""
+def test_bwd_ring_steps_emulated(cuda_lib, W, layout):
+    """Every (rank, step) of the backward ring on one GPU vs the oracle ring backward
+    (block-striped, and the zigzag layout of the f1 ablation)."""
     S, Hq, Hkv = 2048, 4, 2
     q, k, v = make_qkv(S, Hq, Hkv, seed=25, a=6.0)
     dO = make_grad_out(S, Hq, seed=25)
     iv, is_ = random_index(S, Hq, 26, n_off=6, n_col=80)
     qf, kf, vf, dOf = f64(q), f64(k), f64(v), f64(dO)
     O_ref, L_ref = OA.sparse_attention_forward(qf, kf, vf, iv, is_)
-    ref = OR.ring_backward(qf, kf, vf, O_ref, L_ref, dOf, iv, is_, W)
+    ref = OR.ring_backward(qf, kf, vf, O_ref, L_ref, dOf, iv, is_, W, layout=layout)
     idx = ops.VSIndex.from_lists(iv, is_, S)
     # forward on one GPU (global order), then stripe O/LSE to ranks
     o, lse = ops.sparse_attn_fwd(to_dev_bf16(q), to_dev_bf16(k), to_dev_bf16(v), idx)
-    perm = stripe_perm(S, W)
+    perm = layout_perm(S, W, layout)
     pt = [torch.from_numpy(perm[r]).cuda() for r in range(W)]
     Lq = S // W
     loc = lambda x, r: x[pt[r]].contiguous()
@@ -85,14 +87,15 @@ def test_bwd_ring_steps_emulated(cuda_lib, W):
     dk = [torch.zeros(Lq, Hkv, 128, dtype=torch.float32, device="cuda") for _ in range(W)]
     dv = [torch.zeros(Lq, Hkv, 128, dtype=torch.float32, device="cuda") for _ in range(W)]
     for r in range(W):
-        ops.attn_bwd_preprocess(S, W, loc(o, r), loc(dOd, r), D[r])
+        ops.attn_bwd_preprocess(S, W, loc(o, r), loc(dOd, r), D[r], layout=layout)
     sched = OR.schedule(W)
     for held in sched:
         for r in range(W):
             s = held[r]
             # the chunk's dK/dV accumulate directly at its owner (same sums as travelling)
             ops.attn_bwd_step(S, W, r, s, loc(qd, r), loc(kd, s), loc(vd, s), loc(dOd, r),
-                              lse[:, pt[r]].contiguous(), D[r], idx, dq[r], dk[s], dv[s])
+                              lse[:, pt[r]].contiguous(), D[r], idx, dq[r], dk[s], dv[s],
+                              layout=layout)
     torch.cuda.synchronize()
     out = [np.zeros((S, Hq, 128)), np.zeros((S, Hkv, 128)), np.zeros((S, Hkv, 128))]
     for r in range(W):

@@ -10,7 +10,7 @@ import torch
 from oracle import attention as OA
 from oracle import ring as OR
 from oracle import vsidx
-from oracle.sparseformat import stripe_perm
+from oracle.sparseformat import layout_perm
 from paper_2510_18830_b200 import ops
 from synth.generator import bf16_bits_to_f32, make_qkv
 from tests.gpu_util import f64, normwise_err, random_index, to_dev_bf16
@@ -65,15 +65,17 @@ def test_fwd_random_index_many_bars_gqa(cuda_lib, S):
     _check(q, k, v, iv, is_)
 
 
+@pytest.mark.parametrize("layout", ["striped", "zigzag"])
 @pytest.mark.parametrize("W", [2, 4, 8])
-def test_fwd_ring_steps_emulated(cuda_lib, W):
-    """Every (rank, step) of a W-rank striped ring on one GPU vs the oracle ring."""
+def test_fwd_ring_steps_emulated(cuda_lib, W, layout):
+    """Every (rank, step) of a W-rank ring on one GPU vs the oracle ring, in the method's
+    block-striped layout and in the zigzag layout of the f1 ablation."""
     S, Hq, Hkv = 2048, 4, 2
     q, k, v = make_qkv(S, Hq, Hkv, seed=6, a=6.0)
     iv, is_ = random_index(S, Hq, 7, n_off=6, n_col=80)
-    O_ref, L_ref, sched = OR.ring_forward(f64(q), f64(k), f64(v), iv, is_, W)
+    O_ref, L_ref, sched = OR.ring_forward(f64(q), f64(k), f64(v), iv, is_, W, layout=layout)
     idx = ops.VSIndex.from_lists(iv, is_, S)
-    perm = stripe_perm(S, W)
+    perm = layout_perm(S, W, layout)
     Lq = S // W
     qd = [to_dev_bf16(q[perm[r]]) for r in range(W)]
     kd = [to_dev_bf16(k[perm[r]]) for r in range(W)]
@@ -85,7 +87,7 @@ def test_fwd_ring_steps_emulated(cuda_lib, W):
         for r in range(W):
             s = held[r]
             ops.attn_fwd_step(S, W, r, s, t == 0, t == W - 1, qd[r], kd[s], vd[s], idx,
-                              o[r], oacc[r], lse[r])
+                              o[r], oacc[r], lse[r], layout=layout)
     torch.cuda.synchronize()
     Og = np.zeros((S, Hq, 128))
     Lg = np.zeros((Hq, S))

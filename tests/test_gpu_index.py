@@ -34,7 +34,7 @@ def test_column_scores_bitexact(cuda_lib, S, Hq, Hkv, seed):
 
 
 @pytest.mark.parametrize("S,Hq,Hkv,p", [(4096, 8, 1, 0.9), (4096, 8, 1, 0.97), (65536, 16, 2, 0.9),
-                                        (2048, 2, 1, 1.0)])
+                                        (2048, 2, 1, 1.0), (8192, 4, 1, 0.9), (8192, 2, 1, 0.5)])
 def test_index_lists_bitexact(cuda_lib, S, Hq, Hkv, p):
     q, k, _ = make_qkv(S, Hq, Hkv, seed=S + Hq)
     idx = ops.build_vs_index(to_dev_bf16(q), to_dev_bf16(k), p, p)
@@ -79,17 +79,21 @@ np.savez(out, *(list(iv) + list(is_)))
 """
 
 
-@pytest.mark.parametrize("S,Hq,Hkv", [(65536, 16, 2), (4096, 8, 1)])
-def test_index_sort_paths_agree(cuda_lib, tmp_path, S, Hq, Hkv):
-    """The one-sort path (head id in the key's top bits) and the per-head sorts
-    (forced by MT_VS_SORT_PER_HEAD=1, the layout used when the head bits do not fit)
-    give the same lists."""
+@pytest.mark.parametrize("S,Hq,Hkv,env", [
+    (65536, 16, 2, {"MT_VS_SORT_PER_HEAD": "1"}),
+    (4096, 8, 1, {"MT_VS_SORT_PER_HEAD": "1", "MT_VS_SELECT_SMALL": "0"}),
+    (8192, 4, 1, {"MT_VS_SELECT_SMALL": "0"})])
+def test_index_sort_paths_agree(cuda_lib, tmp_path, S, Hq, Hkv, env):
+    """The select paths give the same lists: the one-sort path (head id in the key's top
+    bits), the per-head sorts (forced by MT_VS_SORT_PER_HEAD=1, the layout used when the
+    head bits do not fit) and, for S <= 8192, the one-launch shared-memory select
+    (MT_VS_SELECT_SMALL=0 forces the radix-sort path there)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = str(tmp_path / "per_head.npz")
-    env = dict(os.environ, MT_VS_SORT_PER_HEAD="1", PYTHONPATH=root)
+    env = dict(os.environ, PYTHONPATH=root, **env)
     subprocess.run([sys.executable, "-c", _PER_HEAD_SCRIPT, str(S), str(Hq), str(Hkv), out],
                    check=True, env=env, cwd=root, timeout=600)
     ref = np.load(out)

@@ -1,4 +1,5 @@
-"""Real NCCL rings on 2 / 4 GPUs (flat and hierarchical 2x2) vs the oracle.
+"""Real NCCL rings on 2 / 4 GPUs (flat and hierarchical 2x2; block-striped, and the zigzag
+layout of the f1 ablation on flat rings) vs the oracle.
 
 Each case launches tests/dist_ring_worker.py under torchrun; it is skipped when
 the box has fewer GPUs than ranks (the single-GPU emulation of every ring step
@@ -16,13 +17,14 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("world,inner", [(2, 0), (4, 0), (4, 2)])
-def test_ring_torchrun(world, inner):
+@pytest.mark.parametrize("world,inner,layout", [(2, 0, "striped"), (4, 0, "striped"), (4, 2, "striped"),
+                                                (2, 0, "zigzag"), (4, 0, "zigzag")])
+def test_ring_torchrun(world, inner, layout):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={29500 + world * 10 + inner}",
-           str(ROOT / "tests" / "dist_ring_worker.py"), "--inner", str(inner)]
+           "--master-addr=127.0.0.1", f"--master-port={29500 + world * 10 + inner + (5 if layout == 'zigzag' else 0)}",
+           str(ROOT / "tests" / "dist_ring_worker.py"), "--inner", str(inner), "--layout", layout]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     sys.stdout.write(r.stdout[-4000:])
     assert r.returncode == 0, r.stderr[-4000:]
