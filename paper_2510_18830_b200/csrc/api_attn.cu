@@ -135,7 +135,8 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
                         const float* D, float* dq, float* dk, float* dv, int num_sms,
                         cudaStream_t st);
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
-                              cudaStream_t st);
+                              cudaStream_t st, float* zq = nullptr, float* zk = nullptr,
+                              float* zv = nullptr, int Hkv = 0);
 mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st);
 mt_status f32_to_bf16_x3(const float* x0, void* y0, int64_t n0, const float* x1, void* y1,
                          int64_t n1, const float* x2, void* y2, int64_t n2, cudaStream_t st);
@@ -200,10 +201,8 @@ extern "C" mt_status mt_sparse_attn_bwd(const mt_shape* sh, const void* q, const
   VSPlan plan;
   MT_TRY(vs_plan_build(&plan, S, Hq, Hkv, 1, 0, idx->v_cnt, idx->v_idx, idx->v_stride, idx->s_cnt,
                        idx->s_off, (int)idx->s_stride, w.plan, stream));
-  MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream));
-  // dq, dk, dv are adjacent in the workspace (carve_bwd): one memset clears all three
-  cudaMemsetAsync(w.dq, 0, (size_t)((const char*)(w.dv + S * Hkv * 128) - (const char*)w.dq),
-                  stream);
+  // D, and the fp32 dQ / dK / dV accumulators zeroed in the same pass
+  MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream, w.dq, w.dk, w.dv, Hkv));
   MT_TRY(attn_bwd_step(plan, 0, 0, (int)(S / 64), q, k, v, dO, lse, w.D, w.dq, w.dk, w.dv,
                        device_num_sms(), stream));
   return f32_to_bf16_x3(w.dq, dq, S * Hq * 128, w.dk, dk, S * Hkv * 128, w.dv, dv, S * Hkv * 128,

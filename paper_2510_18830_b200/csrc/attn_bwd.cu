@@ -209,6 +209,7 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile, int nbar)
 }
 
 // ------------------------------------------------------------------ producer
+template <int L>  // sequence layout (plan.cuh), fixed per launch
 __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
                          const CUtensorMap* tmdo, const CUtensorMap* tmk,
                          const CUtensorMap* tmv) {
@@ -304,7 +305,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         int m = sm.cols[row];
         if (m < 0) m = m0;  // padding rows duplicate a live row (masked later)
         const int blk = m >> 6;
-        const int64_t lrow = (int64_t)plan_g2l(pl, blk) * 64 + (m & 63);
+        const int64_t lrow = (int64_t)g2l_<L>(pl, blk) * 64 + (m & 63);
         const size_t goff = ((size_t)lrow * pl.Hkv + T.g) * 128 + c16 * 8;
         const uint32_t doff = (c16 >> 3) * 16384 + sw128(row, c16 & 7);
         cp_async_16(kb + doff, P.k + goff);
@@ -318,7 +319,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     // ---- chunk stream
     if (T.mode == kModeBlock) {
       const bool v1 = T.lb0 + 1 < P.nloc;
-      const int kb0 = plan_l2g(pl, P.s, T.lb0);  // global key block of slot 0
+      const int kb0 = l2g_<L>(pl, P.s, T.lb0);  // global key block of slot 0
       if (pl.tptr) {
         // block-CSR mode (W = 1): the pair's sorted (gq << 1 | slot) entries; a query
         // block attending both slots has two adjacent entries, emitted once (at the
@@ -355,15 +356,15 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         // selected offset, slot 1 (key block kb1) iff gq - kb1 is.  32 query blocks per
         // ballot from the slash bitmap: a scalar walk of the offset list costs a dependent
         // global load per offset and skips (W-1)/W of them.
-        const int kb1 = v1 ? plan_l2g(pl, P.s, T.lb0 + 1) : -1;
-        const int jfirst = plan_count_le(pl, P.r, kb0 - 1);
+        const int kb1 = v1 ? l2g_<L>(pl, P.s, T.lb0 + 1) : -1;
+        const int jfirst = count_le_<L>(pl, P.r, kb0 - 1);
         for (int h = T.h; h < T.h + P.hpt; ++h) {  // the tile's q heads one after another
         const uint32_t* bits = pl.s_bits + (int64_t)h * pl.bits_words;
         auto has = [&](int x) { return x >= 0 && ((bits[x >> 5] >> (x & 31)) & 1u) != 0u; };
         for (int j0 = jfirst; j0 < P.nloc; j0 += 32) {
           const int j = j0 + lane;
           const bool in = j < P.nloc;
-          const int gq = plan_l2g(pl, P.r, j);
+          const int gq = l2g_<L>(pl, P.r, j);
           const bool a = in && has(gq - kb0);
           const bool b = in && v1 && has(gq - kb1);
           const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b);
@@ -371,7 +372,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
           while (bal) {
             const int l = __ffs(bal) - 1;
             bal &= bal - 1;
-            const int gl = __shfl_sync(0xffffffffu, gq, l);
+            const int gl = l2g_<L>(pl, P.r, j0 + l);
             uint32_t flags = 0;
             if ((ba >> l) & 1u) flags |= gl == kb0 ? 5u : 1u;  // slot 0 live (+ diagonal)
             if ((bb >> l) & 1u) flags |= gl == kb1 ? 10u : 2u;  // slot 1 live (+ diagonal)
@@ -384,7 +385,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     } else {
       const int bfirst = sm.cols[0] >> 6;
       // first rank-local query block with global block > bfirst
-      const int j0 = plan_count_le(pl, P.r, bfirst);
+      const int j0 = count_le_<L>(pl, P.r, bfirst);
       // walk this part's query blocks from the last one down: the resident bar tiles
       // of a head start together and share each Q/dO/dQ block while it is in L2
       for (int j = T.j_hi - 1; j >= max(j0, T.j_lo); --j) emit(T.h, j, 0u);
@@ -872,8 +873,13 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         tmem_ld32(tmem + lb + col + c0, a);
         tmem_ld_wait();
         if (!live_row) continue;
+        if (P.dbg & 32) {  // A/B: scalar reductions (round 1)
 #pragma unroll
-        for (int c = 0; c < 32; c += 4) red_add_f32x4(dst + c0 + c, a + c);
+          for (int c = 0; c < 32; ++c) red_add_f32(dst + c0 + c, __uint_as_float(a[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) red_add_f32x4(dst + c0 + c, a + c);
+        }
       }
     }
     tc_fence_before();
@@ -926,7 +932,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
     if (warp == 0) {
-      producer(sm, P, &tmq, &tmdo, &tmk, &tmv);
+      if (P.plan.layout)
+        producer<1>(sm, P, &tmq, &tmdo, &tmk, &tmv);
+      else
+        producer<0>(sm, P, &tmq, &tmdo, &tmk, &tmv);
     } else if (warp == 1) {
       mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
     }
@@ -953,11 +962,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // D_n = dO_n . O_n (Eq. 1's sum_j dL/dA_ij A_ij), one warp per (token, head) row.
+// D = rowsum(dO o O) per (token, q head), one warp per row.  zq / zk / zv (optional):
+// fp32 accumulators zeroed on the way, [rows][128] for dQ and [S_loc][Hkv][128] for dK / dV
+// (the single-GPU backward: saves the memset pass and its launch)
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* o, const __nv_bfloat16* dO, float* D,
-                                      int64_t rows, int Hq, int64_t S_loc) {
+                                      int64_t rows, int Hq, int64_t S_loc, float* zq, float* zk,
+                                      float* zv, int Hkv) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= rows) return;
+  if (zq) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4*>(zq + w * 128)[lane] = z;
+    const int h = (int)(w % Hq);
+    if (h < Hkv) {
+      const int64_t kr = (w / Hq) * Hkv + h;
+      reinterpret_cast<float4*>(zk + kr * 128)[lane] = z;
+      reinterpret_cast<float4*>(zv + kr * 128)[lane] = z;
+    }
+  }
   const uint2 a = reinterpret_cast<const uint2*>(o + w * 128)[lane];
   const uint2 b = reinterpret_cast<const uint2*>(dO + w * 128)[lane];
   const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
@@ -1008,13 +1031,13 @@ static_assert(sizeof(bwd::Smem) <= 232448, "backward SMEM exceeds 227 KB");
 size_t bwd_smem_bytes() { return sizeof(bwd::Smem); }  // the dynamic base is 1024-aligned
 
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
-                              cudaStream_t st) {
+                              cudaStream_t st, float* zq, float* zk, float* zv, int Hkv) {
   const int64_t rows = S_loc * Hq;
   const int threads = 256;
   const int64_t blocks = (rows * 32 + threads - 1) / threads;
   bwd::bwd_preprocess_kernel<<<(unsigned)blocks, threads, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dO), D, rows, Hq,
-      S_loc);
+      S_loc, zq, zk, zv, Hkv);
   return check_launch("bwd_preprocess");
 }
 
@@ -1119,6 +1142,22 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   // MT_BWD_BAR_FIRST=0/1 overrides.
   static const int bar_first_env = getenv("MT_BWD_BAR_FIRST") ? atoi(getenv("MT_BWD_BAR_FIRST")) : -1;
   P.bar_first = bar_first_env >= 0 ? bar_first_env : (nloc <= 2048 ? 1 : 0);
+  static const int split_env = getenv("MT_BWD_SPLIT") ? atoi(getenv("MT_BWD_SPLIT")) : 0;
+  if (split_env && P.n_bar > 0) {  // A/B: BLOCK and BAR tiles as two launches (round 1)
+    Params Pb = P, Pv = P;
+    Pb.n_bar = 0;
+    Pb.n_tiles = P.n_block;
+    Pv.n_block = 0;
+    Pv.n_tiles = P.n_bar;
+    Pv.tile_counter = plan.scratch + 3;
+    cudaMemsetAsync(Pv.tile_counter, 0, sizeof(int), st);
+    const int gb = Pb.n_tiles < num_sms ? Pb.n_tiles : num_sms;
+    if (gb > 0)
+      attn_bwd_kernel<<<gb, kThreads, smem, st>>>(Pb, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+    MT_TRY(check_launch("attn_bwd_kernel(block)"));
+    attn_bwd_kernel<<<num_sms, kThreads, smem, st>>>(Pv, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+    return check_launch("attn_bwd_kernel(bar)");
+  }
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   if (grid > 0)
     attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);

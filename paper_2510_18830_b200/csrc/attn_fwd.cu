@@ -134,6 +134,7 @@ struct Params {
   float* o_acc;
   float* lse;
   int* fix_count;  // tiles flagged for the exact fix-up pass
+  int stabfix;     // 1: chunk-0 fallback stabiliser + underflow check (MT_FWD_STABFIX=0: off, A/B)
   int* fix_list;
   int* tile_counter;  // dynamic tile scheduler (zeroed before the launch)
   int order;          // tile order (MT_FWD_ORDER): 1 head-major (default; L2 reuse of K/V), 0 query-block-major
@@ -192,6 +193,7 @@ __device__ __forceinline__ void tile_coords(const Params& P, int tile, int& h0, 
 // metadata, so a late V slot never delays the next K.  K slots (and the per-chunk meta
 // the MMA reads) are indexed by every chunk including END markers; V slots only by
 // data chunks.
+template <int L>  // sequence layout (plan.cuh), fixed per launch
 __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
                            const CUtensorMap* tmk, const CUtensorMap* tmkp) {
   const int lane = lane_id();
@@ -223,7 +225,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     if (tile >= P.n_tiles) break;
     int h0, h1, j;
     tile_coords(P, tile, h0, h1, j);
-    const int g = plan_l2g(pl, P.r, j);  // global query block (plan.cuh layouts)
+    const int g = l2g_<L>(pl, P.r, j);  // global query block (plan.cuh layouts)
     const int gkv = h0 / grp;
     if (!first_tile) {
       mbar_wait(smem_u32(&sm.qempty), qe_phase);
@@ -259,8 +261,8 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
     {
       // live0 / live1: per slot, bit x = head x of the pair attends that key block
       auto emit_pair = [&](int o0, int o1, uint32_t live0, uint32_t live1) {  // o1 < 0: slot empty
-        const int lb0 = plan_g2l(pl, g - o0);
-        const int lb1 = o1 >= 0 ? plan_g2l(pl, g - o1) : lb0;
+        const int lb0 = g2l_<L>(pl, g - o0);
+        const int lb1 = o1 >= 0 ? g2l_<L>(pl, g - o1) : lb0;
         uint32_t flags = live0 & 3u;
         if (o1 >= 0) flags |= (live1 & 3u) << 2;
         if (o0 == 0) flags |= 16u;
@@ -315,8 +317,11 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
       // the origin's key blocks <= g, nearest first: point m is local key block
       // npts-1-m, offset o(m) = g - l2g(s, npts-1-m) ascending (block-striped: the lattice
       // o = t + mW); tested 32 at a time against both bitmaps
-      const int npts = pl.bptr ? 0 : plan_count_le(pl, P.s, g);
-      auto o_of = [&](int m) { return g - plan_l2g(pl, P.s, npts - 1 - m); };
+      const int npts = pl.bptr ? 0 : count_le_<L>(pl, P.s, g);
+      auto o_of = [&](int m) {
+        if constexpr (L == 0) return P.t + m * W;  // the residue lattice
+        else return g - l2g_<L>(pl, P.s, npts - 1 - m);
+      };
       int f0 = -1, f1 = -1;  // each head's first offset
       for (int m0 = 0; m0 < npts && (f0 < 0 || (h1 >= 0 && f1 < 0)); m0 += 32) {
         const int o = o_of(m0 + lane);
@@ -340,7 +345,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         while (bal) {
           const int l = __ffs(bal) - 1;
           bal &= bal - 1;
-          const int ov = __shfl_sync(0xffffffffu, o, l);
+          const int ov = o_of(m0 + l);
           if (pending < 0) {
             pending = ov;
           } else {
@@ -451,7 +456,7 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
             if (blk < g) {
               more = true;
               keep = !covered(g - blk);
-              lrow = plan_g2l(pl, blk) * 64 + (m & 63);
+              lrow = g2l_<L>(pl, blk) * 64 + (m & 63);
             }
           }
           const uint32_t bal = __ballot_sync(0xffffffffu, keep);
@@ -792,7 +797,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
           // a row with no live key in chunk 0 (ring steps: its head has no slash block of
           // this origin, only bars) takes the chunk's largest score against the same kv
           // head's keys as its scale; the overflow / underflow checks keep it exact
-          if (mx == -INFINITY) mx = mx_all;
+          if (mx == -INFINITY && P.stabfix) mx = mx_all;
           sm.m[row] = mx;
           m = mx;
           mbar_arrive(mready);
@@ -885,7 +890,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
     named_bar_sync(3, kSoftmax);
     {  // underflow: the row has live keys but all of them sit far below the stabiliser
       const float e = fmaxf(sm.emx[0][row], sm.emx[1][row]);
-      if (e > -INFINITY && e < kUnderflow) sm.ovf[ntile & 1] = 1;
+      if (P.stabfix && e > -INFINITY && e < kUnderflow) sm.ovf[ntile & 1] = 1;
     }
     named_bar_sync(3, kSoftmax);
     if (row == 0) MT_CRUMB(5 + wg, 7000000 + (int)ntile);
@@ -1014,7 +1019,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
     if (warp == 0) {
-      producer_k(sm, P, &tmq, &tmk, &tmkp);
+      if (P.plan.layout)
+        producer_k<1>(sm, P, &tmq, &tmk, &tmkp);
+      else
+        producer_k<0>(sm, P, &tmq, &tmk, &tmkp);
     } else if (warp == 2) {
       producer_v(sm, P, &tmv, &tmvp);
     } else if (warp == 1) {
@@ -1195,6 +1203,8 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   static const int ord = getenv("MT_FWD_ORDER") ? atoi(getenv("MT_FWD_ORDER")) : 1;
   P.order = ord;
   P.fix_list = plan.scratch + 16;
+  static const int stabfix = getenv("MT_FWD_STABFIX") ? atoi(getenv("MT_FWD_STABFIX")) : 1;
+  P.stabfix = stabfix;
   static const int pack = getenv("MT_FWD_PACK") ? atoi(getenv("MT_FWD_PACK")) : 1;
   P.packed = pack && plan.kp && plan.pcap > 0;
   const uint64_t S_loc = (uint64_t)nloc * 64;

@@ -27,7 +27,8 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
                         const float* D, float* dq, float* dk, float* dv, int num_sms,
                         cudaStream_t st);
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
-                              cudaStream_t st);
+                              cudaStream_t st, float* zq = nullptr, float* zk = nullptr,
+                              float* zv = nullptr, int Hkv = 0);
 mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st);
 mt_status f32_to_bf16_x3(const float* x0, void* y0, int64_t n0, const float* x1, void* y1,
                          int64_t n1, const float* x2, void* y2, int64_t n2, cudaStream_t st);
@@ -233,10 +234,7 @@ extern "C" mt_status mt_block_sparse_attn_bwd(const mt_shape* sh, const void* q,
   pl.tptr = w.off;
   pl.tidx = w.tsorted;
 
-  MT_TRY(attn_bwd_preprocess(o, dO, D, S, Hq, st));
-  cudaMemsetAsync(dq32, 0, (size_t)S * Hq * 128 * 4, st);
-  cudaMemsetAsync(dk32, 0, (size_t)S * Hkv * 128 * 4, st);
-  cudaMemsetAsync(dv32, 0, (size_t)S * Hkv * 128 * 4, st);
+  MT_TRY(attn_bwd_preprocess(o, dO, D, S, Hq, st, dq32, dk32, dv32, Hkv));  // + zeroed accumulators
   MT_TRY(attn_bwd_step(pl, 0, 0, (int)nb, q, k, v, dO, lse, D, dq32, dk32, dv32,
                        device_num_sms(), st));
   return f32_to_bf16_x3(dq32, dq, S * Hq * 128, dk32, dk, S * Hkv * 128, dv32, dv, S * Hkv * 128,

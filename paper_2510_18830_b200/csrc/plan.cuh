@@ -94,5 +94,15 @@ __host__ __device__ __forceinline__ int plan_g2l(const VSPlan& p, int gb) {
 __host__ __device__ __forceinline__ int plan_count_le(const VSPlan& p, int r, int g) {
   return layout_count_le(p.layout, p.W, p.zc, r, g);
 }
+// the same with the layout fixed at compile time (the kernels' producers are instantiated
+// per layout: the striped walk then compiles to round 1's lattice arithmetic)
+template <int L>
+__device__ __forceinline__ int l2g_(const VSPlan& p, int r, int lb) { return layout_l2g(L, p.W, p.zc, r, lb); }
+template <int L>
+__device__ __forceinline__ int g2l_(const VSPlan& p, int gb) { return layout_g2l(L, p.W, p.zc, gb); }
+template <int L>
+__device__ __forceinline__ int count_le_(const VSPlan& p, int r, int g) {
+  return layout_count_le(L, p.W, p.zc, r, g);
+}
 
 }  // namespace mt

@@ -36,7 +36,8 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
                         const float* D, float* dq, float* dk, float* dv, int num_sms,
                         cudaStream_t st);
 mt_status attn_bwd_preprocess(const void* o, const void* dO, float* D, int64_t S_loc, int Hq,
-                              cudaStream_t st);
+                              cudaStream_t st, float* zq = nullptr, float* zk = nullptr,
+                              float* zv = nullptr, int Hkv = 0);
 mt_status f32_to_bf16(const float* x, void* y, int64_t n, cudaStream_t st);
 mt_status f32_to_bf16_x3(const float* x0, void* y0, int64_t n0, const float* x1, void* y1,
                          int64_t n1, const float* x2, void* y2, int64_t n2, cudaStream_t st);

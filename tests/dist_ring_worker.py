@@ -58,6 +58,22 @@ def main():
         torch.equal(k_r.view(torch.int16), k_r1[rows_t].view(torch.int16))
     lr, lr1 = idx_r.to_lists(), idx_r1.to_lists()
     ok["rope_index"] = bool(same_rot and all(np.array_equal(x, y) for x, y in zip(lr[0] + lr[1], lr1[0] + lr1[1])))
+    # f4 slow-link emulation (MT_EMU_INTER_GBPS / MT_EMU_NODE, comm.cu): every receive from a
+    # rank of another emulated node is held back by bytes / bandwidth; check the profiled
+    # transfer times of a forward honour that bound (and, below, that results stay exact)
+    emu = float(os.environ.get("MT_EMU_INTER_GBPS", "0") or 0)
+    if emu > 0:
+        comm.profile(True)
+        ops.ring_attn_fwd(comm, S, ql, kl, vl, idx, layout=lay)
+        torch.cuda.synchronize()
+        tt = comm.step_times(False)  # [(compute, inner, outer, dkv) ms]
+        comm.profile(False)
+        kv_bytes = 2 * (S // W) * Hkv * 128 * 2
+        floor_ms = kv_bytes / (emu * 1e9) * 1e3
+        node = int(os.environ.get("MT_EMU_NODE", str(a.inner or W)))
+        cross = [x for st in tt for x in st[1:3] if x >= 0]
+        # some transfer of this rank crosses an emulated node boundary when W > node
+        ok["emu_delay"] = bool(W <= node or max(cross, default=0.0) >= 0.9 * floor_ms)
     # ring forward / backward
     o, lse = ops.ring_attn_fwd(comm, S, ql, kl, vl, idx, layout=lay)
     dq, dk, dv = ops.ring_attn_bwd(comm, S, ql, kl, vl, o, lse, dl, idx, layout=lay)

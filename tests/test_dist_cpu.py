@@ -1,5 +1,5 @@
 """Multi-process host logic on CPU (gloo, world size 2): schedule agreement,
-unique-id style broadcast, block striping / un-striping round trip."""
+unique-id style broadcast, block striping / un-striping round trip, zigzag row map."""
 import os
 import socket
 
@@ -42,7 +42,17 @@ def _worker(rank, world, port, out):
     for r in range(world):
         rr = torch.from_numpy(((j // 64) * world + r) * 64 + j % 64)
         y[rr] = parts[r]
-    out[rank] = int(same and ids[0] == bytes(range(128)) and torch.equal(x, y))
+    # 4. the zigzag layout's host row map (bench.zigzag_rows, the rows each rank feeds the
+    # kernels) round-trips the same way and equals the oracle's permutation
+    import bench
+    from oracle.sparseformat import zigzag_perm
+    zr = [torch.from_numpy(bench.zigzag_rows(S, world, r)) for r in range(world)]
+    dist.all_gather(parts, x[zr[rank]].contiguous())
+    z = torch.empty(S)
+    for r in range(world):
+        z[zr[r]] = parts[r]
+    zz_ok = torch.equal(x, z) and all(np.array_equal(zr[r].numpy(), zigzag_perm(S, world)[r]) for r in range(world))
+    out[rank] = int(same and ids[0] == bytes(range(128)) and torch.equal(x, y) and zz_ok)
     dist.destroy_process_group()
 
 
@@ -56,3 +66,12 @@ def test_gloo_world2_host_logic():
 def test_library_schedule_matches_oracle():
     for W, G in [(1, None), (2, None), (4, None), (4, 2), (8, 4), (8, 2), (6, 3)]:
         assert ops.ring_schedule(W, G) == OR.schedule(W, G)
+
+
+def test_bench_layout_rows_match_oracle():
+    import bench
+    from oracle.sparseformat import layout_perm
+    for S, W in ((4096, 1), (4096, 2), (8192, 4), (131072, 8)):
+        for r in range(W):
+            assert np.array_equal(bench.stripe_rows(S, W, r), layout_perm(S, W, "striped")[r])
+            assert np.array_equal(bench.zigzag_rows(S, W, r), layout_perm(S, W, "zigzag")[r])

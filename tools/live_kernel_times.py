@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--xattn", type=float, default=0.0,
+                    help="profile the XAttention index (threshold) instead of the VS step")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -39,6 +41,9 @@ def main():
     flush = torch.empty(4 * 126 * 2 ** 20, dtype=torch.uint8, device=dev)
 
     def step():
+        if a.xattn > 0:
+            ops.xattn_index(qd, kd, a.xattn)
+            return
         idx = ops.build_vs_index(qd, kd, a.p, a.p)
         o, lse = ops.sparse_attn_fwd(qd, kd, vd, idx)
         ops.sparse_attn_bwd(qd, kd, vd, o, lse, dd, idx)
