@@ -361,6 +361,28 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
         for (int h = T.h; h < T.h + P.hpt; ++h) {  // the tile's q heads one after another
         const uint32_t* bits = pl.s_bits + (int64_t)h * pl.bits_words;
         auto has = [&](int x) { return x >= 0 && ((bits[x >> 5] >> (x & 31)) & 1u) != 0u; };
+        if constexpr (L == 0) {
+          // block-striped: gq = kb0 + x on the lattice x = t + mW, slot 1 = kb0 + W
+          // (measured: the generic walk below costs the striped backward ~9 ms at 512K)
+          const int xmax = pl.nb - kb0;  // gq < nb
+          for (int m0 = 0; P.t + m0 * W < xmax; m0 += 32) {
+            const int x = P.t + (m0 + lane) * W;
+            const bool in = x < xmax;
+            const bool a = in && has(x);
+            const bool b = in && v1 && has(x - W);
+            const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b);
+            uint32_t bal = ba | bb;
+            while (bal) {
+              const int l = __ffs(bal) - 1;
+              bal &= bal - 1;
+              const int xs = P.t + (m0 + l) * W;
+              uint32_t flags = 0;
+              if ((ba >> l) & 1u) flags |= xs == 0 ? 5u : 1u;  // slot 0 live (+ diagonal)
+              if ((bb >> l) & 1u) flags |= xs == W ? 10u : 2u;  // slot 1 live (+ diagonal)
+              emit(h, (kb0 + xs - P.r) / W, flags);
+            }
+          }
+        } else {
         for (int j0 = jfirst; j0 < P.nloc; j0 += 32) {
           const int j = j0 + lane;
           const bool in = j < P.nloc;
@@ -378,6 +400,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
             if ((bb >> l) & 1u) flags |= gl == kb1 ? 10u : 2u;  // slot 1 live (+ diagonal)
             emit(h, j0 + l, flags);
           }
+        }
         }
         }
       }
@@ -454,7 +477,10 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     MT_CRUMB(0, 2);
     mbar_wait(smem_u32(&sm.kvfull), ntile & 1);
     ++ntile;
-    fence_proxy_async_smem();  // BAR tiles: K/V rows arrived by cp.async (generic proxy)
+    {  // BAR tiles: K/V rows arrived by cp.async (generic proxy)
+      const ChunkMeta& m0 = sm.meta[c % kStages];  // the tile's first event (waited above)
+      if (m0.kind == kChunk && m0.mode == kModeBar) fence_proxy_async_smem();
+    }
     tc_fence_after();
     // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and its
     // warpgroup's TMEM region is drained; the gradient MMAs of chunk g as soon as its

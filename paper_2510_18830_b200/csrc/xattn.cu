@@ -4,15 +4,18 @@
 // Per q head h (kv head h / (Hq/Hkv)), block B = 128, stride st = 16, n = S / st:
 //   1. Qr[i] = (q[i st + st-1], ..., q[i st]), Kr[j] = (k[j st], ..., k[j st + st-1])
 //      (2048-wide rows; reshape kernels), so A = Qr Kr^T / (st sqrt d) sums each
-//      st x st sub-block's antidiagonal — a plain bf16 GEMM with fp32 output (cuBLAS),
-//      row chunks of R, columns bounded by the chunk's causal limit;
-//   2.-3. one CTA per 128-block row I: row softmax over j <= i (online max/sum), then
-//      the 8 x 8 block sums Bs[I][J], J <= I (lower triangle, fp32);
+//      st x st sub-block's antidiagonal;
+//   2.-3. row softmax over j <= i, then the 8 x 8 block sums Bs[I][J], J <= I (lower
+//      triangle, fp32).  Default: one hand-written tcgen05 kernel does 1.-3. without
+//      materialising A (xattn_score.cu).  MT_XATTN_CUBLAS=1: round 1's path, A by a cuBLAS
+//      bf16 GEMM in row chunks of R (columns bounded causally), then one CTA per 128-block
+//      row for the online max/sum and the block sums;
 //   4. all heads at once: stable segmented sort of each row descending (ties keep the
 //      smaller J first), one warp per row keeps J while the sum before it is
 //      < tau * row total; the diagonal is always kept (bitmap [Hq][nI][nI/32]);
 //   5. 64-token CSR: count, scan, fill (query blocks 2I, 2I+1; key blocks 2J, 2J+1,
 //      the diagonal's causal half).
+#include <cstdlib>
 #include <mutex>
 #include <cublas_v2.h>
 
@@ -25,6 +28,11 @@ namespace mt {
 
 mt_status check_shape(const mt_shape* sh, int W);
 mt_status check_device();
+int device_num_sms();
+size_t xattn_score_scratch_bytes(int64_t n, int nI, int num_sms);
+mt_status xattn_scores_tc(const void* qr, const void* kr, int64_t n, int nI, int hb, int h0,
+                          int Hkv, int grp, float scale_log2, float* tri, int64_t T,
+                          void* scratch, int num_sms, cudaStream_t st);
 
 namespace {
 
@@ -237,8 +245,24 @@ struct XWs {
   size_t cub_bytes;
   void* gemm_ws;   // cuBLAS workspace (cublasSetWorkspace): no allocation inside the GEMM
   int64_t R;  // stride rows per GEMM chunk
+  // hand-written path (xattn_score.cu): q heads reshaped hb at a time, every kv head's K
+  __nv_bfloat16 *qrb, *krall;
+  void* xsc;  // per-CTA P / Mt scratch
+  int hb;
   size_t total;
 };
+
+// q heads per fused-score launch: enough (head, row tile) items for ~8 per SM
+inline int xattn_hb(int64_t n, int Hq) {
+  const int nrt = (int)((n + 127) / 128);
+  int hb = (8 * 148 + nrt - 1) / nrt;
+  return hb < 1 ? 1 : (hb > Hq ? Hq : hb);
+}
+// MT_XATTN_CUBLAS=1: round 1's cuBLAS GEMM + softmax pass (A/B)
+inline bool xattn_use_cublas() {
+  static const bool v = getenv("MT_XATTN_CUBLAS") && atoi(getenv("MT_XATTN_CUBLAS"));
+  return v;
+}
 
 XWs carve(void* base, const mt_shape* sh) {
   const int64_t S = sh->seq_len, n = S / kSt, nI = S / kB, nb = S / 64;
@@ -277,6 +301,10 @@ XWs carve(void* base, const mt_shape* sh) {
   w.cub_bytes = a > b ? a : b;
   w.cub_tmp = take(w.cub_bytes);
   w.gemm_ws = take(kGemmWs);
+  w.hb = xattn_hb(n, Hq);
+  w.qrb = (__nv_bfloat16*)take((size_t)w.hb * n * kWide * 2);
+  w.krall = (__nv_bfloat16*)take((size_t)sh->n_kv_heads * n * kWide * 2);
+  w.xsc = take(xattn_score_scratch_bytes(n, (int)nI, 148));
   w.total = o;
   return w;
 }
@@ -335,14 +363,36 @@ extern "C" mt_status mt_xattn_index_count(const mt_shape* sh, const mt_xattn_par
   const int64_t S = sh->seq_len, n = S / kSt, nI = S / kB, nb = S / 64;
   const int Hq = sh->n_q_heads, Hkv = sh->n_kv_heads, grp = Hq / Hkv;
   const int64_t T = nI * (nI + 1) / 2;
-  cublasHandle_t hb = handle();
-  if (!hb) return fail(MT_ECUDA, "cublasCreate failed");
-  if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS ||
-      cublasSetWorkspace(hb, w.gemm_ws, kGemmWs) != CUBLAS_STATUS_SUCCESS)
-    return fail(MT_ECUDA, "cublasSetStream/SetWorkspace failed");
+  cublasHandle_t hb = nullptr;
+  if (xattn_use_cublas()) {
+    hb = handle();
+    if (!hb) return fail(MT_ECUDA, "cublasCreate failed");
+    if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS ||
+        cublasSetWorkspace(hb, w.gemm_ws, kGemmWs) != CUBLAS_STATUS_SUCCESS)
+      return fail(MT_ECUDA, "cublasSetStream/SetWorkspace failed");
+  }
   const float alpha = 1.f / (kSt * sqrtf((float)kD)), beta = 0.f;
   const int rgrid = 148 * 8;
-  for (int h = 0; h < Hq; ++h) {
+  if (!xattn_use_cublas()) {
+    // hand-written tcgen05 scores with the softmax / block sums fused (xattn_score.cu)
+    const int sms = device_num_sms() < 148 ? device_num_sms() : 148;
+    for (int g = 0; g < Hkv; ++g) {
+      reshape_kernel<<<rgrid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(k),
+                                           w.krall + (size_t)g * n * kWide, n, Hkv, g, 0);
+      MT_TRY(check_launch("xattn reshape k"));
+    }
+    for (int h0 = 0; h0 < Hq; h0 += w.hb) {
+      const int hb = Hq - h0 < w.hb ? Hq - h0 : w.hb;
+      for (int hh = 0; hh < hb; ++hh) {
+        reshape_kernel<<<rgrid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                             w.qrb + (size_t)hh * n * kWide, n, Hq, h0 + hh, 1);
+        MT_TRY(check_launch("xattn reshape q"));
+      }
+      MT_TRY(xattn_scores_tc(w.qrb, w.krall, n, (int)nI, hb, h0, Hkv, grp,
+                             alpha * 1.4426950408889634f, w.tri, T, w.xsc, sms, st));
+    }
+  }
+  for (int h = 0; h < Hq && xattn_use_cublas(); ++h) {
     if (h % grp == 0) {
       reshape_kernel<<<rgrid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(k), w.kr, n, Hkv,
                                            h / grp, 0);

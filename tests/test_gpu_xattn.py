@@ -9,7 +9,8 @@ SURVEY §8(f) f2) vs the fp64 oracle (oracle/xattn.py).
   threshold mass reached, greedy order, minimality;
 * the 64-token CSR equals the expansion (step 5) of the GPU's own kept sets, bit
   for bit, and drives the block-sparse attention to finite outputs;
-* at 512K (the bench shape, 4 score-GEMM chunks), sampled rows of every head.
+* 2944 tokens: a partial last 128-row tile of the fused score kernel (xattn_score.cu);
+* at 512K (the bench shape; head batches of the fused kernel), sampled rows of four heads.
 """
 import numpy as np
 import pytest
@@ -49,7 +50,7 @@ def _tri_row(scores_h, I):
     return scores_h[b: b + I + 1]
 
 
-@pytest.mark.parametrize("S,Hq,Hkv,a", [(4096, 4, 2, 6.0), (2048, 2, 1, 16.0)])
+@pytest.mark.parametrize("S,Hq,Hkv,a", [(4096, 4, 2, 6.0), (2048, 2, 1, 16.0), (2944, 3, 1, 6.0)])
 def test_xattn_index_matches_oracle(cuda_lib, S, Hq, Hkv, a):
     q, k, v = make_qkv(S, Hq, Hkv, seed=S + 3, a=a)
     qd, kd = to_dev_bf16(q), to_dev_bf16(k)
