@@ -6,11 +6,13 @@
 // Per q head h (kv head h / grp), stride st = 16, n = S / 16 stride rows:
 //   A[i][j] = Qr[i] . Kr[j] / (st sqrt d)   (Qr, Kr: 2048-wide reshaped rows, xattn.cu)
 //   Bs[I][J] = sum_{i in I, j in J} softmax_{j <= i}(A[i][.])_j      (I, J: 8 stride rows)
-// Tiles: 128 stride rows (16 query blocks) x 128 stride columns, K = 2048 streamed by TMA
-// in 64-wide chunks (SW128, 16 KB per operand per chunk) through a 6-stage ring; the
-// accumulator is double-buffered in TMEM (2 x 128 columns).  A CTA walks one row tile's
-// column tiles C = 0 .. R in order, and its 4 epilogue warps (thread = stride row = TMEM
-// lane) keep the running max / sum of their row (online softmax, log2 domain) and write
+// Tiles: 128 stride rows (16 query blocks) x 256 stride columns (M = 128, N = 256: the
+// 2048-deep contraction moves (128 + 256) x 2048 x 2 bytes per tile, so wider tiles cut
+// the operand traffic per flop), K = 2048 streamed by TMA in 64-wide chunks (SW128) through
+// a 4-stage ring; the accumulator is double-buffered in TMEM (2 x 256 columns).  A CTA
+// walks one row tile's column tiles in order, as 128-column halves C = 0 .. R, and its 4
+// epilogue warps (thread = stride row = TMEM lane) keep the running max / sum of their row
+// (online softmax, log2 domain) and write
 //   P[r][J] = sum_{j in J} 2^(A log2e - m_C)   and   Mt[r][C] = m_C
 // (m_C: the running max after tile C) to a per-CTA scratch.  After the diagonal tile the
 // same warps combine their row tile:
@@ -27,15 +29,17 @@
 namespace mt {
 namespace xs {
 
-constexpr int kStages = 6;
+constexpr int kStages = 4;
 constexpr int kChunk = 64;            // K elements per stage
 constexpr int kKChunks = 2048 / kChunk;
-constexpr uint32_t kTileBytes = 128 * kChunk * 2;  // 16 KB per operand per stage
+constexpr int kN = 256;               // stride columns per MMA tile (two 128-column halves)
+constexpr uint32_t kTileA = 128 * kChunk * 2;  // 16 KB per stage
+constexpr uint32_t kTileB = kN * kChunk * 2;   // 32 KB per stage
 constexpr int kThreads = 192;
 
 struct Smem {
-  uint8_t a[kStages][kTileBytes];
-  uint8_t b[kStages][kTileBytes];
+  uint8_t a[kStages][kTileA];
+  uint8_t b[kStages][kTileB];
   uint64_t full[kStages], empty[kStages];
   uint64_t tfull[2], tempty[2];
   float fm[128], fl[128];  // final row max (log2) / sum of the item
@@ -50,7 +54,8 @@ struct Params {
   int h0;           // first q head of the launch (global)
   int grp;          // q heads per kv head
   float scale_log2; // log2(e) / (st sqrt d)
-  float* P;         // per CTA: [128][nI]
+  int ldp;          // P row stride: 16 nrt (16-byte aligned rows)
+  float* P;         // per CTA: [128][ldp]
   float* Mt;        // per CTA: [128][nrt]
   float* tri;       // [Hq][nI (nI + 1) / 2] block scores, row I at I (I + 1) / 2
   int64_t T;        // nI (nI + 1) / 2
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(smem_u32(&sm.tmem_base), 256);
+  if (warp == 1) tmem_alloc(smem_u32(&sm.tmem_base), 2 * kN);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmb);
@@ -100,15 +105,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int hh, R;
     for (int k = 0; item_of(p, k, hh, R); ++k) {
       const int kvh = (p.h0 + hh) / p.grp;
-      for (int C = 0; C <= R; ++C)
+      for (int C2 = 0; 2 * C2 <= R; ++C2)
         for (int kc = 0; kc < kKChunks; ++kc, ++it) {
           const uint32_t s = it % kStages;
           mbar_wait(smem_u32(&sm.empty[s]), ((it / kStages) & 1) ^ 1);
           if (lane == 0) {
             const uint32_t bar = smem_u32(&sm.full[s]);
-            mbar_expect_tx(bar, 2 * kTileBytes);
+            mbar_expect_tx(bar, kTileA + kTileB);
             tma_load_3d(smem_u32(sm.a[s]), &tma, bar, kc * kChunk, R * 128, hh);
-            tma_load_3d(smem_u32(sm.b[s]), &tmb, bar, kc * kChunk, C * 128, kvh);
+            tma_load_3d(smem_u32(sm.b[s]), &tmb, bar, kc * kChunk, C2 * kN, kvh);
           }
           __syncwarp();
         }
@@ -116,15 +121,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---- MMA issuer
     const bool leader = elect_one();
-    constexpr uint32_t idesc = make_idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idesc = make_idesc_bf16(128, kN, false, false);
     uint32_t it = 0, tile = 0;
     int hh, R;
     for (int k = 0; item_of(p, k, hh, R); ++k) {
-      for (int C = 0; C <= R; ++C, ++tile) {
+      for (int C2 = 0; 2 * C2 <= R; ++C2, ++tile) {
         const uint32_t b = tile & 1;
         mbar_wait(smem_u32(&sm.tempty[b]), ((tile >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + 128 * b;
+        const uint32_t d = tmem + kN * b;
         for (int kc = 0; kc < kKChunks; ++kc, ++it) {
           const uint32_t s = it % kStages;
           mbar_wait(smem_u32(&sm.full[s]), (it / kStages) & 1);
@@ -149,59 +154,64 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = q * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127 over the 4 epilogue warps
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    float* P = p.P + (size_t)blockIdx.x * 128 * p.nI;
+    float* P = p.P + (size_t)blockIdx.x * 128 * p.ldp;
     float* Mt = p.Mt + (size_t)blockIdx.x * 128 * p.nrt;
     uint32_t tile = 0;
     int hh, R;
     for (int k = 0; item_of(p, k, hh, R); ++k) {
       const int64_t grow = (int64_t)R * 128 + r;  // this thread's stride row
       float m = -INFINITY, l = 0.f;
-      for (int C = 0; C <= R; ++C, ++tile) {
+      for (int C2 = 0; 2 * C2 <= R; ++C2, ++tile) {
         const uint32_t b = tile & 1;
         mbar_wait(smem_u32(&sm.tfull[b]), (tile >> 1) & 1);
         tc_fence_after();
-        uint32_t v[4][32];
+        for (int half = 0; half < 2; ++half) {  // 128-column halves C = 2 C2 + half
+          const int C = 2 * C2 + half;
+          if (C > R) break;  // beyond the diagonal tile: nothing valid
+          uint32_t v[4][32];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) tmem_ld32(tmem + lane_base + 128 * b + 32 * g, v[g]);
-        tmem_ld_wait();
+          for (int g = 0; g < 4; ++g)
+            tmem_ld32(tmem + lane_base + kN * b + 128 * half + 32 * g, v[g]);
+          tmem_ld_wait();
+          // valid columns: j <= i (causal, the diagonal tile) and j < n
+          const int64_t c0 = (int64_t)C * 128;
+          int lim = (int)min((int64_t)127, min(grow, p.n - 1) - c0);  // last valid column
+          if (grow >= p.n) lim = -1;
+          float tmax = -INFINITY;
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (32 * g + c <= lim) tmax = fmaxf(tmax, __uint_as_float(v[g][c]) * p.scale_log2);
+          const float mn = fmaxf(m, tmax);
+          float part[16];
+          float s = 0.f;
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float acc = 0.f;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const int col = 32 * g + 8 * jj + c;
+                const float e = col <= lim ? exp2f(__uint_as_float(v[g][8 * jj + c]) * p.scale_log2 - mn) : 0.f;
+                acc += e;
+              }
+              part[4 * g + jj] = acc;
+              s += acc;
+            }
+          l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) + s;
+          m = mn;
+          if (grow < p.n) {
+            float4* dst = reinterpret_cast<float4*>(P + (size_t)r * p.ldp + 16 * C);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              dst[u] = make_float4(part[4 * u], part[4 * u + 1], part[4 * u + 2], part[4 * u + 3]);
+            Mt[(size_t)r * p.nrt + C] = mn;
+          }
+        }
         tc_fence_before();
         mbar_arrive(smem_u32(&sm.tempty[b]));  // the accumulator may be overwritten
-        // valid columns: j <= i (causal, the diagonal tile) and j < n
-        const int64_t c0 = (int64_t)C * 128;
-        int lim = (int)min((int64_t)127, min(grow, p.n - 1) - c0);  // last valid column
-        if (grow >= p.n) lim = -1;
-        float tmax = -INFINITY;
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-#pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (32 * g + c <= lim) tmax = fmaxf(tmax, __uint_as_float(v[g][c]) * p.scale_log2);
-        const float mn = fmaxf(m, tmax);
-        float part[16];
-        float s = 0.f;
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            float acc = 0.f;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const int col = 32 * g + 8 * jj + c;
-              const float e = col <= lim ? exp2f(__uint_as_float(v[g][8 * jj + c]) * p.scale_log2 - mn) : 0.f;
-              acc += e;
-            }
-            part[4 * g + jj] = acc;
-            s += acc;
-          }
-        l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) + s;
-        m = mn;
-        if (grow < p.n) {
-          float4* dst = reinterpret_cast<float4*>(P + (size_t)r * p.nI + 16 * C);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            dst[u] = make_float4(part[4 * u], part[4 * u + 1], part[4 * u + 2], part[4 * u + 3]);
-          Mt[(size_t)r * p.nrt + C] = mn;
-        }
       }
       // ---- combine the row tile: Bs[I][J] for its 16 query blocks, J <= I
       sm.fm[r] = m;
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = 8 * ib + rr;
             const float lr = sm.fl[row];
             if (lr > 0.f)
-              acc += P[(size_t)row * p.nI + J] * exp2f(Mt[(size_t)row * p.nrt + J / 16] - sm.fm[row]) / lr;
+              acc += P[(size_t)row * p.ldp + J] * exp2f(Mt[(size_t)row * p.nrt + J / 16] - sm.fm[row]) / lr;
           }
           out[J] = acc;
         }
@@ -230,14 +240,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  if (warp == 1) tmem_dealloc(tmem, 2 * kN);
 }
 
 }  // namespace xs
 
 size_t xattn_score_scratch_bytes(int64_t n, int nI, int num_sms) {
   const int nrt = (int)((n + 127) / 128);
-  return (size_t)num_sms * 128 * ((size_t)nI + nrt) * 4;
+  (void)nI;
+  return (size_t)num_sms * 128 * ((size_t)16 * nrt + nrt) * 4;
 }
 
 // Block scores of q heads [h0, h0 + hb) into tri (layout above).  qr: [hb][n][2048] bf16
@@ -254,15 +265,17 @@ mt_status xattn_scores_tc(const void* qr, const void* kr, int64_t n, int nI, int
   p.h0 = h0;
   p.grp = grp;
   p.scale_log2 = scale_log2;
+  p.ldp = 16 * p.nrt;
   p.P = static_cast<float*>(scratch);
-  p.Mt = p.P + (size_t)num_sms * 128 * nI;
+  p.Mt = p.P + (size_t)num_sms * 128 * p.ldp;
   p.tri = tri;
   p.T = T;
   CUtensorMap ta, tb;
   if (make_tmap_bf16_3d(&ta, qr, 2048, (uint64_t)n, (uint64_t)hb, kChunk, 128, 1) ||
-      make_tmap_bf16_3d(&tb, kr, 2048, (uint64_t)n, (uint64_t)Hkv, kChunk, 128, 1))
+      make_tmap_bf16_3d(&tb, kr, 2048, (uint64_t)n, (uint64_t)Hkv, kChunk, kN, 1))
     return fail(MT_ECUDA, "cuTensorMapEncodeTiled (xattn scores) failed");
   const size_t smem = sizeof(Smem) + 1024;
+  if (p.ldp < 0) return fail(MT_ESHAPE, "xattn scores: bad shape");
   if (cudaFuncSetAttribute(xattn_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return fail(MT_ECUDA, "cudaFuncSetAttribute(xattn_score_kernel) failed");
