@@ -598,6 +598,85 @@ __global__ void __launch_bounds__(kSelThreads) select_small(const uint64_t* keys
   compact(bits, words, out, (which ? s_cnt : v_cnt) + h);
 }
 
+// S <= 4096: the same select with the keys SORTED in one CTA (cub::BlockRadixSort over the
+// key bits, 512 threads x 8 keys, blocked arrangement), then the budget by a block scan of
+// the sorted scores: k = 1 + the first position whose inclusive mass reaches the budget
+// (topp_count's rule), and the first k keys marked.  Measured faster than the radix search
+// above at 4K (whose rounds rescan every key while most share the leading bits).
+constexpr int kSortSel = 4096;
+constexpr int kSortItems = kSortSel / kSelThreads;  // 8
+__global__ void __launch_bounds__(kSelThreads) select_sorted(const uint64_t* keysV, const uint64_t* keysP,
+                                                              int64_t nV, int64_t nP, uint64_t pq_v,
+                                                              uint64_t pq_s, int ibV, int ibP,
+                                                              int32_t* v_cnt, int32_t* v_idx,
+                                                              int64_t v_stride, int32_t* s_cnt,
+                                                              int32_t* s_off, int64_t s_stride) {
+  using Sort = cub::BlockRadixSort<uint64_t, kSelThreads, kSortItems>;
+  using Scan = cub::BlockScan<unsigned long long, kSelThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t bits[kSortSel / 32];
+  __shared__ int kmin;
+  const int h = blockIdx.x, which = blockIdx.y;
+  const int n = (int)(which ? nP : nV);
+  const int ib = which ? ibP : ibV;
+  const uint64_t pq = which ? pq_s : pq_v;
+  const uint64_t* src = (which ? keysP : keysV) + (size_t)h * n;
+  const int nbits = kScoreBits + ib;  // < 64 for n <= 4096
+  const uint64_t lowmask = (1ull << nbits) - 1;
+  const uint64_t smax = (1ull << kScoreBits) - 1;
+  const int tid = threadIdx.x;
+  const int words = (n + 31) / 32;
+  for (int x = tid; x < words; x += kSelThreads) bits[x] = 0u;
+  if (tid == 0) kmin = n;
+  uint64_t key[kSortItems];
+#pragma unroll
+  for (int u = 0; u < kSortItems; ++u) {  // blocked: thread t holds positions 8t .. 8t + 7
+    const int x = tid * kSortItems + u;
+    key[u] = x < n ? (src[x] & lowmask) : (1ull << nbits);  // padding sorts last
+  }
+  Sort(tmp.sort).Sort(key, 0, nbits + 1);
+  __syncthreads();
+  unsigned long long sc[kSortItems], tsum = 0;
+#pragma unroll
+  for (int u = 0; u < kSortItems; ++u) {
+    const bool pad = key[u] >> nbits;
+    sc[u] = pad ? 0ull : smax - ((key[u] >> ib) & smax);
+    tsum += sc[u];
+  }
+  unsigned long long excl, tot;
+  Scan(tmp.scan).ExclusiveSum(tsum, excl, tot);
+  int k = n;  // p = 1: every item (reading R22)
+  if (pq < (1ull << 24)) {
+    const unsigned long long rhs = pq * tot;
+    unsigned long long cum = excl;
+#pragma unroll
+    for (int u = 0; u < kSortItems; ++u) {
+      cum += sc[u];
+      const int pos = tid * kSortItems + u;
+      if (pos < n && (cum << 24) >= rhs) {
+        atomicMin(&kmin, pos + 1);
+        break;
+      }
+    }
+    __syncthreads();
+    k = kmin;
+  }
+  const uint64_t imask = (1ull << ib) - 1;
+#pragma unroll
+  for (int u = 0; u < kSortItems; ++u)
+    if (tid * kSortItems + u < k) {
+      const uint32_t idx = (uint32_t)(key[u] & imask);
+      atomicOr(&bits[idx >> 5], 1u << (idx & 31));
+    }
+  if (tid == 0) atomicOr(&bits[0], 1u);  // forced: column 0 / offset 0 (reading R7)
+  __syncthreads();
+  int32_t* out = which ? s_off + (size_t)h * s_stride : v_idx + (size_t)h * v_stride;
+  compact(bits, words, out, (which ? s_cnt : v_cnt) + h);
+}
+
 __global__ void fill_f32(float* p, float v, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -735,9 +814,15 @@ mt_status vsidx_build(VSCollectives* coll, int64_t S, int Hq, int Hkv, int W, in
   // MT_VS_SELECT_SMALL=0 forces the radix-sort path (tests compare the two)
   static const bool small_ok = !getenv("MT_VS_SELECT_SMALL") || atoi(getenv("MT_VS_SELECT_SMALL"));
   if (S <= kSmallSel && small_ok) {
-    select_small<<<dim3(Hq, 2), kSelThreads, 0, st>>>(w.keysV, w.keysP, S, nb, pq_v, pq_s, kv.ib,
-                                                  kp.ib, v_cnt, v_idx, v_stride, s_cnt, s_off,
-                                                  s_stride);
+    if (S <= kSortSel) {
+      select_sorted<<<dim3(Hq, 2), kSelThreads, 0, st>>>(w.keysV, w.keysP, S, nb, pq_v, pq_s,
+                                                         kv.ib, kp.ib, v_cnt, v_idx, v_stride,
+                                                         s_cnt, s_off, s_stride);
+    } else {
+      select_small<<<dim3(Hq, 2), kSelThreads, 0, st>>>(w.keysV, w.keysP, S, nb, pq_v, pq_s,
+                                                        kv.ib, kp.ib, v_cnt, v_idx, v_stride,
+                                                        s_cnt, s_off, s_stride);
+    }
     return check_launch("vs select_small");
   }
   size_t tb;

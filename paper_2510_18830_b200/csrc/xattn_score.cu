@@ -18,9 +18,14 @@
 // same warps combine their row tile:
 //   Bs[I][J] = sum_{r in I} P[r][J] 2^(Mt[r][J/16] - m_r) / l_r
 // Work items (head, row tile) are dealt in descending row-tile order, snake-wise over the
-// persistent CTAs (the work of a row tile is proportional to R + 1).
+// persistent CTAs (the work of a row tile is proportional to R + 1).  Default: clusters of
+// two CTAs take row tiles 2j + 1 and 2j and share every B tile (each loads one 128-row
+// half and multicasts it; a stage is refilled once both CTAs' MMAs released it), which
+// halves the B traffic (MT_XATTN_PAIR=0: one CTA per row tile).
 // Warp roles: 0 TMA, 1 MMA (one elected lane), 2-5 epilogue.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -61,16 +66,44 @@ struct Params {
   int64_t T;        // nI (nI + 1) / 2
 };
 
-// item k of this CTA: the snake-dealt k-th item; items sorted by descending row tile
+// item k of this CTA: the snake-dealt k-th item; items sorted by descending row tile.
+// kPair: CTAs come in clusters of two that take row tiles 2j + 1 and 2j of one head (both
+// walk column tiles 0 .. j) and share each 256-row B tile, every CTA loading one half and
+// multicasting it to both (a row tile past the end computes masked rows only).
+template <bool kPair>
 __device__ __forceinline__ bool item_of(const Params& p, int k, int& hh, int& R) {
-  const int G = gridDim.x;
-  const int i = k * G + ((k & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
-  if (i >= p.hb * p.nrt) return false;
-  R = p.nrt - 1 - i / p.hb;
+  const int G = kPair ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int me = kPair ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+  const int i = k * G + ((k & 1) ? G - 1 - me : me);
+  const int nu = kPair ? (p.nrt + 1) / 2 : p.nrt;
+  if (i >= p.hb * nu) return false;
   hh = i % p.hb;
+  if (kPair)
+    R = 2 * (nu - 1 - i / p.hb) + 1 - (int)(blockIdx.x & 1);
+  else
+    R = p.nrt - 1 - i / p.hb;
   return true;
 }
 
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const void* tmap, uint32_t bar, int c0,
+                                               int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     xattn_score_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tma,
                        const __grid_constant__ CUtensorMap tmb) {
@@ -81,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), kPair ? 2 : 1);  // kPair: both CTAs' MMAs read the stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
@@ -96,16 +129,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // the peer's barriers are initialised
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  const int crank = kPair ? (int)(blockIdx.x & 1) : 0;
 
   if (warp == 0) {
     // ---- TMA producer
     uint32_t it = 0;
     int hh, R;
-    for (int k = 0; item_of(p, k, hh, R); ++k) {
+    for (int k = 0; item_of<kPair>(p, k, hh, R); ++k) {
       const int kvh = (p.h0 + hh) / p.grp;
-      for (int C2 = 0; 2 * C2 <= R; ++C2)
+      const int rmax = kPair ? (R | 1) : R;  // the pair walks the odd row tile's columns
+      for (int C2 = 0; 2 * C2 <= rmax; ++C2)
         for (int kc = 0; kc < kKChunks; ++kc, ++it) {
           const uint32_t s = it % kStages;
           mbar_wait(smem_u32(&sm.empty[s]), ((it / kStages) & 1) ^ 1);
@@ -113,7 +149,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t bar = smem_u32(&sm.full[s]);
             mbar_expect_tx(bar, kTileA + kTileB);
             tma_load_3d(smem_u32(sm.a[s]), &tma, bar, kc * kChunk, R * 128, hh);
-            tma_load_3d(smem_u32(sm.b[s]), &tmb, bar, kc * kChunk, C2 * kN, kvh);
+            if constexpr (kPair)  // this CTA's half of B, to both CTAs of the pair
+              tma_load_3d_mc(smem_u32(sm.b[s]) + crank * (kTileB / 2), &tmb, bar, kc * kChunk,
+                             C2 * kN + crank * (kN / 2), kvh, (uint16_t)3);
+            else
+              tma_load_3d(smem_u32(sm.b[s]), &tmb, bar, kc * kChunk, C2 * kN, kvh);
           }
           __syncwarp();
         }
@@ -124,8 +164,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc = make_idesc_bf16(128, kN, false, false);
     uint32_t it = 0, tile = 0;
     int hh, R;
-    for (int k = 0; item_of(p, k, hh, R); ++k) {
-      for (int C2 = 0; 2 * C2 <= R; ++C2, ++tile) {
+    for (int k = 0; item_of<kPair>(p, k, hh, R); ++k) {
+      const int rmax = kPair ? (R | 1) : R;
+      for (int C2 = 0; 2 * C2 <= rmax; ++C2, ++tile) {
         const uint32_t b = tile & 1;
         mbar_wait(smem_u32(&sm.tempty[b]), ((tile >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -140,7 +181,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < kChunk; kk += 16)
               mma_ss(d, sdesc_add(da, kk * 2), sdesc_add(db, kk * 2), idesc, (kc | kk) ? 1u : 0u);
-            mma_commit(smem_u32(&sm.empty[s]));
+            if constexpr (kPair)
+              mma_commit_mc(smem_u32(&sm.empty[s]), (uint16_t)3);  // frees the stage in both CTAs
+            else
+              mma_commit(smem_u32(&sm.empty[s]));
           }
           __syncwarp();
         }
@@ -158,10 +202,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* Mt = p.Mt + (size_t)blockIdx.x * 128 * p.nrt;
     uint32_t tile = 0;
     int hh, R;
-    for (int k = 0; item_of(p, k, hh, R); ++k) {
+    for (int k = 0; item_of<kPair>(p, k, hh, R); ++k) {
       const int64_t grow = (int64_t)R * 128 + r;  // this thread's stride row
+      const int rmax = kPair ? (R | 1) : R;
       float m = -INFINITY, l = 0.f;
-      for (int C2 = 0; 2 * C2 <= R; ++C2, ++tile) {
+      for (int C2 = 0; 2 * C2 <= rmax; ++C2, ++tile) {
         const uint32_t b = tile & 1;
         mbar_wait(smem_u32(&sm.tfull[b]), (tile >> 1) & 1);
         tc_fence_after();
@@ -239,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // no multicast or remote arrive is still in flight
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 2 * kN);
 }
@@ -270,18 +316,43 @@ mt_status xattn_scores_tc(const void* qr, const void* kr, int64_t n, int nI, int
   p.Mt = p.P + (size_t)num_sms * 128 * p.ldp;
   p.tri = tri;
   p.T = T;
+  // MT_XATTN_PAIR=0: one CTA per row tile, each loading its whole B tile (A/B switch)
+  static const bool pair = !getenv("MT_XATTN_PAIR") || atoi(getenv("MT_XATTN_PAIR"));
   CUtensorMap ta, tb;
   if (make_tmap_bf16_3d(&ta, qr, 2048, (uint64_t)n, (uint64_t)hb, kChunk, 128, 1) ||
-      make_tmap_bf16_3d(&tb, kr, 2048, (uint64_t)n, (uint64_t)Hkv, kChunk, kN, 1))
+      make_tmap_bf16_3d(&tb, kr, 2048, (uint64_t)n, (uint64_t)Hkv, kChunk, pair ? kN / 2 : kN, 1))
     return fail(MT_ECUDA, "cuTensorMapEncodeTiled (xattn scores) failed");
   const size_t smem = sizeof(Smem) + 1024;
   if (p.ldp < 0) return fail(MT_ESHAPE, "xattn scores: bad shape");
-  if (cudaFuncSetAttribute(xattn_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (pair) {
+    if (cudaFuncSetAttribute(xattn_score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return fail(MT_ECUDA, "cudaFuncSetAttribute(xattn_score_kernel) failed");
+    const int units = hb * ((p.nrt + 1) / 2);
+    int pairs = num_sms / 2;
+    if (units < pairs) pairs = units;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, xattn_score_kernel<true>, p, ta, tb) != cudaSuccess)
+      return fail(MT_ECUDA, "cudaLaunchKernelEx(xattn_score_kernel, cluster 2) failed");
+    return check_launch("xattn_score_kernel");
+  }
+  if (cudaFuncSetAttribute(xattn_score_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return fail(MT_ECUDA, "cudaFuncSetAttribute(xattn_score_kernel) failed");
   const int items = hb * p.nrt;
   const int grid = items < num_sms ? items : num_sms;
-  xattn_score_kernel<<<grid, kThreads, smem, st>>>(p, ta, tb);
+  xattn_score_kernel<false><<<grid, kThreads, smem, st>>>(p, ta, tb);
   return check_launch("xattn_score_kernel");
 }
 
