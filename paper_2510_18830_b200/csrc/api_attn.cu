@@ -3,6 +3,8 @@
 // caller's stream.
 #include <mutex>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -202,7 +204,14 @@ extern "C" mt_status mt_sparse_attn_bwd(const mt_shape* sh, const void* q, const
   MT_TRY(vs_plan_build(&plan, S, Hq, Hkv, 1, 0, idx->v_cnt, idx->v_idx, idx->v_stride, idx->s_cnt,
                        idx->s_off, (int)idx->s_stride, w.plan, stream));
   // D, and the fp32 dQ / dK / dV accumulators zeroed in the same pass
-  MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream, w.dq, w.dk, w.dv, Hkv));
+  static const bool memset_acc = getenv("MT_BWD_MEMSET") && atoi(getenv("MT_BWD_MEMSET"));
+  if (memset_acc) {  // A/B: round 1's separate memset of the accumulators
+    MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream));
+    cudaMemsetAsync(w.dq, 0, (size_t)((const char*)(w.dv + S * Hkv * 128) - (const char*)w.dq),
+                    stream);
+  } else {
+    MT_TRY(attn_bwd_preprocess(o, dO, w.D, S, Hq, stream, w.dq, w.dk, w.dv, Hkv));
+  }
   MT_TRY(attn_bwd_step(plan, 0, 0, (int)(S / 64), q, k, v, dO, lse, w.D, w.dq, w.dk, w.dv,
                        device_num_sms(), stream));
   return f32_to_bf16_x3(w.dq, dq, S * Hq * 128, w.dk, dk, S * Hkv * 128, w.dv, dv, S * Hkv * 128,
