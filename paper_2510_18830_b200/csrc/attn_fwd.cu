@@ -135,6 +135,7 @@ struct Params {
   float* lse;
   int* fix_count;  // tiles flagged for the exact fix-up pass
   int stabfix;     // 1: chunk-0 fallback stabiliser + underflow check (MT_FWD_STABFIX=0: off, A/B)
+  int dbg;         // profiling knock-outs (MT_FWD_DBG): bit0 skip the softmax math (wrong results)
   int* fix_list;
   int* tile_counter;  // dynamic tile scheduler (zeroed before the launch)
   int order;          // tile order (MT_FWD_ORDER): 1 head-major (default; L2 reuse of K/V), 0 query-block-major
@@ -813,7 +814,7 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
       float emax = -INFINITY;
       bool any_live = false;
 #pragma unroll 1
-      for (int cg = 0; cg < 4; ++cg) {
+      for (int cg = 0; cg < ((P.dbg & 1) ? 0 : 4); ++cg) {  // MT_FWD_DBG=1: no softmax (timing only)
         uint32_t sv[32], pk[16];
         tmem_ld32(Sb + 32 * cg, sv);
         tmem_ld_wait();
@@ -1204,6 +1205,8 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.order = ord;
   P.fix_list = plan.scratch + 16;
   static const int stabfix = getenv("MT_FWD_STABFIX") ? atoi(getenv("MT_FWD_STABFIX")) : 1;
+  static const int fdbg = getenv("MT_FWD_DBG") ? atoi(getenv("MT_FWD_DBG")) : 0;
+  P.dbg = fdbg;
   P.stabfix = stabfix;
   static const int pack = getenv("MT_FWD_PACK") ? atoi(getenv("MT_FWD_PACK")) : 1;
   P.packed = pack && plan.kp && plan.pcap > 0;
