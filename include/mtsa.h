@@ -81,7 +81,9 @@ typedef struct {
   int32_t n_q_heads;  /* Hq */
   int32_t n_kv_heads; /* Hkv; q head h uses kv head h / (Hq / Hkv) */
   int32_t head_dim;   /* d, must be 128 */
-  int32_t block;      /* B = stripe = slash block = window rows, must be 64 */
+  int32_t block;      /* B = stripe = slash block, must be 64 */
+  int32_t last_q;     /* window rows of Alg. 1 (`last_q`, never given: reading R2), must be
+                         64 = one block; 0 means 64 */
   int32_t layout;     /* MT_LAYOUT_STRIPED or MT_LAYOUT_ZIGZAG (multi-rank calls) */
 } mt_shape;
 

@@ -27,7 +27,7 @@ class MTError(RuntimeError):
 class Shape(ctypes.Structure):
     _fields_ = [("seq_len", ctypes.c_int64), ("n_q_heads", ctypes.c_int32),
                 ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
-                ("block", ctypes.c_int32), ("layout", ctypes.c_int32)]
+                ("block", ctypes.c_int32), ("last_q", ctypes.c_int32), ("layout", ctypes.c_int32)]
 
 
 class VSParams(ctypes.Structure):

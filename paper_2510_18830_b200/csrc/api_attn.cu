@@ -55,6 +55,8 @@ mt_status check_shape(const mt_shape* sh, int W) {
   if (!sh) return fail(MT_ESHAPE, "shape is NULL");
   if (sh->head_dim != 128) return fail(MT_EUNSUPPORTED, "head_dim must be 128 (got %d)", sh->head_dim);
   if (sh->block != 64) return fail(MT_EUNSUPPORTED, "block must be 64 (got %d)", sh->block);
+  if (sh->last_q != 0 && sh->last_q != 64)
+    return fail(MT_EUNSUPPORTED, "last_q must be 64 (got %d; reading R2)", sh->last_q);
   if (sh->n_q_heads <= 0 || sh->n_kv_heads <= 0 || sh->n_q_heads % sh->n_kv_heads)
     return fail(MT_ESHAPE, "bad head counts Hq=%d Hkv=%d", sh->n_q_heads, sh->n_kv_heads);
   if (sh->seq_len < 64 || sh->seq_len % 64)

@@ -35,7 +35,7 @@ LAYOUTS = {"striped": 0, "zigzag": 1}  # MT_LAYOUT_STRIPED / MT_LAYOUT_ZIGZAG (i
 
 
 def shape(seq_len: int, n_q_heads: int, n_kv_heads: int, layout: str = "striped") -> _lib.Shape:
-    return _lib.Shape(seq_len, n_q_heads, n_kv_heads, HEAD_DIM, BLOCK, LAYOUTS[layout])
+    return _lib.Shape(seq_len, n_q_heads, n_kv_heads, HEAD_DIM, BLOCK, BLOCK, LAYOUTS[layout])
 
 
 @dataclass

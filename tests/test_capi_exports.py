@@ -48,3 +48,23 @@ def test_host_only_calls_work_without_a_gpu():
     _lib.check(lib.mt_ring_schedule(W, W, out))
     assert [out[t * W + r] for t in range(W) for r in range(W)] == \
         [(r - t) % W for t in range(W) for r in range(W)]
+
+
+def test_shape_validation_runs_before_any_device_work():
+    """mt_shape checks (include/mtsa.h) are host logic: d, block, last_q (reading R2: 64, 0 = 64)
+    and the layout field are rejected with their status codes before any CUDA call."""
+    from paper_2510_18830_b200 import ops
+    lib = _lib.lib()
+    prm = ops.VSParams(0.9, 0.9)
+
+    def status(**kw):
+        sh = ops.shape(4096, 8, 1)
+        for k, v in kw.items():
+            setattr(sh, k, v)
+        return lib.mt_build_vs_index(None, ctypes.byref(sh), ctypes.byref(prm), None, None, None,
+                                     None, 0, None)
+    assert status(head_dim=64) == 7      # MT_EUNSUPPORTED
+    assert status(block=32) == 7
+    assert status(last_q=32) == 7
+    assert status(layout=5) == 1         # MT_ESHAPE
+    assert status(seq_len=4000) == 2     # MT_EWINDOW
