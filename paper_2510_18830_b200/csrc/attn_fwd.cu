@@ -268,7 +268,13 @@ __device__ void producer_k(Smem& sm, const Params& P, const CUtensorMap* tmq,
         if (o1 >= 0) flags |= (live1 & 3u) << 2;
         if (o0 == 0) flags |= 16u;
         if (o1 == 0) flags |= 32u;
+#ifdef MT_TL_PROD
+        if (lane == 0) MT_TL(4, dk);  // producer reached the chunk (before the vmeta / K waits)
+#endif
         VMeta& vm = vmacquire();
+#ifdef MT_TL_PROD
+        if (lane == 0) MT_TL(5, dk);  // vmeta slot acquired
+#endif
         kacquire();
         if (lane == 0) {
           vm.kind = kBlk;
@@ -777,7 +783,9 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
           base = (base & ~(1023u << (10 * bb))) | (((cnt_get(base, bb) + tile_events(n, bb)) & 1023u) << (10 * bb));
         break;
       }
+#ifndef MT_TL_PROD
       if (row == 0) MT_TL(4, cm.seq);
+#endif
       tc_fence_after();
       if (!m_synced) {
         if (wg == 0) {  // chunk 0: exact max of the row's live scores
@@ -858,7 +866,9 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(pfull);
+#ifndef MT_TL_PROD
       if (row == 0) MT_TL(5, cm.seq);
+#endif
     }
     if (tile < 0) break;  // DONE
     int h0, h1, j;
