@@ -143,10 +143,20 @@ struct Tile {
   int j_lo, j_hi;  // BAR: local query blocks [j_lo, j_hi) of this part
 };
 
+// Tile kinds a launch holds (template M): kOnlyBlock / kOnlyBar launches (large sequences:
+// the block pass compiles without any bar-tile branch, as round 1's) or kMixed (one launch
+// for both kinds: short sequences, where the tail of one pass overlaps the other).
+enum : int { kOnlyBlock = 0, kOnlyBar = 1, kMixed = 2 };
+template <int M>
+__device__ __forceinline__ bool is_block(int mode) { return M == kOnlyBlock || (M == kMixed && mode == kModeBlock); }
+template <int M>
+__device__ __forceinline__ bool is_bar(int mode) { return M == kOnlyBar || (M == kMixed && mode == kModeBar); }
+
 // BAR tiles of this launch: sum over q heads of ceil(|origin list| / 128) x parts
+template <int M>
 __device__ __forceinline__ int bar_tile_count(const Params& P) {
   const VSPlan& pl = P.plan;
-  if (P.n_bar == 0) return 0;
+  if (M == kOnlyBlock || P.n_bar == 0) return 0;
   int n = 0;
   for (int h = 0; h < pl.Hq; ++h)
     n += (pl.vptr[h * (pl.W + 1) + P.s + 1] - pl.vptr[h * (pl.W + 1) + P.s] + 127) / 128;
@@ -156,13 +166,19 @@ __device__ __forceinline__ int bar_tile_count(const Params& P) {
 // One launch runs both tile kinds (the tail of one overlaps the other): BLOCK tiles
 // [0, n_block) and BAR tiles after them, or BAR tiles first when P.bar_first (their
 // per-tile work is the longest).  nbar = bar_tile_count(P).
+template <int M>
 __device__ __forceinline__ Tile decode_tile(const Params& P, int tile, int nbar) {
   Tile T{};
   const VSPlan& pl = P.plan;
   const int W = pl.W;
-  if (tile < 0 || tile >= P.n_block + nbar) return T;
+  const int nblk = M == kOnlyBar ? 0 : P.n_block;
+  if (tile < 0 || tile >= nblk + nbar) return T;
   int bt;  // BLOCK tile index, or -1
-  if (P.bar_first) {
+  if (M == kOnlyBlock) {
+    bt = tile;
+  } else if (M == kOnlyBar) {
+    bt = -1 - tile;
+  } else if (P.bar_first) {
     bt = tile >= nbar ? tile - nbar : -1;
     if (bt < 0) bt = -1 - tile;  // BAR tile -(bt + 1)
   } else {
@@ -209,7 +225,7 @@ __device__ __forceinline__ Tile decode_tile(const Params& P, int tile, int nbar)
 }
 
 // ------------------------------------------------------------------ producer
-template <int L>  // sequence layout (plan.cuh), fixed per launch
+template <int L, int M>  // sequence layout (plan.cuh) and tile kinds, fixed per launch
 __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
                          const CUtensorMap* tmdo, const CUtensorMap* tmk,
                          const CUtensorMap* tmv) {
@@ -220,7 +236,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
   uint32_t c = 0;  // chunk events (incl. END)
   uint32_t ntile = 0;
   int cur_mode = kModeBlock;
-  const int nbar = bar_tile_count(P);
+  const int nbar = bar_tile_count<M>(P);
   auto emit = [&](int h, int j, uint32_t flags) {
     const uint32_t stage = c % kStages;
     MT_CRUMB(2, 1000000 + (int)c);
@@ -264,7 +280,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
       if (lane == 0) tile = atomicAdd(P.tile_counter, 1);
       tile = __shfl_sync(0xffffffffu, tile, 0);
     }
-    const Tile T = decode_tile(P, tile, nbar);
+    const Tile T = decode_tile<M>(P, tile, nbar);
     if (!T.ok) break;
     cur_mode = T.mode;
     if (T.skip) continue;
@@ -278,7 +294,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     }
     ++ntile;
     const uint32_t kvbar = smem_u32(&sm.kvfull);
-    if (T.mode == kModeBlock) {
+    if (is_block<M>(T.mode)) {
       const bool v1 = T.lb0 + 1 < P.nloc;
       if (lane == 0) {
         // a missing second slot re-loads block lb0: every K/V row must be finite
@@ -317,7 +333,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
     }
 
     // ---- chunk stream
-    if (T.mode == kModeBlock) {
+    if (is_block<M>(T.mode)) {
       const bool v1 = T.lb0 + 1 < P.nloc;
       const int kb0 = l2g_<L>(pl, P.s, T.lb0);  // global key block of slot 0
       if (pl.tptr) {
@@ -443,6 +459,7 @@ __device__ void producer(Smem& sm, const Params& P, const CUtensorMap* tmq,
 // Chunk k of a tile goes to softmax warpgroup k & 1.  Per chunk: S^T, dP^T into
 // the shared TMEM pair, then the gradient MMAs of the previous chunk (dV, dK
 // accumulate; dQ^T into that warpgroup's buffer).
+template <int M>
 __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
   const bool leader = elect_one();
   const uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // S^T, dP^T
@@ -479,7 +496,8 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     ++ntile;
     {  // BAR tiles: K/V rows arrived by cp.async (generic proxy)
       const ChunkMeta& m0 = sm.meta[c % kStages];  // the tile's first event (waited above)
-      if (m0.kind == kChunk && m0.mode == kModeBar) fence_proxy_async_smem();
+      if (M == kOnlyBar || (M == kMixed && m0.kind == kChunk && m0.mode == kModeBar))
+        fence_proxy_async_smem();
     }
     tc_fence_after();
     // Event-driven issue: S^T/dP^T of chunk k as soon as its Q/dO landed and its
@@ -643,6 +661,7 @@ __device__ __forceinline__ void softmax_half(const uint32_t (&sv)[32], const uin
   }
 }
 
+template <int M>
 __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUtensorMap* tmdq,
                             const CUtensorMap* tmdk, const CUtensorMap* tmdv) {
   const int w = warp_id();
@@ -662,7 +681,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
   uint32_t su = 0, gw = 0;  // sfull events, gdone waits
   uint32_t ntile = 0;
-  const int nbar = bar_tile_count(P);
+  const int nbar = bar_tile_count<M>(P);
   bool staging_busy = false;  // a bulk reduce may still be reading this warpgroup's buffer
 
   auto wait_staging = [&]() {  // warpgroup-uniform
@@ -768,14 +787,14 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         tile = cm.kind == kEnd ? cm.tile : -1;
         break;
       }
-      if (cm.mode == kModeBar && my_col == -2) my_col = sm.cols[row];
+      if (is_bar<M>(cm.mode) && my_col == -2) my_col = sm.cols[row];
 #ifndef MT_TL_WARPS
       if (row == 0) MT_TL(4, cm.seq);
 #endif
       tc_fence_after();
       // which of the 64 queries see this key row
       uint64_t vis;
-      if (cm.mode == kModeBlock) {
+      if (is_block<M>(cm.mode)) {
         const bool live = (cm.flags >> slot) & 1u;
         const bool diag = (cm.flags >> (2 + slot)) & 1u;
         vis = live ? (diag ? (~0ull << kk) : ~0ull) : 0ull;  // causal: query i >= key kk
@@ -841,7 +860,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       had_chunk = true;
     }
     if (tile < 0) break;  // DONE
-    const Tile T = decode_tile(P, tile, nbar);
+    const Tile T = decode_tile<M>(P, tile, nbar);
     wait_staging();  // the epilogue stages dK/dV in the same buffer
     tc_fence_after();
     if (row == 0) sm.tile_chunks[wg] = had_chunk ? 1 : 0;
@@ -852,7 +871,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
     // ---- dK (warpgroup 0) / dV (warpgroup 1) epilogue: the tile's key rows
     bool live_row;
     int64_t lrow;
-    if (T.mode == kModeBlock) {
+    if (is_block<M>(T.mode)) {
       live_row = any_chunk && !(slot == 1 && T.lb0 + 1 >= P.nloc);
       lrow = (int64_t)(T.lb0 + slot) * 64 + kk;
     } else {
@@ -861,7 +880,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       lrow = live_row ? (int64_t)plan_g2l(pl, m >> 6) * 64 + (m & 63) : 0;
     }
     const uint32_t col = wg == 0 ? kColDK : kColDV;
-    if (T.mode == kModeBlock) {
+    if (is_block<M>(T.mode)) {
       // rows lb0*64 .. +127 are contiguous: stage [128 rows][32 d] fp32 (SW128) in this
       // warpgroup's P/dS buffer, two column groups per round, and bulk reduce-add them
       // (rows past the chunk end are clipped by the tensor map; they hold zeros anyway)
@@ -916,6 +935,9 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   }
 }
 
+// one instantiation per sequence layout: each carries only its own producer walk (the kernel
+// with both was 52% larger, and its instruction footprint measurably slowed the striped case)
+template <int L, int M>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmdo,
@@ -958,12 +980,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
     if (warp == 0) {
-      if (P.plan.layout)
-        producer<1>(sm, P, &tmq, &tmdo, &tmk, &tmv);
-      else
-        producer<0>(sm, P, &tmq, &tmdo, &tmk, &tmv);
+      producer<L, M>(sm, P, &tmq, &tmdo, &tmk, &tmv);
     } else if (warp == 1) {
-      mma_issuer(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
+      mma_issuer<M>(sm, P, tmem);  // whole warp: uniform control flow, one elected lane issues
     }
 #ifdef MT_TIMELINE
     else if (warp == 3 && blockIdx.x == 0) {
@@ -978,7 +997,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
-    softmax_bwd(sm, P, tmem, &tmdq, &tmdk, &tmdv);
+    softmax_bwd<M>(sm, P, tmem, &tmdq, &tmdk, &tmdv);
     if (threadIdx.x % 128 == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
@@ -1138,14 +1157,22 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   const size_t smem = bwd_smem_bytes();
   // set on every launch: the attribute applies to the current device only (a process may
   // drive several GPUs), and the call is cheap next to the launch
-  if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem) != cudaSuccess)
-    return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_bwd) failed");
-  // one launch: BLOCK (slash) tiles and BAR (vertical) tiles share the dynamic tile counter
-  cudaMemsetAsync(P.tile_counter, 0, sizeof(int), st);
+  using KernelFn = void (*)(Params, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                           CUtensorMap, CUtensorMap);
+  KernelFn kernels[2][3] = {{attn_bwd_kernel<0, kOnlyBlock>, attn_bwd_kernel<0, kOnlyBar>,
+                             attn_bwd_kernel<0, kMixed>},
+                            {attn_bwd_kernel<1, kOnlyBlock>, attn_bwd_kernel<1, kOnlyBar>,
+                             attn_bwd_kernel<1, kMixed>}};
+  KernelFn* kl = kernels[plan.layout ? 1 : 0];
+  for (int m = 0; m < 3; ++m)
+    if (cudaFuncSetAttribute(kl[m], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_bwd) failed");
+  // BLOCK (slash) tiles and BAR (vertical) tiles share one dynamic tile counter per launch
+  cudaMemsetAsync(P.tile_counter, 0, 2 * sizeof(int), st);
   const int npairs = (nloc + 1) / 2;
   // fewer heads per BLOCK tile when the launch would otherwise hold too few tiles to fill
-  // the SMs (short sequences / many ring ranks); the bar tiles below are counted too
+  // the SMs (short sequences / many ring ranks)
   while (P.hpt > 1 && (plan.Hq / P.hpt) * npairs < 2 * num_sms) {
     int h2 = P.hpt - 1;
     while (grp % h2) --h2;
@@ -1164,31 +1191,34 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   P.bar_parts = (nloc + P.bar_part_len - 1) / P.bar_part_len;
   P.n_bar = plan.bptr ? 0 : plan.Hq * (int)((S_loc + 127) / 128) * P.bar_parts;
   P.n_tiles = P.n_block + P.n_bar;
-  // BAR tiles first (longest first) up to 2048 local blocks; beyond that their long query
-  // walks evict the BLOCK tiles' shared Q/dO blocks from L2 (measured at 512K, W = 1:
-  // 298 ms bar-first vs 279 ms block-first; at 4K: 0.095 vs 0.116 ms, 128K: 17.8 vs 18.1).
-  // MT_BWD_BAR_FIRST=0/1 overrides.
-  static const int bar_first_env = getenv("MT_BWD_BAR_FIRST") ? atoi(getenv("MT_BWD_BAR_FIRST")) : -1;
-  P.bar_first = bar_first_env >= 0 ? bar_first_env : (nloc <= 2048 ? 1 : 0);
-  static const int split_env = getenv("MT_BWD_SPLIT") ? atoi(getenv("MT_BWD_SPLIT")) : 0;
-  if (split_env && P.n_bar > 0) {  // A/B: BLOCK and BAR tiles as two launches (round 1)
+  // Up to 2048 local blocks: ONE launch with the BAR tiles first (the longest first), so the
+  // tail of one pass overlaps the other (4K: 0.25 -> 0.095 ms, 128K: 17.8 vs 18.1 ms).  Beyond:
+  // a block-only launch, then a bar-only launch; their kernels compile without the other kind's
+  // branches (a mixed kernel measured 4% slower on the 512K block pass, and with the bar tiles
+  // first 298 vs 279 ms).  MT_BWD_SPLIT=0/1 overrides.
+  static const int split_env = getenv("MT_BWD_SPLIT") ? atoi(getenv("MT_BWD_SPLIT")) : -1;
+  const bool split = P.n_bar > 0 && (split_env >= 0 ? split_env != 0 : nloc > 2048);
+  if (split) {
     Params Pb = P, Pv = P;
     Pb.n_bar = 0;
     Pb.n_tiles = P.n_block;
     Pv.n_block = 0;
     Pv.n_tiles = P.n_bar;
     Pv.tile_counter = plan.scratch + 3;
-    cudaMemsetAsync(Pv.tile_counter, 0, sizeof(int), st);
     const int gb = Pb.n_tiles < num_sms ? Pb.n_tiles : num_sms;
-    if (gb > 0)
-      attn_bwd_kernel<<<gb, kThreads, smem, st>>>(Pb, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+    if (gb > 0) kl[kOnlyBlock]<<<gb, kThreads, smem, st>>>(Pb, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
     MT_TRY(check_launch("attn_bwd_kernel(block)"));
-    attn_bwd_kernel<<<num_sms, kThreads, smem, st>>>(Pv, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+    kl[kOnlyBar]<<<num_sms, kThreads, smem, st>>>(Pv, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
     return check_launch("attn_bwd_kernel(bar)");
   }
+  P.bar_first = 1;
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
-  if (grid > 0)
-    attn_bwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+  if (grid > 0) {
+    if (P.n_bar > 0)
+      kl[kMixed]<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+    else  // block-CSR mode: block tiles only
+      kl[kOnlyBlock]<<<grid, kThreads, smem, st>>>(P, tmq, tmdo, tmk, tmv, tmdq, tmdk, tmdv);
+  }
   return check_launch("attn_bwd_kernel");
 }
 

@@ -971,6 +971,8 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
   }
 }
 
+// one instantiation per sequence layout (each carries only its own K-producer walk)
+template <int L>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
@@ -1030,10 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
     if (warp == 0) {
-      if (P.plan.layout)
-        producer_k<1>(sm, P, &tmq, &tmk, &tmkp);
-      else
-        producer_k<0>(sm, P, &tmq, &tmk, &tmkp);
+      producer_k<L>(sm, P, &tmq, &tmk, &tmkp);
     } else if (warp == 2) {
       producer_v(sm, P, &tmv, &tmvp);
     } else if (warp == 1) {
@@ -1238,12 +1237,13 @@ mt_status attn_fwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   }
   const size_t smem = fwd_smem_bytes();
   // set on every launch: the attribute applies to the current device only
-  if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem) != cudaSuccess)
+  auto kernel = plan.layout ? attn_fwd_kernel<1> : attn_fwd_kernel<0>;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
     return fail(MT_ECUDA, "cudaFuncSetAttribute(attn_fwd) failed (smem %zu)", smem);
   const int grid = P.n_tiles < num_sms ? P.n_tiles : num_sms;
   cudaMemsetAsync(P.fix_count, 0, 2 * sizeof(int), st);  // fix-up count, tile counter
-  if (grid > 0) attn_fwd_kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv, tmkp, tmvp);
+  if (grid > 0) kernel<<<grid, kThreads, smem, st>>>(P, tmq, tmk, tmv, tmkp, tmvp);
   MT_TRY(check_launch("attn_fwd_kernel"));
   attn_fwd_fixup<<<num_sms, 256, 0, st>>>(P, static_cast<const __nv_bfloat16*>(q));
   return check_launch("attn_fwd_fixup");
