@@ -449,7 +449,8 @@ def run_ours(args):
     fl_fwd = 4 * 128 * pairs / W
     t_bwd, t_fwd = ph[2] / 1e3, ph[1] / 1e3
     ach = fl_bwd / t_bwd / 1e12
-    roof = {"bound": "tensor", "kernel": "attn_bwd (one launch: slash + vertical tiles, per-rank)",
+    roof = {"bound": "tensor", "kernel": ("attn_bwd per rank and ring step: slash-block launch + vertical-bar launch "
+                                          "when nloc > 2048 blocks, else one mixed launch"),
             "achieved": round(ach, 1), "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
             "frac": round(ach / pk["bf16_tflops_sustained"], 4),
             "peak_source": f"{pk_src} bf16 cuBLAS sustained (burst {pk['bf16_tflops']})",
