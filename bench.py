@@ -254,7 +254,9 @@ def run_ours(args):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    def step(qx, kx, vx, dox, marks=None):
+    def step(qx, kx, vx, dox, marks=None, mid=None):
+        """index + forward + backward; mid() (if given) runs between the forward and the
+        backward (the e2e loop queues its host copies there)."""
         e = [ev() for _ in range(4)] if marks is not None else None
         if e: e[0].record(stream)
         idx = ops.build_vs_index(qx, kx, p, p, comm=comm, seq_len=S, layout=lay)
@@ -264,6 +266,8 @@ def run_ours(args):
         else:
             o, lse = ops.ring_attn_fwd(comm, S, qx, kx, vx, idx, layout=lay)
         if e: e[2].record(stream)
+        if mid is not None:
+            mid()
         if comm is None:
             g = ops.sparse_attn_bwd(qx, kx, vx, o, lse, dox, idx)
         else:
@@ -353,10 +357,15 @@ def run_ours(args):
 
     # ---- end to end through the public API with host buffers.  Every step's inputs
     # are copied host->device from pinned memory and its dQ/dK/dV device->host inside
-    # the timed region; copies run on their own streams, double-buffered, so step
-    # i+1's upload and step i-1's download overlap step i's kernels.
+    # the timed region; copies run on their own streams, double-buffered.  They are queued
+    # behind each step's forward, so they run during its backward: step i+1's upload and
+    # step i-1's download overlap step i's backward, and the copy engines stay free for
+    # the forward ring's KV transfers (a 600 MB host copy queued ahead of a ring transfer
+    # on the same engine stalls the ring).  MT_BENCH_E2E_EARLY=1: the previous schedule
+    # (uploads queued at the start of the step, downloads at its end).
     e2e = None
     if not args.no_e2e:
+        early = os.environ.get("MT_BENCH_E2E_EARLY", "0") == "1"
         pin = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
                for x in (hq_, hk_, hv_, hdo)]
         h2d = sum(x.numel() * 2 for x in pin)
@@ -373,9 +382,9 @@ def run_ours(args):
         a, b = ev(), ev()
         a.record(stream)
 
-        def upload(i):
+        def upload(i, after):
             bb = i % 2
-            cin.wait_event(a)
+            cin.wait_event(after)
             if i >= 2:
                 cin.wait_event(ev_done[bb])  # step i-2 finished reading this buffer
             with torch.cuda.stream(cin):
@@ -383,21 +392,37 @@ def run_ours(args):
                     d_.copy_(h_, non_blocking=True)
             ev_in[bb].record(cin)
 
-        upload(0)
+        def download(i, after):
+            bb = i % 2
+            cout.wait_event(after)
+            with torch.cuda.stream(cout):
+                for hy, y in zip(host_out[bb], keep[bb]):
+                    hy.copy_(y, non_blocking=True)
+                    y.record_stream(cout)
+
+        upload(0, a)
         d2h = 0
         for i in range(args.steps):
             bb = i % 2
-            if i + 1 < args.steps:
-                upload(i + 1)
+            if early and i + 1 < args.steps:
+                upload(i + 1, a)
             stream.wait_event(ev_in[bb])
-            _, g = step(*dbuf[bb])
+
+            def mid(i=i):
+                if early:
+                    return
+                fwd_done = torch.cuda.Event()
+                fwd_done.record(stream)
+                if i + 1 < args.steps:
+                    upload(i + 1, fwd_done)
+                if i >= 1:
+                    download(i - 1, fwd_done)
+
+            _, g = step(*dbuf[bb], mid=mid)
             ev_done[bb].record(stream)
-            cout.wait_event(ev_done[bb])
-            with torch.cuda.stream(cout):
-                for hy, y in zip(host_out[bb], g):
-                    hy.copy_(y, non_blocking=True)
-                    y.record_stream(cout)
             keep[bb] = g
+            if early or i == args.steps - 1:
+                download(i, ev_done[bb])
             d2h = sum(y.numel() * y.element_size() for y in g)
         stream.wait_stream(cout)
         b.record(stream)
@@ -408,7 +433,10 @@ def run_ours(args):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": S * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "copies": "pinned host <-> device on two copy streams, double-buffered across steps"}
+               "copies": ("pinned host <-> device on two copy streams, double-buffered; queued at the start / end "
+                             "of each step" if early else
+                             "pinned host <-> device on two copy streams, double-buffered; step i+1's "
+                             "upload and step i-1's download run during step i's backward")}
 
     # ---- ring step profile: one extra, untimed step with CUDA events
     # around each step's kernels and transfers (rank 0's view)
