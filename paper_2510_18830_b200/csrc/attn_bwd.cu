@@ -508,6 +508,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     uint32_t k = 0, g = 0;  // tile-local: chunks whose S^T issued / gradients issued
     // per region: stage / producer seq of its pending chunk (scalars: no local memory)
     uint32_t pst0 = 0, pst1 = 0, end_stage = 0;
+    uint32_t plv0 = 3, plv1 = 3;  // live 64-key slots (bit 0 / 1) of the pending chunk
     int pseq0 = 0, pseq1 = 0, end_tile = 0;
     auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
     auto try_grads = [&]() {  // gradient MMAs of chunk g (softmax warpgroup g & 1)
@@ -531,9 +532,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
           mma_ts(tmem + kColDV, R + kq / 2, sdesc_add(dom, kq * 128), id_kv, acc);
           mma_ts(tmem + kColDK, R + 32 + kq / 2, sdesc_add(dqm, kq * 128), id_kv, acc);
         }
+        // dQ^T = K^T dS^T contracts over the tile's 128 keys: a dead 64-key slot (its dS^T
+        // rows are zero) is skipped, 4 of the 8 K-steps (0.86 of the 512K bench chunks have
+        // exactly one live slot)
+        const uint32_t lv = bg ? plv1 : plv0;
+        const int k0 = (lv & 1u) ? 0 : 64, k1 = (lv & 2u) ? 128 : 64;
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16)
-          mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > 0);
+          if (kk >= k0 && kk < k1)
+            mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > k0);
         mma_commit(smem_u32(&sm.gdone[bg]));
         mma_commit(smem_u32(&sm.empty[st]));
         MT_TL(3, bg ? pseq1 : pseq0);
@@ -576,11 +583,15 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
         mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
         MT_TL(2, sm.meta[stage].seq);
       }
+      uint32_t lv = (is_block<M>(sm.meta[stage].mode) && !(P.dbg & 128)) ? (sm.meta[stage].flags & 3u) : 3u;
+      lv = lv ? lv : 3u;
       if (b) {
+        plv1 = lv;
         pst1 = stage;
         pseq1 = sm.meta[stage].seq;
         ++sq1;
       } else {
+        plv0 = lv;
         pst0 = stage;
         pseq0 = sm.meta[stage].seq;
         ++sq0;
@@ -816,6 +827,14 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         nd[row - 64] = -nd[row - 64] * P.inv_sqrt_d;
       named_bar_sync(wg_bar, 128);
       uint32_t pk[32], dk[32];
+      // a key row no query of the chunk sees contributes P = dS = 0.  In BLOCK mode a dead
+      // 64-key slot is two whole warps (slot = row / 64): they skip the TMEM loads and the
+      // exponentials (0.43 of the slot-rows of the 512K bench index) and
+      // leave the MUFU / FMA pipes of their SM sub-partitions to the other warpgroup.
+      if (!(P.dbg & 64) && __all_sync(0xffffffffu, vis == 0ull)) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) pk[c] = dk[c] = 0u;
+      } else
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // 32 queries at a time (register budget)
         uint32_t sv[32], dpv[32];
