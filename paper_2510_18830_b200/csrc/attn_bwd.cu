@@ -831,23 +831,28 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       // 64-key slot is two whole warps (slot = row / 64): they skip the TMEM loads and the
       // exponentials (0.43 of the slot-rows of the 512K bench index) and
       // leave the MUFU / FMA pipes of their SM sub-partitions to the other warpgroup.
-      if (!(P.dbg & 64) && __all_sync(0xffffffffu, vis == 0ull)) {
+      const bool dead = !(P.dbg & 64) && __all_sync(0xffffffffu, vis == 0ull);
+      if (dead) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) pk[c] = dk[c] = 0u;
-      } else
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // 32 queries at a time (register budget)
-        uint32_t sv[32], dpv[32];
-        tmem_ld32(R + 32 * hf, sv);
-        tmem_ld32(R + 64 + 32 * hf, dpv);
+      } else {
+        // all 64 queries' S^T and dP^T in one round of TMEM loads (one load latency per chunk)
+        uint32_t sv[2][32], dpv[2][32];
+        tmem_ld32(R, sv[0]);
+        tmem_ld32(R + 64, dpv[0]);
+        tmem_ld32(R + 32, sv[1]);
+        tmem_ld32(R + 96, dpv[1]);
         tmem_ld_wait();
-        const uint32_t vh = (uint32_t)(vis >> (32 * hf));
-        if (vh == 0xffffffffu)
-          softmax_half<false>(sv, dpv, nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
-                              pk + 16 * hf, dk + 16 * hf);
-        else
-          softmax_half<true>(sv, dpv, nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
-                             pk + 16 * hf, dk + 16 * hf);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t vh = (uint32_t)(vis >> (32 * hf));
+          if (vh == 0xffffffffu)
+            softmax_half<false>(sv[hf], dpv[hf], nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
+                                pk + 16 * hf, dk + 16 * hf);
+          else
+            softmax_half<true>(sv[hf], dpv[hf], nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
+                               pk + 16 * hf, dk + 16 * hf);
+        }
       }
       // P^T, dS^T over S^T in this warpgroup's TMEM region (A of dV, dK)
 #ifdef MT_TL_WGSPLIT
@@ -859,6 +864,8 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
 #ifdef MT_TL_WGSPLIT
       if (row == 0) MT_TL(7, cm.seq);  // staging buffer free
 #endif
+      // dS^T rows of a dead BLOCK slot are not read: dQ^T skips that slot's K-steps
+      if (!(dead && is_block<M>(cm.mode) && !(P.dbg & 128)))
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) {
         const uint32_t sw = (uint32_t)((c16 ^ (row & 7)) << 4);

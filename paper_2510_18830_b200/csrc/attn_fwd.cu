@@ -824,10 +824,14 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
 #pragma unroll 1
       for (int cg = 0; cg < ((P.dbg & 1) ? 0 : 4); ++cg) {  // MT_FWD_DBG=1: no softmax (timing only)
         uint32_t sv[32], pk[16];
-        tmem_ld32(Sb + 32 * cg, sv);
-        tmem_ld_wait();
         const uint32_t lv = live_bits(cm, x, qi, cg);
         any_live |= lv != 0u;
+        // a 32-key group no row of the warp sees (a head of the pair without this slash
+        // block: ~1/3 of the rows on the bench index) needs no TMEM load
+        if (!__all_sync(0xffffffffu, lv == 0u || m == -INFINITY)) {
+          tmem_ld32(Sb + 32 * cg, sv);
+          tmem_ld_wait();
+        }
         if (lv == ~0u && m != -INFINITY) {
           // every key live (the common case): FFMA + MUFU + max + add per key
           float la = 0.f, lb2 = 0.f;

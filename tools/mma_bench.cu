@@ -82,6 +82,14 @@ __global__ void __launch_bounds__(128, 1) bench(int variant, int reps, long long
           for (int kk = 0; kk < 128; kk += 16)
             mma_ts(tmem + 256, tmem + 448 + kk / 2, sdesc_add(dq, (kk >> 6) * 8192 + (kk & 63) * 2), id_s, kk > 0);
         }
+        if (variant == 9) {  // S^T + dP^T at M = 64 (one live 64-key slot), N = 64
+#pragma unroll
+          for (int kk = 0; kk < 128; kk += 16) {
+            const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2, qo = (kk >> 6) * 8192 + (kk & 63) * 2;
+            mma_ss(tmem + 256, sdesc_add(dK, ko), sdesc_add(dq, qo), make_idesc_bf16(64, 64, false, false), kk > 0);
+            mma_ss(tmem + 320, sdesc_add(dV, ko), sdesc_add(ddo, qo), make_idesc_bf16(64, 64, false, false), kk > 0);
+          }
+        }
         if (variant == 4) {  // S^T only, K-major B but N=128 (two query blocks)
 #pragma unroll
           for (int kk = 0; kk < 128; kk += 16) {
@@ -109,11 +117,12 @@ int main() {
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   const char* names[] = {"S^T+dP^T (16x M128N64 KK)", "dV+dK (8x M128N128 K/MN)", "dQ^T (8x M128N64 MN/MN)",
                          "all per chunk (32 MMAs)", "S^T-like N128 KK (8x)", "dV+dK .ts (8x M128N128)",
-                         "chunk: SS S/dP/dQ + ts dV/dK", "issue: 32x M128N8", "S^T .ts A=K (8x N64)"};
+                         "chunk: SS S/dP/dQ + ts dV/dK", "issue: 32x M128N8", "S^T .ts A=K (8x N64)",
+                         "S^T+dP^T M64 (16x M64N64 KK)"};
   const double ideal[] = {16 * 32, 8 * 64, 8 * 32, 16 * 32 + 8 * 64 + 8 * 32, 8 * 64, 8 * 64,
-                          24 * 32 + 8 * 64, 32 * 4, 8 * 32};
+                          24 * 32 + 8 * 64, 32 * 4, 8 * 32, 16 * 32};
   for (int grid : {1, 148}) {
-    for (int v = 0; v < 9; ++v) {
+    for (int v = 0; v < 10; ++v) {
       const int reps = 2000;
       bench<<<grid, 128, 140 * 1024>>>(v, reps, d);
       long long h[148];
