@@ -1221,9 +1221,10 @@ mt_status attn_bwd_step(const VSPlan& plan, int r, int s, int nloc, const void* 
   // tail of one pass overlaps the other (4K: 0.25 -> 0.095 ms, 128K: 17.8 vs 18.1 ms).  Beyond:
   // a block-only launch, then a bar-only launch; their kernels compile without the other kind's
   // branches (a mixed kernel measured 4% slower on the 512K block pass, and with the bar tiles
-  // first 298 vs 279 ms).  MT_BWD_SPLIT=0/1 overrides.
+  // first 298 vs 279 ms).  Ring steps (W > 1) split from 2048 local blocks on: 512K on 4 GPUs,
+  // 74.1 -> 72.1 ms per backward (profiles/r02d_split4/).  MT_BWD_SPLIT=0/1 overrides.
   static const int split_env = getenv("MT_BWD_SPLIT") ? atoi(getenv("MT_BWD_SPLIT")) : -1;
-  const bool split = P.n_bar > 0 && (split_env >= 0 ? split_env != 0 : nloc > 2048);
+  const bool split = P.n_bar > 0 && (split_env >= 0 ? split_env != 0 : (nloc > 2048 || (plan.W > 1 && nloc >= 2048)));
   if (split) {
     Params Pb = P, Pv = P;
     Pb.n_bar = 0;
