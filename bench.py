@@ -361,11 +361,13 @@ def run_ours(args):
     # behind each step's forward, so they run during its backward: step i+1's upload and
     # step i-1's download overlap step i's backward, and the copy engines stay free for
     # the forward ring's KV transfers (a 600 MB host copy queued ahead of a ring transfer
-    # on the same engine stalls the ring).  MT_BENCH_E2E_EARLY=1: the previous schedule
-    # (uploads queued at the start of the step, downloads at its end).
+    # on the same engine stalls the ring).  MT_BENCH_E2E_EARLY=1 (the default on one GPU):
+    # uploads queued at the start of the step, downloads at its end.
     e2e = None
     if not args.no_e2e:
-        early = os.environ.get("MT_BENCH_E2E_EARLY", "0") == "1"
+        # one GPU (no ring): the upload of step i+1 starts with step i (at C1's 0.22 ms steps a
+        # copy queued behind the forward delays the next step: e2e 6.2 vs 2.8 M tokens/s)
+        early = os.environ.get("MT_BENCH_E2E_EARLY", "1" if W == 1 else "0") == "1"
         pin = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
                for x in (hq_, hk_, hv_, hdo)]
         h2d = sum(x.numel() * 2 for x in pin)
