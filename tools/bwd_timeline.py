@@ -52,8 +52,8 @@ if "--wgsplit" in sys.argv:  # MT_TL_WGSPLIT: 6 = math done, 7 = staging buffer 
 if "--issuer" in sys.argv:
     for n, (a, b) in {"publish -> G waits pass": (5, 6), "G waits pass -> G issued": (6, 3),
                       "S waits pass -> S issued": (7, 2), "data in smem -> S waits pass": (1, 7),
-                      "S issued(k) -> S waits pass(k+1)": None}.items():
-        if (a, b) is None or n.startswith("S issued(k)"):
+                      "S issued(k) -> S waits pass(k+1)": (0, 0)}.items():
+        if n.startswith("S issued(k)"):
             d = E[7][1:] - E[2][:-1]
         else:  # noqa
             d = E[b] - E[a]
