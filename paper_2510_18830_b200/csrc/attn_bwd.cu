@@ -58,6 +58,11 @@ namespace bwd {
 // halves.  3 (-DMT_BWD_STAGES=3) gives each a 32 KB buffer and ONE bulk reduce-add per
 // chunk, but measured slower (296 vs 278 ms at 512K: the loads starve with 3 stages).
 constexpr int kStages = MT_BWD_STAGES;
+#ifndef MT_BWD_SPLIT_SDP
+#define MT_BWD_SPLIT_SDP 1  // S^T committed before dP^T is issued (P^T overlaps the dP^T MMAs)
+#endif
+// (Issuing dV += P^T dO as soon as P^T was in TMEM, ahead of dS^T, measured 258.6 vs 249.5 ms
+// at 512K: the extra MMA group in the in-order tensor pipe delays the other region's S^T.)
 constexpr int kThreads = 384;   // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-2: softmax
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB (128 keys x d)
 constexpr uint32_t kTileQ = 64 * 128 * 2;    // 16 KB (64 queries x d)
@@ -102,6 +107,7 @@ struct Smem {
   uint64_t full[kStages], empty[kStages];
   uint64_t kvfull, kvempty, tfree;
   uint64_t sfull[2], dsfull[2], gdone[2], dqfree[2];  // dqfree: region drained
+  uint64_t dpfull[2];  // dP^T landed (MMA commit; S^T lands first, on sfull)
   uint32_t tmem_base;
 };
 
@@ -511,7 +517,7 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
     uint32_t plv0 = 3, plv1 = 3;  // live 64-key slots (bit 0 / 1) of the pending chunk
     int pseq0 = 0, pseq1 = 0, end_tile = 0;
     auto uni = [](bool x) { return __shfl_sync(0xffffffffu, x ? 1 : 0, 0) != 0; };
-    auto try_grads = [&]() {  // gradient MMAs of chunk g (softmax warpgroup g & 1)
+    auto try_grads = [&]() {  // dK, dQ^T of chunk g (softmax warpgroup g & 1)
       const uint32_t bg = g & 1;
       uint32_t& ds = bg ? ds1 : ds0;
       if (!uni(mbar_test_wait(smem_u32(&sm.dsfull[bg]), ds & 1))) return false;
@@ -578,9 +584,17 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
           const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
           const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
           mma_ss(R, sdesc_add(dK, ko), sdesc_add(dq, qo), id_s, kk > 0);
+          if (!MT_BWD_SPLIT_SDP) mma_ss(R + 64, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
+        }
+        mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T ready (P^T starts on it)
+        if (MT_BWD_SPLIT_SDP)
+#pragma unroll
+        for (int kk = 0; kk < 128; kk += 16) {
+          const uint32_t ko = (kk >> 6) * 16384 + (kk & 63) * 2;
+          const uint32_t qo = (kk >> 6) * 8192 + (kk & 63) * 2;
           mma_ss(R + 64, sdesc_add(dV, ko), sdesc_add(ddo, qo), id_s, kk > 0);
         }
-        mma_commit(smem_u32(&sm.sfull[b]));  // 2 of 2: S^T, dP^T ready
+        mma_commit(smem_u32(&sm.dpfull[b]));  // dP^T ready
         MT_TL(2, sm.meta[stage].seq);
       }
       uint32_t lv = (is_block<M>(sm.meta[stage].mode) && !(P.dbg & 128)) ? (sm.meta[stage].flags & 3u) : 3u;
@@ -638,40 +652,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 32 queries of one key row: P = exp2(S log2e/sqrt d - LSE log2e), dS = P (dP - D)/sqrt d,
-// packed to bf16 pairs.  nl[q] = -LSE_q log2e, nd[q] = -D_q/sqrt d (pre-scaled per
-// chunk).  kMasked: queries whose bit in `vis` is clear get P = dS = 0.
-template <bool kMasked>
-__device__ __forceinline__ void softmax_half(const uint32_t (&sv)[32], const uint32_t (&dpv)[32],
-                                             const float* nl, const float* nd, float scale_log2,
-                                             float inv_sqrt_d, uint32_t vis, uint32_t* pk,
-                                             uint32_t* dk) {
-#pragma unroll
-  for (int c = 0; c < 32; c += 4) {
-    const float4 l4 = *reinterpret_cast<const float4*>(nl + c);
-    const float4 d4 = *reinterpret_cast<const float4*>(nd + c);
-    const float la[4] = {l4.x, l4.y, l4.z, l4.w};
-    const float da[4] = {d4.x, d4.y, d4.z, d4.w};
-    float p[4], ds[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = c + u;
-      // (ex2_poly for a quarter of these measured no gain here: MUFU is not this kernel's bound)
-      p[u] = ex2(fmaf(__uint_as_float(sv[q]), scale_log2, la[u]));
-      ds[u] = p[u] * fmaf(__uint_as_float(dpv[q]), inv_sqrt_d, da[u]);
-      if (kMasked) {
-        const bool on = (vis >> q) & 1u;
-        p[u] = on ? p[u] : 0.f;
-        ds[u] = on ? ds[u] : 0.f;
-      }
-    }
-    pk[c >> 1] = pack_bf16x2(p[0], p[1]);
-    pk[(c >> 1) + 1] = pack_bf16x2(p[2], p[3]);
-    dk[c >> 1] = pack_bf16x2(ds[0], ds[1]);
-    dk[(c >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
-  }
-}
-
 template <int M>
 __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUtensorMap* tmdq,
                             const CUtensorMap* tmdk, const CUtensorMap* tmdv) {
@@ -682,15 +662,15 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   const int slot = row >> 6, kk = row & 63;
   const uint32_t lb = (uint32_t)(quad * 32) << 16;
   const VSPlan& pl = P.plan;
-  const int W = pl.W;
   const uint32_t sfull = smem_u32(&sm.sfull[wg]);
   const uint32_t R = tmem + lb + kColR + 128 * wg;  // this warpgroup's TMEM region (own lanes)
   const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
+  const uint32_t dpfull = smem_u32(&sm.dpfull[wg]);
   const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
   const uint32_t pdbuf = smem_u32(sm.pd[wg]);
   const uint32_t drow = pdbuf + row * 128;  // dS^T row in SMEM (B of dQ^T)
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
-  uint32_t su = 0, gw = 0;  // sfull events, gdone waits
+  uint32_t su = 0, gw = 0, dpu = 0;  // sfull events, gdone waits, dP^T chunks
   uint32_t ntile = 0;
   const int nbar = bar_tile_count<M>(P);
   bool staging_busy = false;  // a bulk reduce may still be reading this warpgroup's buffer
@@ -826,39 +806,57 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
       else
         nd[row - 64] = -nd[row - 64] * P.inv_sqrt_d;
       named_bar_sync(wg_bar, 128);
-      uint32_t pk[32], dk[32];
       // a key row no query of the chunk sees contributes P = dS = 0.  In BLOCK mode a dead
       // 64-key slot is two whole warps (slot = row / 64): they skip the TMEM loads and the
       // exponentials (0.43 of the slot-rows of the 512K bench index) and
       // leave the MUFU / FMA pipes of their SM sub-partitions to the other warpgroup.
       const bool dead = !(P.dbg & 64) && __all_sync(0xffffffffu, vis == 0ull);
+      // phase 1: P^T = exp2(S^T log2e/sqrt d - LSE log2e) while the dP^T MMAs still run;
+      // P^T (bf16 pairs) over S^T columns 0-31
+      float p[64];
+      uint32_t pk[32];
       if (dead) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = dk[c] = 0u;
+        for (int c = 0; c < 64; ++c) p[c] = 0.f;
       } else {
-        // all 64 queries' S^T and dP^T in one round of TMEM loads (one load latency per chunk)
-        uint32_t sv[2][32], dpv[2][32];
+        uint32_t sv[2][32];
         tmem_ld32(R, sv[0]);
-        tmem_ld32(R + 64, dpv[0]);
         tmem_ld32(R + 32, sv[1]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const float e = ex2(fmaf(__uint_as_float(sv[q >> 5][q & 31]), P.scale_log2, nl[q]));
+          p[q] = ((vis >> q) & 1ull) ? e : 0.f;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) pk[c] = pack_bf16x2(p[2 * c], p[2 * c + 1]);
+      tmem_st32(R, pk);
+      // phase 2: dS^T = P^T o (dP^T - D) / sqrt d (pre-scaled D) once dP^T has landed
+      uint32_t dk[32];
+      if (dead) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dk[c] = 0u;
+      } else {
+        mbar_wait(dpfull, dpu & 1);
+        tc_fence_after();
+        uint32_t dpv[2][32];
+        tmem_ld32(R + 64, dpv[0]);
         tmem_ld32(R + 96, dpv[1]);
         tmem_ld_wait();
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const uint32_t vh = (uint32_t)(vis >> (32 * hf));
-          if (vh == 0xffffffffu)
-            softmax_half<false>(sv[hf], dpv[hf], nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
-                                pk + 16 * hf, dk + 16 * hf);
-          else
-            softmax_half<true>(sv[hf], dpv[hf], nl + 32 * hf, nd + 32 * hf, P.scale_log2, P.inv_sqrt_d, vh,
-                               pk + 16 * hf, dk + 16 * hf);
+        for (int c = 0; c < 32; ++c) {
+          const int q = 2 * c;
+          const float d0 = p[q] * fmaf(__uint_as_float(dpv[q >> 5][q & 31]), P.inv_sqrt_d, nd[q]);
+          const float d1 = p[q + 1] * fmaf(__uint_as_float(dpv[(q + 1) >> 5][(q + 1) & 31]), P.inv_sqrt_d, nd[q + 1]);
+          dk[c] = pack_bf16x2(d0, d1);
         }
       }
-      // P^T, dS^T over S^T in this warpgroup's TMEM region (A of dV, dK)
+      ++dpu;
+      // dS^T over S^T columns 32-63 in this warpgroup's TMEM region (A of dK)
 #ifdef MT_TL_WGSPLIT
       if (row == 0) MT_TL(6, cm.seq);  // math done
 #endif
-      tmem_st32(R, pk);
       tmem_st32(R + 32, dk);
       wait_staging();  // the previous chunk's dQ reduce has read the buffer
 #ifdef MT_TL_WGSPLIT
@@ -989,6 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&sm.dsfull[b]), 128);
       mbar_init(smem_u32(&sm.gdone[b]), 1);
       mbar_init(smem_u32(&sm.dqfree[b]), 128);
+      mbar_init(smem_u32(&sm.dpfull[b]), 1);
     }
     fence_barrier_init();
   }
