@@ -107,6 +107,7 @@ struct Smem {
   uint64_t full[kStages], empty[kStages];
   uint64_t kvfull, kvempty, tfree;
   uint64_t sfull[2], dsfull[2], gdone[2], dqfree[2];  // dqfree: region drained
+  uint64_t dqdone[2];  // dQ^T complete (committed before dV / dK: the drain overlaps them)
   uint64_t dpfull[2];  // dP^T landed (MMA commit; S^T lands first, on sfull)
   uint32_t tmem_base;
 };
@@ -532,21 +533,23 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       const uint64_t dstm = sdesc_add(dDSTmn0, bg * kTilePD);
       const uint32_t R = tmem + kColR + 128 * bg;
       if (leader) {
-#pragma unroll
-        for (int kq = 0; kq < 64; kq += 16) {  // A = P^T / dS^T from TMEM (2 bf16 per column)
-          const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
-          mma_ts(tmem + kColDV, R + kq / 2, sdesc_add(dom, kq * 128), id_kv, acc);
-          mma_ts(tmem + kColDK, R + 32 + kq / 2, sdesc_add(dqm, kq * 128), id_kv, acc);
-        }
-        // dQ^T = K^T dS^T contracts over the tile's 128 keys: a dead 64-key slot (its dS^T
-        // rows are zero) is skipped, 4 of the 8 K-steps (0.86 of the 512K bench chunks have
-        // exactly one live slot)
+        // dQ^T = K^T dS^T first, with its own commit, so the warpgroup drains it while dV / dK
+        // run.  It contracts over the tile's 128 keys: a dead 64-key slot (its dS^T rows are
+        // zero) is skipped, 4 of the 8 K-steps (0.86 of the 512K bench chunks have exactly one
+        // live slot)
         const uint32_t lv = bg ? plv1 : plv0;
         const int k0 = (lv & 1u) ? 0 : 64, k1 = (lv & 2u) ? 128 : 64;
 #pragma unroll
         for (int kk = 0; kk < 128; kk += 16)
           if (kk >= k0 && kk < k1)
             mma_ss(R + 64, sdesc_add(dKmn, kk * 128), sdesc_add(dstm, kk * 128), id_q, kk > k0);
+        mma_commit(smem_u32(&sm.dqdone[bg]));
+#pragma unroll
+        for (int kq = 0; kq < 64; kq += 16) {  // A = P^T / dS^T from TMEM (2 bf16 per column)
+          const uint32_t acc = (acc_started || kq > 0) ? 1u : 0u;
+          mma_ts(tmem + kColDV, R + kq / 2, sdesc_add(dom, kq * 128), id_kv, acc);
+          mma_ts(tmem + kColDK, R + 32 + kq / 2, sdesc_add(dqm, kq * 128), id_kv, acc);
+        }
         mma_commit(smem_u32(&sm.gdone[bg]));
         mma_commit(smem_u32(&sm.empty[st]));
         MT_TL(3, bg ? pseq1 : pseq0);
@@ -569,6 +572,9 @@ __device__ void mma_issuer(Smem& sm, const Params& P, uint32_t tmem) {
       // region b is free once the chunk it held two chunks ago was drained
       const uint32_t nsq = b ? sq1 : sq0;
       if (nsq > 0 && !uni(mbar_test_wait(smem_u32(&sm.dqfree[b]), (nsq - 1) & 1)))
+        return false;
+      // ... and its dV / dK MMAs (readers of P^T / dS^T in the region) are complete
+      if (nsq > 0 && !uni(mbar_test_wait(smem_u32(&sm.gdone[b]), (nsq - 1) & 1)))
         return false;
 #ifdef MT_TL_ISSUER
       if (leader) MT_TL(7, sm.meta[stage].seq);
@@ -665,12 +671,13 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   const uint32_t sfull = smem_u32(&sm.sfull[wg]);
   const uint32_t R = tmem + lb + kColR + 128 * wg;  // this warpgroup's TMEM region (own lanes)
   const uint32_t dsfull = smem_u32(&sm.dsfull[wg]), gdone = smem_u32(&sm.gdone[wg]);
+  const uint32_t dqdone = smem_u32(&sm.dqdone[wg]);
   const uint32_t dpfull = smem_u32(&sm.dpfull[wg]);
   const uint32_t dqfree = smem_u32(&sm.dqfree[wg]);
   const uint32_t pdbuf = smem_u32(sm.pd[wg]);
   const uint32_t drow = pdbuf + row * 128;  // dS^T row in SMEM (B of dQ^T)
   const uint32_t wg_bar = 1 + wg;  // named barrier of this warpgroup
-  uint32_t su = 0, gw = 0, dpu = 0;  // sfull events, gdone waits, dP^T chunks
+  uint32_t su = 0, gw = 0, dpu = 0;  // sfull events, dqdone waits (= chunks), dP^T chunks
   uint32_t ntile = 0;
   const int nbar = bar_tile_count<M>(P);
   bool staging_busy = false;  // a bulk reduce may still be reading this warpgroup's buffer
@@ -688,7 +695,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
   // rewritten (next P/dS^T or the epilogue).
   auto drain_dq = [&](int h, int j, int seq) {
     if (row == 0) MT_CRUMB(3 + wg, 2000000 + (int)gw);
-    mbar_wait(gdone, gw & 1);  // gradient MMAs done: P/dS^T free, dQ^T complete
+    mbar_wait(dqdone, gw & 1);  // dQ^T complete (dS^T in SMEM read; dV / dK may still run)
     ++gw;
 #if !defined(MT_TL_WARPS) && !defined(MT_TL_ISSUER) && !defined(MT_TL_WGSPLIT)
     if (row == 0) MT_TL(6, seq);
@@ -886,6 +893,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
     if (tile < 0) break;  // DONE
     const Tile T = decode_tile<M>(P, tile, nbar);
     wait_staging();  // the epilogue stages dK/dV in the same buffer
+    if (gw > 0) mbar_wait(gdone, (gw - 1) & 1);  // this warpgroup's last dV / dK MMAs
     tc_fence_after();
     if (row == 0) sm.tile_chunks[wg] = had_chunk ? 1 : 0;
     if (row == 0) MT_CRUMB(3 + wg, 5000000 + (int)ntile);
@@ -986,6 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&sm.sfull[b]), 2);
       mbar_init(smem_u32(&sm.dsfull[b]), 128);
       mbar_init(smem_u32(&sm.gdone[b]), 1);
+      mbar_init(smem_u32(&sm.dqdone[b]), 1);
       mbar_init(smem_u32(&sm.dqfree[b]), 128);
       mbar_init(smem_u32(&sm.dpfull[b]), 1);
     }
