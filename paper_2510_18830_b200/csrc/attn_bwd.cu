@@ -652,6 +652,26 @@ __device__ __forceinline__ void red_add_f32x4(float* addr, const uint32_t* v) {
 }
 
 
+// packed fp32 pair arithmetic (FFMA2 / FMUL2 on sm_100): two IEEE round-to-nearest results
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -830,10 +850,25 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         tmem_ld32(R, sv[0]);
         tmem_ld32(R + 32, sv[1]);
         tmem_ld_wait();
+        const float2 sc2 = make_float2(P.scale_log2, P.scale_log2);
+        if (vis == ~0ull) {  // every query sees the row (the common case)
 #pragma unroll
-        for (int q = 0; q < 64; ++q) {
-          const float e = ex2(fmaf(__uint_as_float(sv[q >> 5][q & 31]), P.scale_log2, nl[q]));
-          p[q] = ((vis >> q) & 1ull) ? e : 0.f;
+          for (int q = 0; q < 64; q += 2) {
+            const float2 t = ffma2(make_float2(__uint_as_float(sv[q >> 5][q & 31]),
+                                               __uint_as_float(sv[q >> 5][(q & 31) + 1])),
+                                   sc2, *reinterpret_cast<const float2*>(nl + q));
+            p[q] = ex2(t.x);
+            p[q + 1] = ex2(t.y);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 64; q += 2) {
+            const float2 t = ffma2(make_float2(__uint_as_float(sv[q >> 5][q & 31]),
+                                               __uint_as_float(sv[q >> 5][(q & 31) + 1])),
+                                   sc2, *reinterpret_cast<const float2*>(nl + q));
+            p[q] = ((vis >> q) & 1ull) ? ex2(t.x) : 0.f;
+            p[q + 1] = ((vis >> (q + 1)) & 1ull) ? ex2(t.y) : 0.f;
+          }
         }
       }
 #pragma unroll
@@ -851,12 +886,15 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         tmem_ld32(R + 64, dpv[0]);
         tmem_ld32(R + 96, dpv[1]);
         tmem_ld_wait();
+        const float2 iv2 = make_float2(P.inv_sqrt_d, P.inv_sqrt_d);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 32; ++c) {  // packed f32x2 FMA / MUL: the same IEEE results per lane
           const int q = 2 * c;
-          const float d0 = p[q] * fmaf(__uint_as_float(dpv[q >> 5][q & 31]), P.inv_sqrt_d, nd[q]);
-          const float d1 = p[q + 1] * fmaf(__uint_as_float(dpv[(q + 1) >> 5][(q + 1) & 31]), P.inv_sqrt_d, nd[q + 1]);
-          dk[c] = pack_bf16x2(d0, d1);
+          const float2 u = ffma2(make_float2(__uint_as_float(dpv[q >> 5][q & 31]),
+                                             __uint_as_float(dpv[q >> 5][(q & 31) + 1])),
+                                 iv2, *reinterpret_cast<const float2*>(nd + q));
+          const float2 d = fmul2(make_float2(p[q], p[q + 1]), u);
+          dk[c] = pack_bf16x2(d.x, d.y);
         }
       }
       ++dpu;
