@@ -19,11 +19,12 @@
 //               (the paper's "backward for all vertical lines").
 // Per chunk (M = 128 keys, N = 64 queries), in the TMEM region of the softmax
 // warpgroup that owns the chunk:
-//   S^T = K Q^T, dP^T = V dO^T              (tcgen05, SMEM x SMEM -> TMEM)
-//   P^T, dS^T (bf16, dS pre-scaled by 1/sqrt d) in registers -> tcgen05.st back
-//     over S^T (A operands of the next two MMAs); dS^T also -> SMEM
-//   dV += P^T dO, dK += dS^T Q              (A from TMEM, N = 128)
-//   dQ^T = K^T dS^T                          (TMEM over dP^T, M = d) -> bulk reduce-add
+//   S^T = K Q^T, then dP^T = V dO^T         (tcgen05, SMEM x SMEM -> TMEM; separate commits)
+//   P^T from S^T while dP^T runs, then dS^T (bf16, dS pre-scaled by 1/sqrt d), both
+//     tcgen05.st back over S^T (A operands of dV, dK); dS^T also -> SMEM
+//   dQ^T = K^T dS^T                          (TMEM over dP^T, M = d; live 64-key slots only)
+//     committed on its own: the warpgroup drains it (bulk reduce-add) while
+//   dV += P^T dO, dK += dS^T Q              (A from TMEM, N = 128) run
 // Keeping P^T/dS^T in TMEM saves 48 KB of shared-memory traffic per chunk: the
 // SMEM x SMEM N = 64 MMAs are shared-memory-bandwidth bound (51 instead of 32
 // cycles per MMA, tools/mma_bench.cu), so SMEM bytes are this kernel's currency.
