@@ -834,19 +834,19 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
         }
         if (lv == ~0u && m != -INFINITY) {
           // every key live (the common case): FFMA + MUFU + max + add per key
-          float la = 0.f, lb2 = 0.f;
+          // packed f32x2 FMA / ADD (FFMA2 / FADD2): the same IEEE results as the scalar pairs
+          float2 ls = make_float2(0.f, 0.f);
+          const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m, -m);
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 2) {
-            const float t0 = fmaf(__uint_as_float(sv[cc]), sc, -m);
-            const float t1 = fmaf(__uint_as_float(sv[cc + 1]), sc, -m);
-            const float p0 = ex2(t0);
-            const float p1 = (cc & 2) ? ex2_poly(t1) : ex2(t1);
-            emax = fmaxf(emax, fmaxf(t0, t1));
-            la += p0;
-            lb2 += p1;
+            const float2 t = ffma2(make_float2(__uint_as_float(sv[cc]), __uint_as_float(sv[cc + 1])), sc2, nm2);
+            const float p0 = ex2(t.x);
+            const float p1 = (cc & 2) ? ex2_poly(t.y) : ex2(t.y);
+            emax = fmaxf(emax, fmaxf(t.x, t.y));
+            ls = fadd2(ls, make_float2(p0, p1));
             pk[cc >> 1] = pack_bf16x2(p0, p1);
           }
-          l += la + lb2;
+          l += ls.x + ls.y;
         } else if (lv == 0u || m == -INFINITY) {
 #pragma unroll
           for (int cc = 0; cc < 16; ++cc) pk[cc] = 0u;
