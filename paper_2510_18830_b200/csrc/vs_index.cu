@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "f32x2.cuh"
 #include "plan.cuh"
 #include "rope.cuh"
 #include "vsidx.cuh"
@@ -110,7 +111,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
                                                              float* M,
                                                              const __grid_constant__ RopeArgs ra,
                                                              __nv_bfloat16* k_out) {
-  __shared__ __align__(16) float qs[64][128];
+  // window queries as row pairs: qs2[i / 2][c][i % 2], so one 16-byte load gives rows (i, i + 1)
+  // at columns c and c + 1 for two packed f32x2 FMAs (FFMA2: per lane the same IEEE fma)
+  __shared__ __align__(16) float qs2[32][128][2];
   __shared__ float wmax[kThreads / 32][64];
   extern __shared__ __align__(16) uint4 krot[];  // kRope: [16][kThreads] rotated rows
   const int h = blockIdx.y;
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
   const int rlo = blockIdx.z * (64 / gridDim.z), rhi = rlo + 64 / gridDim.z;
   for (int e = threadIdx.x + rlo * 128; e < rhi * 128; e += kThreads) {
     const int i = e >> 7, c = e & 127;
-    qs[i][c] = __bfloat162float(qwin[((size_t)i * g.Hq + h) * 128 + c]);
+    qs2[i >> 1][c][i & 1] = __bfloat162float(qwin[((size_t)i * g.Hq + h) * 128 + c]);
   }
   __syncthreads();
   const int64_t m = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -159,9 +162,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll 1
   for (int i0 = rlo; i0 < rhi; i0 += kRows) {
-    float acc[kRows];
+    float2 acc2[kRows / 2];  // rows (i0 + 2 rp, i0 + 2 rp + 1)
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) acc[r] = 0.f;
+    for (int rp = 0; rp < kRows / 2; ++rp) acc2[rp] = make_float2(0.f, 0.f);
 #pragma unroll 1
     for (int cb = 0; cb < 128; cb += kKB) {
       float kf[kKB];
@@ -180,14 +183,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
         }
       }
 #pragma unroll
-      for (int c = 0; c < kKB; c += 4) {
+      for (int c = 0; c < kKB; c += 2) {
+        const float2 k0 = make_float2(kf[c], kf[c]), k1 = make_float2(kf[c + 1], kf[c + 1]);
 #pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-          const float4 qv = *reinterpret_cast<const float4*>(&qs[i0 + r][cb + c]);
-          acc[r] = __fmaf_rn(qv.x, kf[c], acc[r]);
-          acc[r] = __fmaf_rn(qv.y, kf[c + 1], acc[r]);
-          acc[r] = __fmaf_rn(qv.z, kf[c + 2], acc[r]);
-          acc[r] = __fmaf_rn(qv.w, kf[c + 3], acc[r]);
+        for (int rp = 0; rp < kRows / 2; ++rp) {
+          const float4 qv = *reinterpret_cast<const float4*>(&qs2[(i0 >> 1) + rp][cb + c][0]);
+          acc2[rp] = ffma2(make_float2(qv.x, qv.y), k0, acc2[rp]);  // I1's fold, column c
+          acc2[rp] = ffma2(make_float2(qv.z, qv.w), k1, acc2[rp]);  // then column c + 1
         }
       }
     }
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) stage1_scores(Geo g, con
     for (int r = 0; r < kRows; ++r) {
       const int i = i0 + r;
       const bool causal = mg <= n0 + i;
-      const float tv = causal ? acc[r] : -INFINITY;
+      const float tv = causal ? ((r & 1) ? acc2[r >> 1].y : acc2[r >> 1].x) : -INFINITY;
       if (in) th[(size_t)i * g.S_loc + m] = tv;
       float mx = tv;
 #pragma unroll
