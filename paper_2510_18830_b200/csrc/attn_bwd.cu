@@ -134,7 +134,9 @@ struct Params {
   int static_tiles;         // 1: round-robin tiles instead (A/B switch, MT_BWD_STATIC=1)
   int bar_parts;            // BAR: query-range parts per column group
   int bar_part_len;         // BAR: query blocks per part
-  int dbg;                  // profiling knock-outs (MT_BWD_DBG): bit0 skip dQ reduce-adds
+  int dbg;                  // A/B and profiling switches (MT_BWD_DBG): bit0 skip dQ reduce-adds
+                            // (timing only), bit2 per-element dQ red.add, bit5 scalar BAR dK/dV
+                            // red.add, bit6 no dead-slot softmax skip, bit7 no dQ^T slot skip
   int hpt;                  // BLOCK: q heads per tile (of one kv head; their dK/dV sum stays in
                             // TMEM, so the tile's K/V load and dK/dV epilogue are shared)
 };
