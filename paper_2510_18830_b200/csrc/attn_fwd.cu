@@ -53,6 +53,9 @@ namespace fwd {
 #define MT_FWD_VST 3
 #endif
 constexpr int kKSt = MT_FWD_KST, kVSt = MT_FWD_VST;
+#ifndef MT_FWD_POLY
+#define MT_FWD_POLY 0  // 1: a quarter of the all-live exponentials by the FMA-pipe cubic (A/B)
+#endif
 constexpr int kThreads = 384;  // warpgroup 0: producers, MMA, gatherer; warpgroups 1-2: softmax
 constexpr int kSoftmax = 256;
 constexpr uint32_t kTileKV = 128 * 128 * 2;  // 32 KB
@@ -840,8 +843,13 @@ __device__ void softmax_epilogue(Smem& sm, const Params& P, uint32_t tmem) {
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 2) {
             const float2 t = ffma2(make_float2(__uint_as_float(sv[cc]), __uint_as_float(sv[cc + 1])), sc2, nm2);
+#if MT_FWD_POLY == 0
+            const float p0 = ex2(t.x);
+            const float p1 = ex2(t.y);
+#else
             const float p0 = ex2(t.x);
             const float p1 = (cc & 2) ? ex2_poly(t.y) : ex2(t.y);
+#endif
             emax = fmaxf(emax, fmaxf(t.x, t.y));
             ls = fadd2(ls, make_float2(p0, p1));
             pk[cc >> 1] = pack_bf16x2(p0, p1);
