@@ -808,14 +808,12 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
         }
         vis = live ? ~0ull : 0ull;
       }
-      // per-query constants of the chunk, once: -LSE log2(e) and -D / sqrt(d)
-      float* nl = sm.lse[cm.stage];
-      float* nd = sm.dd[cm.stage];
-      if (row < 64)
-        nl[row] = -nl[row] * 1.4426950408889634f;
-      else
-        nd[row - 64] = -nd[row - 64] * P.inv_sqrt_d;
-      named_bar_sync(wg_bar, 128);
+      // per-query constants of the chunk, scaled in registers as they are used (no barrier):
+      // -LSE log2(e) and -D / sqrt(d), the same products as a pre-scaled copy
+      const float* nl = sm.lse[cm.stage];
+      const float* nd = sm.dd[cm.stage];
+      const float2 nlog2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
+      const float2 nisd = make_float2(-P.inv_sqrt_d, -P.inv_sqrt_d);
       // a key row no query of the chunk sees contributes P = dS = 0.  In BLOCK mode a dead
       // 64-key slot is two whole warps (slot = row / 64): they skip the TMEM loads and the
       // exponentials (0.43 of the slot-rows of the 512K bench index) and
@@ -839,7 +837,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
           for (int q = 0; q < 64; q += 2) {
             const float2 t = ffma2(make_float2(__uint_as_float(sv[q >> 5][q & 31]),
                                                __uint_as_float(sv[q >> 5][(q & 31) + 1])),
-                                   sc2, *reinterpret_cast<const float2*>(nl + q));
+                                   sc2, fmul2(*reinterpret_cast<const float2*>(nl + q), nlog2e));
             p[q] = ex2(t.x);
             p[q + 1] = ex2(t.y);
           }
@@ -848,7 +846,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
           for (int q = 0; q < 64; q += 2) {
             const float2 t = ffma2(make_float2(__uint_as_float(sv[q >> 5][q & 31]),
                                                __uint_as_float(sv[q >> 5][(q & 31) + 1])),
-                                   sc2, *reinterpret_cast<const float2*>(nl + q));
+                                   sc2, fmul2(*reinterpret_cast<const float2*>(nl + q), nlog2e));
             p[q] = ((vis >> q) & 1ull) ? ex2(t.x) : 0.f;
             p[q + 1] = ((vis >> (q + 1)) & 1ull) ? ex2(t.y) : 0.f;
           }
@@ -875,7 +873,7 @@ __device__ void softmax_bwd(Smem& sm, const Params& P, uint32_t tmem, const CUte
           const int q = 2 * c;
           const float2 u = ffma2(make_float2(__uint_as_float(dpv[q >> 5][q & 31]),
                                              __uint_as_float(dpv[q >> 5][(q & 31) + 1])),
-                                 iv2, *reinterpret_cast<const float2*>(nd + q));
+                                 iv2, fmul2(*reinterpret_cast<const float2*>(nd + q), nisd));
           const float2 d = fmul2(make_float2(p[q], p[q + 1]), u);
           dk[c] = pack_bf16x2(d.x, d.y);
         }
